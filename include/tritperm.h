@@ -1,0 +1,143 @@
+/*
+ * tritperm.h -- C ABI of the B200-native Gray-code Ryser permanent mod 3.
+ *
+ * Library: paper_2407_20205_b200/lib/libtritperm_b200.so (sm_100a kernels,
+ * static cudart).  Plain pointers and sizes only; no torch types.
+ *
+ * Each entry point replaces one native (numba) dispatcher of the reference
+ * package tritperm (/root/reference/pkg/src/tritperm, cited src/<file>:<line>):
+ *
+ *   tp_range_sum        <- _kernels.chunk_sum        src/_kernels.py:90-128
+ *                          (called at src/permanent.py:194,248,251)
+ *   tp_range_sum_multi  <- the ThreadPool fan-out of perm_mod3_parallel
+ *                          src/permanent.py:232-255 (one range per device)
+ *   tp_mc_zero_count    <- _kernels.mc_zero_count    src/_kernels.py:245-255
+ *                          (called at src/experiments.py:180,183,186)
+ *   tp_mc_sample_entries<- _kernels.mc_sample_entries src/_kernels.py:258-272
+ *                          (called at tests/test_rng.py:53)
+ *   tp_perm_batch       <- new: per-matrix perm mod 3 + histogram for a batch
+ *                          (the per-trial loop of mc_zero_count,
+ *                          src/_kernels.py:251-254, over caller matrices)
+ *
+ * Conventions (identical to the reference):
+ *   - packed planes: mags[t], sgns[t] are row t of the matrix; column k is bit
+ *     n-1-k (src/core_f3.py:14-16, src/permanent.py:94-100);
+ *   - steps are Gray-code steps i; step i visits subset gray(i)=i^(i>>1) and
+ *     carries sign (-1)^(popcount(sgn)+i) when every column is nonzero
+ *     (src/_kernels.py:111-127).  Step 0 (empty subset) contributes 0;
+ *   - partial sum over [lo,hi) = plus - minus, bit-equal to chunk_sum;
+ *   - perm mod 3 = cmod3((-1)^n * (plus - minus))  (src/permanent.py:116-119);
+ *     classes are {0,1,2} with 2 == -1.
+ *
+ * Errors: every function returns 0 on success and a negative TP_E* code on
+ * failure; tp_last_error() returns a thread-local message.  Validation that
+ * the reference does in Python (ValueError) is repeated here so a caller that
+ * skips the Python layer still gets a clean error instead of a fault.
+ * Calls are synchronous unless named *_async; the library owns one stream and
+ * a cached workspace per device and serialises calls per device.
+ */
+#ifndef TRITPERM_H
+#define TRITPERM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TP_OK 0
+#define TP_E_INVALID (-1)   /* bad argument (maps to ValueError)            */
+#define TP_E_CUDA (-2)      /* CUDA runtime error (maps to RuntimeError)     */
+#define TP_E_NODEV (-3)     /* no usable sm_100 device                       */
+
+#define TP_MAX_N 64
+
+/* ABI version (major*100 + minor). */
+int tp_version(void);
+
+/* Thread-local message for the last failing call on this thread. */
+const char *tp_last_error(void);
+
+/* Number of visible CUDA devices that can run the sm_100a kernels. */
+int tp_device_count(int *count);
+
+/* SM count, max SM clock (kHz) and compute capability of `device`. */
+int tp_device_info(int device, int *sm_count, int *max_clock_khz, int *cc_major, int *cc_minor);
+
+/* Partial Ryser sum over steps [lo, hi) of one matrix given as reference
+ * planes (n <= 63, 0 <= lo <= hi <= 2^n).  Replaces _kernels.chunk_sum
+ * (src/_kernels.py:90-128): *plus - *minus == chunk_sum(mags,sgns,n,lo,hi). */
+int tp_range_sum(const uint64_t *mags, const uint64_t *sgns, int n,
+                 uint64_t lo, uint64_t hi, int device,
+                 uint64_t *plus, uint64_t *minus);
+
+/* Same, asynchronous: the counters {plus, minus} are ADDED into the device
+ * buffer d_pm[2] on `stream` (a cudaStream_t; NULL = the library stream of
+ * `device`).  Used by the one-process-per-GPU path, which all-reduces d_pm
+ * with NCCL. */
+int tp_range_sum_async(const uint64_t *mags, const uint64_t *sgns, int n,
+                       uint64_t lo, uint64_t hi, int device,
+                       uint64_t *d_pm, void *stream);
+
+/* [lo, hi) split into ndev contiguous parts (split_steps rule,
+ * src/permanent.py:221-229), one per listed device, run concurrently from one
+ * host thread, counters summed on the host.  Result is invariant to ndev. */
+int tp_range_sum_multi(const uint64_t *mags, const uint64_t *sgns, int n,
+                       uint64_t lo, uint64_t hi, const int *devices, int ndev,
+                       uint64_t *plus, uint64_t *minus);
+
+/* Batch of B matrices, uint8 entries [B][n][n] (host memory; values reduced
+ * mod 3, so {0,1,2} classes or any non-negative integers), 1 <= n <= 64.
+ * Outputs (each may be NULL): out_class[B] in {0,1,2}, out_partial[B] raw
+ * partial sums over [1,2^n) (n <= 62), hist[3] counts of each class. */
+int tp_perm_batch(const uint8_t *entries, int64_t B, int n, int device,
+                  int8_t *out_class, int64_t *out_partial, int64_t *hist);
+
+/* Device-pointer variant, asynchronous on `stream` (NULL = library stream).
+ * d_entries: device uint8 [B][n][n].  d_class (int8[B]), d_pm (uint64[B][2]
+ * plus/minus) and d_hist (int64[3]) are device buffers, each may be NULL;
+ * d_hist is accumulated into (caller zeroes it).  Returns the number of
+ * kernel launches issued in *launches (may be NULL). */
+int tp_perm_batch_async(const uint8_t *d_entries, int64_t B, int n, int device,
+                        int8_t *d_class, uint64_t *d_pm, int64_t *d_hist,
+                        void *stream, int *launches);
+
+/* Monte Carlo tally over trials [t0, t1) with the reference's per-trial
+ * splitmix64 streams (src/rng.py, src/_kernels.py:212-242), sampled on the
+ * device.  *zeros == mc_zero_count(n, t0, t1, seed); hist[3] (may be NULL)
+ * gets the per-class counts.  1 <= n <= 64. */
+int tp_mc_zero_count(int n, int64_t t0, int64_t t1, uint64_t seed, int device,
+                     int64_t *zeros, int64_t *hist);
+
+/* Per-trial classes for trials [t0,t0+count) into host out_class[count]. */
+int tp_mc_classes(int n, int64_t t0, int64_t count, uint64_t seed, int device,
+                  int8_t *out_class);
+
+/* uint8 classes {0,1,2} (2 == -1) of trials [t0, t0+count), row-major
+ * [count][n][n], sampled on the device with the reference stream
+ * (src/rng.py:68-71 sample_square).  out is host memory, or device memory
+ * when out_on_device != 0 (then the call is asynchronous on `stream`). */
+int tp_sample_classes(int n, int64_t t0, int64_t count, uint64_t seed, int device,
+                      uint8_t *out, int out_on_device, void *stream);
+
+/* Centred entries {-1,0,1} (row-major, n*n) of one trial, sampled on the
+ * device (audit hook; replaces _kernels.mc_sample_entries). */
+int tp_mc_sample_entries(int n, int64_t trial, uint64_t seed, int device,
+                         int8_t *out);
+
+/* Device self-test of the packed primitives on 32-bit words, evaluated with
+ * the same lop3 sequences the walk kernels use:
+ *   op 0 = add_reps formula   (src/core_f3.py:123-131, bit-exact incl. the
+ *          sign bit of zero results, i.e. ADD_TABLE_ROWS),
+ *   op 1 = sub_reps formula   (src/core_f3.py:134-138; the walk's step),
+ *   op 2 = walk ADD = sub_reps of the negated row (m2, m2^s2); equal to
+ *          add_reps on every decoded trit, may differ on zero-sign bits.
+ * in[k*4+{0,1,2,3}] = mag1,sgn1,mag2,sgn2; out[k*2+{0,1}] = mag,sgn of the
+ * result (standard encoding). */
+int tp_selftest_ops(const uint32_t *in, int count, int op, int device, uint32_t *out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TRITPERM_H */

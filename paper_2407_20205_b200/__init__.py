@@ -1,0 +1,69 @@
+"""B200-native Gray-code Ryser permanent mod 3 (arXiv 2407.20205).
+
+Drop-in for the hot path of the reference package ``tritperm``: the same
+entry-point names and signatures (``MatrixF3``, ``perm_chunk``,
+``perm_mod3_fast``, ``perm_mod3_parallel``, ``split_steps``,
+``resolve_jobs``, ``montecarlo_zero``, ``sample_trial_matrix``, ...), with
+the traversal in hand-written sm_100a CUDA reached through a C ABI
+(include/tritperm.h, lib/libtritperm_b200.so).  No CPU fallback.
+"""
+
+from .core_f3 import (
+    PackedF3Vec,
+    add_reps,
+    decode,
+    encode,
+    is_full_magnitude,
+    negate,
+    sign_parity,
+    sub_reps,
+)
+from .experiments import (
+    McHistogram,
+    McResult,
+    montecarlo_hist,
+    montecarlo_zero,
+    sample_trial_matrix,
+    trial_classes,
+)
+from .permanent import (
+    ChunkResult,
+    MatrixF3,
+    cmod3,
+    perm_chunk,
+    perm_mod3_batch,
+    perm_mod3_fast,
+    perm_mod3_parallel,
+    resolve_gpus,
+    resolve_jobs,
+    split_steps,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "ChunkResult",
+    "MatrixF3",
+    "McHistogram",
+    "McResult",
+    "PackedF3Vec",
+    "add_reps",
+    "cmod3",
+    "decode",
+    "encode",
+    "is_full_magnitude",
+    "montecarlo_hist",
+    "montecarlo_zero",
+    "negate",
+    "perm_chunk",
+    "perm_mod3_batch",
+    "perm_mod3_fast",
+    "perm_mod3_parallel",
+    "resolve_gpus",
+    "resolve_jobs",
+    "sample_trial_matrix",
+    "sign_parity",
+    "split_steps",
+    "sub_reps",
+    "trial_classes",
+]

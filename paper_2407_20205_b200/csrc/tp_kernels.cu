@@ -1,0 +1,389 @@
+// tp_kernels.cu -- sm_100a kernels of the Gray-code Ryser permanent mod 3.
+//
+// Work decomposition (north_star): subset S of the rows is written
+// S = (gray(a) << 5) | l, where lane l of a warp owns the low 5 subset bits
+// and the warp walks the "high step" a in Gray order.  All 32 lanes apply the
+// same row at every step (no divergence); only the starting vectors differ.
+// Reference steps [32a, 32b) are exactly the subsets
+// {(gray(h) << 5) | l : h in [a, b), l in [0, 32)}, so partial sums over
+// 32-aligned step ranges are bit-equal to chunk_sum (src/_kernels.py:90-128);
+// lane l at high step a is reference step i = 32a + (ginv5(l) ^ 31*(a&1)),
+// which the generic kernel uses to mask unaligned [lo, hi).
+//
+// Kernels
+//   k_walk_fast<NW,V>   persistent, dynamic work queue over (matrix, chunk)
+//                       items; the walk is unrolled in 2^V-step superblocks
+//                       whose V low rows live in registers; 3*NW LOP3 per
+//                       subset (ALU pipe) + predicated IMADs (FMA pipe).
+//   k_walk_generic<NW>  runtime-row walk with per-lane step masking: small n,
+//                       unaligned range heads/tails, and the fast kernel's
+//                       exact per-block replay logic in scalar form.
+//   k_pack              uint8 [B][n][n] classes -> RowRec [B][64].
+//   k_sample            splitmix64 per-trial sampler -> RowRec (+ entries).
+//   k_finalize          (plus, minus) -> class {0,1,2}, raw partial, histogram.
+//   k_selftest_ops      packed primitives on caller words.
+#include "tp_device.cuh"
+#include "tp_kernels.cuh"
+
+namespace tp {
+
+// ---------------------------------------------------------------------------
+// Exact replay of one superblock from its saved entry state.  Used only when
+// the fast path's event slots cannot represent the block exactly (two events
+// of the same step parity in one lane, or -- for NW=2 -- any primary event).
+// abase is even, so the parity of step abase+j is j&1.
+// ---------------------------------------------------------------------------
+template <int NW>
+__device__ __noinline__ void replay_block(const RowRec* R, uint32_t ze0, uint32_t ze1, uint32_t ge0,
+                                          uint32_t ge1, unsigned long long abase, int len, uint32_t lanepar,
+                                          uint32_t* ev_out, uint32_t* odd_out) {
+  uint32_t z[2] = {ze0, ze1}, g[2] = {ge0, ge1};
+  uint32_t ev = 0, odd = 0;
+  for (int j = 0; j < len; ++j) {
+    if (j > 0) runtime_step<NW>(R, abase + (unsigned long long)j, z, g);
+    if (is_full<NW>(z)) {
+      ev += 1;
+      odd += (sign_parity<NW>(g) ^ (uint32_t)(j & 1) ^ lanepar) & 1u;
+    }
+  }
+  *ev_out = ev;
+  *odd_out = odd;
+}
+
+__device__ __forceinline__ void warp_flush(unsigned long long* pm, uint32_t plus, uint32_t minus, uint32_t lane) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    plus += __shfl_xor_sync(FULL, plus, off);
+    minus += __shfl_xor_sync(FULL, minus, off);
+  }
+  if (lane == 0) {
+    if (plus) atomicAdd(pm, (unsigned long long)plus);
+    if (minus) atomicAdd(pm + 1, (unsigned long long)minus);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fast walk.
+// ---------------------------------------------------------------------------
+template <int NW, int V>
+__global__ void __launch_bounds__(kWalkThreads) k_walk_fast(FastParams p) {
+  __shared__ RowRec srow[kWalkThreads / 32][64];
+  const uint32_t lane = threadIdx.x & 31u;
+  RowRec* R = srow[threadIdx.x >> 5];
+  const uint32_t lanepar = __popc(lane) & 1u;
+  const uint32_t one = p.one;
+
+  for (;;) {
+    unsigned long long item = 0;
+    if (lane == 0) item = atomicAdd(p.queue, 1ull);
+    item = __shfl_sync(FULL, item, 0);
+    if (item >= p.items) break;
+    const unsigned long long b = item / p.chunks;
+    const unsigned long long c = item - b * p.chunks;
+    const unsigned long long A0 = p.F0 + c * p.L;
+    const unsigned long long A1 = (A0 + p.L < p.F1) ? A0 + p.L : p.F1;
+
+    __syncwarp();
+    {
+      const uint4* src = reinterpret_cast<const uint4*>(p.rows + b * 64);
+      uint4* dst = reinterpret_cast<uint4*>(R);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dst[lane + 32 * k] = src[lane + 32 * k];
+    }
+    __syncwarp();
+
+    // Rows 5 .. 5+V-1 flip inside a superblock at compile-time positions.
+    uint32_t SM[V][NW], SS[V][NW], SA[V][NW];
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        SM[v][w] = R[5 + v].m[w];
+        SS[v][w] = R[5 + v].s[w];
+        SA[v][w] = R[5 + v].a[w];
+      }
+
+    uint32_t z[2], g[2];
+    seed_state<NW>(R, p.n, A0, lane, p.z0_init, p.z1_init, z, g);
+
+    uint32_t ev = 0, odd = 0;
+    const unsigned long long Bb = A0 >> V, Be = A1 >> V;
+    for (unsigned long long B = Bb; B < Be; ++B) {
+      if (B != Bb) runtime_step<NW>(R, B << V, z, g);  // superblock entry step
+      const uint32_t ze0 = z[0], ze1 = z[1], ge0 = g[0], ge1 = g[1];
+      uint32_t cnt0 = 0, cnt1 = 0, slot0 = 0, slot1 = 0;
+      if (NW == 1) record_slot(z[0], g[0], cnt0, slot0, one);
+      else record_count(z[0], cnt0, one);
+
+      // Row 5+V-1 flips at j = 2^(V-1); it leaves iff bit V of the step,
+      // i.e. bit 0 of B, is set.
+      uint32_t SX[NW];
+#pragma unroll
+      for (int w = 0; w < NW; ++w) SX[w] = (B & 1ull) ? SS[V - 1][w] : SA[V - 1][w];
+
+#pragma unroll
+      for (int j = 1; j < (1 << V); ++j) {
+        const int t = ctz_c(j);
+        const bool leave = (t + 1 < V) ? (((j >> (t + 1)) & 1) != 0) : false;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          const uint32_t sop = (t == V - 1) ? SX[w] : (leave ? SS[t][w] : SA[t][w]);
+          sub_word(z[w], g[w], SM[t][w], sop);
+        }
+        if (NW == 1) {
+          if (j & 1) record_slot(z[0], g[0], cnt1, slot1, one);
+          else record_slot(z[0], g[0], cnt0, slot0, one);
+        } else {
+          record_count(z[0], cnt0, one);
+        }
+      }
+
+      // Superblock end: fold the events in exactly.
+      if (__any_sync(FULL, (cnt0 | cnt1) != 0)) {
+        uint32_t bev = 0, bodd = 0;
+        bool need_replay;
+        if (NW == 1) {
+          if (cnt0 == 1) { bev += 1; bodd += (__popc(slot0) ^ lanepar) & 1u; }
+          if (cnt1 == 1) { bev += 1; bodd += (__popc(slot1) ^ 1u ^ lanepar) & 1u; }
+          need_replay = __any_sync(FULL, cnt0 > 1 || cnt1 > 1);
+        } else {
+          need_replay = true;
+        }
+        if (need_replay) replay_block<NW>(R, ze0, ze1, ge0, ge1, B << V, 1 << V, lanepar, &bev, &bodd);
+        ev += bev;
+        odd += bodd;
+      }
+    }
+    warp_flush(p.pm + 2 * b, ev - odd, odd, lane);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Generic walk: segments [a0, a1) of high steps with lanes masked to the
+// reference step range [lo, hi).
+// ---------------------------------------------------------------------------
+template <int NW>
+__global__ void __launch_bounds__(kWalkThreads) k_walk_generic(GenericParams p) {
+  __shared__ RowRec srow[kWalkThreads / 32][64];
+  const uint32_t lane = threadIdx.x & 31u;
+  RowRec* R = srow[threadIdx.x >> 5];
+  const uint32_t lanepar = __popc(lane) & 1u;
+  const uint32_t jl = ginv5(lane);
+  const unsigned long long warps = (unsigned long long)gridDim.x * (kWalkThreads / 32);
+  for (unsigned long long item = blockIdx.x * (kWalkThreads / 32) + (threadIdx.x >> 5); item < p.items;
+       item += warps) {
+    const unsigned long long b = item / p.nseg;
+    const int sgi = (int)(item - b * p.nseg);
+    unsigned long long a0 = p.seg_a0[0], a1 = p.seg_a1[0];
+#pragma unroll
+    for (int q = 1; q < kMaxSeg; ++q)
+      if (sgi == q) { a0 = p.seg_a0[q]; a1 = p.seg_a1[q]; }
+    __syncwarp();
+    {
+      const uint4* src = reinterpret_cast<const uint4*>(p.rows + b * 64);
+      uint4* dst = reinterpret_cast<uint4*>(R);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dst[lane + 32 * k] = src[lane + 32 * k];
+    }
+    __syncwarp();
+    uint32_t z[2], g[2];
+    seed_state<NW>(R, p.n, a0, lane, p.z0_init, p.z1_init, z, g);
+    uint32_t ev = 0, odd = 0;
+    for (unsigned long long a = a0; a < a1; ++a) {
+      if (a != a0) runtime_step<NW>(R, a, z, g);
+      const unsigned long long i = (a << 5) + (jl ^ ((a & 1ull) ? 31u : 0u));
+      if ((!p.masked || (i >= p.lo && i < p.hi)) && is_full<NW>(z)) {
+        ev += 1;
+        odd += (sign_parity<NW>(g) ^ (uint32_t)(a & 1ull) ^ lanepar) & 1u;
+      }
+    }
+    warp_flush(p.pm + 2 * b, ev - odd, odd, lane);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Packing: one warp per matrix; column k of row t -> plane bit n-1-k
+// (src/core_f3.py:14-16), split into two 32-bit words.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void store_row(RowRec* dst, unsigned long long mag, unsigned long long sgn) {
+  RowRec r;
+  r.m[0] = (uint32_t)mag;
+  r.m[1] = (uint32_t)(mag >> 32);
+  r.s[0] = (uint32_t)sgn;
+  r.s[1] = (uint32_t)(sgn >> 32);
+  r.a[0] = r.m[0] ^ r.s[0];
+  r.a[1] = r.m[1] ^ r.s[1];
+  r.pad[0] = 0;
+  r.pad[1] = 0;
+  *dst = r;
+}
+
+__global__ void k_pack(const uint8_t* __restrict__ entries, long long B, int n, RowRec* __restrict__ rows) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long b = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); b < B; b += warps) {
+    const uint8_t* E = entries + b * (long long)n * n;
+    for (int t = 0; t < 64; ++t) {
+      unsigned long long mag = 0, sgn = 0;
+      if (t < n) {
+        uint32_t v0 = lane < (uint32_t)n ? (uint32_t)E[t * n + lane] % 3u : 0u;
+        uint32_t v1 = lane + 32 < (uint32_t)n ? (uint32_t)E[t * n + lane + 32] % 3u : 0u;
+        const unsigned long long m = (unsigned long long)__ballot_sync(FULL, v0 != 0) |
+                                     ((unsigned long long)__ballot_sync(FULL, v1 != 0) << 32);
+        const unsigned long long s = (unsigned long long)__ballot_sync(FULL, v0 == 2) |
+                                     ((unsigned long long)__ballot_sync(FULL, v1 == 2) << 32);
+        mag = __brevll(m) >> (64 - n);
+        sgn = __brevll(s) >> (64 - n);
+      }
+      if (lane == 0) store_row(rows + b * 64 + t, mag, sgn);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Device sampler: the reference's per-trial splitmix64 stream
+// (src/rng.py:25-71, src/_kernels.py:212-242), one thread per trial.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z;
+}
+
+__global__ void k_sample(int n, long long t0, long long count, unsigned long long seed, RowRec* __restrict__ rows,
+                         uint8_t* __restrict__ entries_out) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  const unsigned long long trial = (unsigned long long)(t0 + k);
+  const unsigned long long golden = 0x9E3779B97F4A7C15ull;
+  unsigned long long state = mix64(mix64(seed) ^ ((trial + 1ull) * golden));
+  unsigned long long word = 0;
+  int pairs = 0;
+  RowRec* dst = rows ? rows + k * 64 : nullptr;
+  for (int i = 0; i < n; ++i) {
+    unsigned long long mag = 0, sgn = 0;
+    for (int col = 0; col < n; ++col) {
+      unsigned long long v;
+      for (;;) {
+        if (pairs == 0) {
+          state += golden;
+          word = mix64(state);
+          pairs = 32;
+        }
+        v = word & 3ull;
+        word >>= 2;
+        pairs -= 1;
+        if (v != 3ull) break;
+      }
+      if (v != 0) {
+        const unsigned long long bit = 1ull << (n - 1 - col);
+        mag |= bit;
+        if (v == 2) sgn |= bit;
+      }
+      if (entries_out) entries_out[k * (long long)n * n + i * n + col] = (uint8_t)v;  // class {0,1,2}
+    }
+    if (dst) store_row(dst + i, mag, sgn);
+  }
+  if (dst)
+    for (int i = n; i < 64; ++i) store_row(dst + i, 0, 0);
+}
+
+// ---------------------------------------------------------------------------
+// Finalisation: perm mod 3 = cmod3((-1)^n (plus - minus)) (src/permanent.py:116-119),
+// computed from plus and minus separately so it is exact for every n <= 64.
+// ---------------------------------------------------------------------------
+__global__ void k_finalize(const unsigned long long* __restrict__ pm, long long B, int n, int8_t* __restrict__ cls,
+                           long long* __restrict__ partial, long long* __restrict__ hist) {
+  const long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  int r = -1;
+  if (b < B) {
+    const unsigned long long P = pm[2 * b], M = pm[2 * b + 1];
+    int d = (int)(P % 3ull) - (int)(M % 3ull);
+    if (d < 0) d += 3;
+    if ((n & 1) && d) d = 3 - d;
+    r = d;
+    if (cls) cls[b] = (int8_t)r;
+    if (partial) partial[b] = (long long)(P - M);
+  }
+  if (hist) {
+    const uint32_t lane = threadIdx.x & 31u;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const uint32_t cnt = __popc(__ballot_sync(FULL, r == c));
+      if (lane == 0 && cnt) atomicAdd(reinterpret_cast<unsigned long long*>(hist + c), (unsigned long long)cnt);
+    }
+  }
+}
+
+__global__ void k_selftest_ops(const uint32_t* __restrict__ in, int count, int op, uint32_t* __restrict__ out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  uint32_t mag = in[4 * k], sgn = in[4 * k + 1], m2 = in[4 * k + 2], s2 = in[4 * k + 3];
+  if (op == 0) {
+    add_ref_word(mag, sgn, m2, s2);
+  } else {
+    uint32_t z = ~mag, g = sgn;
+    sub_word(z, g, m2, op == 1 ? s2 : (m2 ^ s2));
+    mag = ~z;
+    sgn = g;
+  }
+  out[2 * k] = mag;
+  out[2 * k + 1] = sgn;
+}
+
+// ---------------------------------------------------------------------------
+// Host-side launch wrappers (called by the runtime in tp_runtime.cu).
+// ---------------------------------------------------------------------------
+template <int NW, int V>
+static const void* fast_fn() {
+  return reinterpret_cast<const void*>(&k_walk_fast<NW, V>);
+}
+
+const void* walk_fast_symbol(int nw) { return nw == 1 ? fast_fn<1, kV1>() : fast_fn<2, kV2>(); }
+const void* walk_generic_symbol(int nw) {
+  return nw == 1 ? reinterpret_cast<const void*>(&k_walk_generic<1>)
+                 : reinterpret_cast<const void*>(&k_walk_generic<2>);
+}
+
+cudaError_t launch_walk_fast(int nw, int grid, const FastParams& p, cudaStream_t st) {
+  if (nw == 1) k_walk_fast<1, kV1><<<grid, kWalkThreads, 0, st>>>(p);
+  else k_walk_fast<2, kV2><<<grid, kWalkThreads, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_walk_generic(int nw, int grid, const GenericParams& p, cudaStream_t st) {
+  if (nw == 1) k_walk_generic<1><<<grid, kWalkThreads, 0, st>>>(p);
+  else k_walk_generic<2><<<grid, kWalkThreads, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack(const uint8_t* entries, long long B, int n, RowRec* rows, int grid, cudaStream_t st) {
+  k_pack<<<grid, 256, 0, st>>>(entries, B, n, rows);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sample(int n, long long t0, long long count, unsigned long long seed, RowRec* rows,
+                          uint8_t* entries_out, cudaStream_t st) {
+  const int threads = 128;
+  const long long grid = (count + threads - 1) / threads;
+  k_sample<<<(unsigned)grid, threads, 0, st>>>(n, t0, count, seed, rows, entries_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const unsigned long long* pm, long long B, int n, int8_t* cls, long long* partial,
+                            long long* hist, cudaStream_t st) {
+  const int threads = 256;
+  const long long grid = (B + threads - 1) / threads;
+  k_finalize<<<(unsigned)grid, threads, 0, st>>>(pm, B, n, cls, partial, hist);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_selftest(const uint32_t* in, int count, int op, uint32_t* out, cudaStream_t st) {
+  k_selftest_ops<<<(count + 127) / 128, 128, 0, st>>>(in, count, op, out);
+  return cudaGetLastError();
+}
+
+}  // namespace tp

@@ -1,0 +1,658 @@
+// tp_runtime.cu -- host runtime and C ABI (include/tritperm.h).
+//
+// The runtime replaces the reference's Python/numba orchestration
+// (src/permanent.py:181-255, src/experiments.py:158-190): it plans a step
+// range into fast (superblock-aligned) and generic (masked) work, owns one
+// stream + a grow-only device workspace per device, launches the sm_100a
+// kernels and folds the per-matrix (plus, minus) counters into classes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/tritperm.h"
+#include "tp_kernels.cuh"
+
+using tp::RowRec;
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+#define TP_CUDA(call)                                                                          \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess) return fail(TP_E_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                                       __FILE__, __LINE__);                                    \
+  } while (0)
+
+struct Device {
+  int id = -1;
+  bool ready = false;
+  int sm_count = 0;
+  int max_clock_khz = 0;
+  int cc_major = 0, cc_minor = 0;
+  int fast_blocks_per_sm[3] = {0, 0, 0};  // indexed by NW
+  int generic_blocks_per_sm[3] = {0, 0, 0};
+  cudaStream_t stream = nullptr;
+  void* ws = nullptr;  // grow-only workspace
+  size_t ws_size = 0;
+  std::mutex mu;
+};
+
+Device g_dev[64];
+std::mutex g_init_mu;
+
+int ensure_device(int dev, Device** out) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    return fail(TP_E_NODEV, "no CUDA device available (%s)", e == cudaSuccess ? "count=0" : cudaGetErrorString(e));
+  if (dev < 0 || dev >= count || dev >= 64) return fail(TP_E_INVALID, "device %d out of range [0,%d)", dev, count);
+  Device& d = g_dev[dev];
+  std::lock_guard<std::mutex> lk(g_init_mu);
+  if (!d.ready) {
+    TP_CUDA(cudaSetDevice(dev));
+    cudaDeviceProp prop;
+    TP_CUDA(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10 || prop.minor != 0)
+      return fail(TP_E_NODEV, "device %d is sm_%d%d; this build carries sm_100a code only", dev, prop.major,
+                  prop.minor);
+    d.id = dev;
+    d.sm_count = prop.multiProcessorCount;
+    TP_CUDA(cudaDeviceGetAttribute(&d.max_clock_khz, cudaDevAttrClockRate, dev));
+    d.cc_major = prop.major;
+    d.cc_minor = prop.minor;
+    for (int nw = 1; nw <= 2; ++nw) {
+      TP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.fast_blocks_per_sm[nw], tp::walk_fast_symbol(nw),
+                                                            tp::kWalkThreads, 0));
+      TP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.generic_blocks_per_sm[nw],
+                                                            tp::walk_generic_symbol(nw), tp::kWalkThreads, 0));
+      if (d.fast_blocks_per_sm[nw] < 1 || d.generic_blocks_per_sm[nw] < 1)
+        return fail(TP_E_CUDA, "walk kernels cannot be resident on device %d", dev);
+    }
+    TP_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+    d.ready = true;
+  }
+  *out = &d;
+  return TP_OK;
+}
+
+// Grow-only workspace.  Caller holds d.mu and has set the device.
+int ensure_ws(Device& d, size_t bytes) {
+  if (d.ws_size >= bytes) return TP_OK;
+  if (d.ws) {
+    TP_CUDA(cudaStreamSynchronize(d.stream));
+    TP_CUDA(cudaFree(d.ws));
+    d.ws = nullptr;
+    d.ws_size = 0;
+  }
+  size_t sz = std::max<size_t>(bytes, 1 << 20);
+  TP_CUDA(cudaMalloc(&d.ws, sz));
+  d.ws_size = sz;
+  return TP_OK;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Workspace carve-up for a batch of B matrices.
+struct Carve {
+  size_t off = 0;
+  template <class T>
+  T* take(char* base, size_t count) {
+    off = align_up(off, 256);
+    T* p = reinterpret_cast<T*>(base ? base + off : nullptr);
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+uint32_t zmask(int bits) {
+  if (bits <= 0) return 0u;
+  if (bits >= 32) return 0xffffffffu;
+  return (1u << bits) - 1u;
+}
+
+// ---------------------------------------------------------------------------
+// Planner: one reference step range [lo, hi) for every matrix of a batch.
+// ---------------------------------------------------------------------------
+struct Plan {
+  int nw = 1;
+  bool fast = false;
+  tp::FastParams fp{};
+  tp::GenericParams gp{};
+  int fast_grid = 0, generic_grid = 0;
+};
+
+// full = true: the whole range [0, 2^n) of every matrix (n <= 64), planned
+// directly in high steps so n = 64 does not overflow; lo/hi are then unused.
+void make_plan(const Device& d, int n, unsigned long long B, unsigned long long lo, unsigned long long hi, bool full,
+               const RowRec* rows, unsigned long long* pm, unsigned long long* queue, Plan& pl) {
+  pl = Plan();
+  pl.nw = n <= 32 ? 1 : 2;
+  const int V = pl.nw == 1 ? tp::kV1 : tp::kV2;
+  const unsigned long long SB = 1ull << V;
+  const uint32_t z0 = zmask(std::min(n, 32)), z1 = zmask(n - 32);
+
+  pl.gp.rows = rows;
+  pl.gp.pm = pm;
+  pl.gp.n = n;
+  pl.gp.z0_init = z0;
+  pl.gp.z1_init = z1;
+  pl.gp.nseg = 0;
+  unsigned long long a_lo, a_hi, A0, A1;
+  if (full) {
+    const unsigned long long H = n >= 5 ? (1ull << (n - 5)) : 1ull;
+    a_lo = A0 = 0;
+    a_hi = A1 = H;
+    pl.gp.lo = 0;
+    pl.gp.hi = n >= 5 ? ~0ull : (1ull << n);  // n < 5: lanes >= 2^n inactive
+    pl.gp.masked = n < 5 ? 1 : 0;
+  } else {
+    if (lo >= hi) return;
+    a_lo = lo >> 5;
+    a_hi = (hi + 31) >> 5;  // high steps touched (hi <= 2^63)
+    A0 = (lo + 31) >> 5;
+    A1 = hi >> 5;  // fully covered high steps [A0, A1)
+    pl.gp.lo = lo;
+    pl.gp.hi = hi;
+    pl.gp.masked = 1;
+  }
+  if (B == 0) return;
+  const unsigned long long F0 = (A0 + SB - 1) / SB * SB, F1 = A1 / SB * SB;
+  const bool fast = (n >= 5 + V) && F0 < F1;
+  auto add_seg = [&](unsigned long long a0, unsigned long long a1) {
+    if (a0 < a1) {
+      pl.gp.seg_a0[pl.gp.nseg] = a0;
+      pl.gp.seg_a1[pl.gp.nseg] = a1;
+      pl.gp.nseg++;
+    }
+  };
+  if (fast) {
+    add_seg(a_lo, F0);
+    add_seg(F1, a_hi);
+    // Chunking: enough items for a few per resident warp, chunks a power of
+    // two multiple of the superblock, capped so per-item counters stay 32-bit.
+    const unsigned long long total = F1 - F0;
+    const unsigned long long warps =
+        (unsigned long long)d.sm_count * d.fast_blocks_per_sm[pl.nw] * (tp::kWalkThreads / 32);
+    const unsigned long long want_items = warps * 8;
+    unsigned long long L = SB;
+    const unsigned long long Lmax = 1ull << 20;
+    while (L < Lmax && (total + 2 * L - 1) / (2 * L) * B >= want_items) L <<= 1;
+    pl.fast = true;
+    pl.fp.rows = rows;
+    pl.fp.pm = pm;
+    pl.fp.queue = queue;
+    pl.fp.F0 = F0;
+    pl.fp.F1 = F1;
+    pl.fp.L = L;
+    pl.fp.chunks = (total + L - 1) / L;
+    pl.fp.items = pl.fp.chunks * B;
+    pl.fp.n = n;
+    pl.fp.z0_init = z0;
+    pl.fp.z1_init = z1;
+    pl.fp.one = 1u;
+    const unsigned long long max_grid = (unsigned long long)d.sm_count * d.fast_blocks_per_sm[pl.nw];
+    const unsigned long long need = (pl.fp.items + 7) / 8;
+    pl.fast_grid = (int)std::max<unsigned long long>(1, std::min(max_grid, need));
+  } else {
+    add_seg(a_lo, a_hi);
+  }
+  pl.gp.items = (unsigned long long)pl.gp.nseg * B;
+  if (pl.gp.items) {
+    const unsigned long long max_grid = (unsigned long long)d.sm_count * d.generic_blocks_per_sm[pl.nw];
+    const unsigned long long need = (pl.gp.items + 7) / 8;
+    pl.generic_grid = (int)std::max<unsigned long long>(1, std::min(max_grid, need));
+  }
+}
+
+// Enqueue the walk of plan `pl`; returns launches in *launches.
+int run_plan(const Plan& pl, cudaStream_t st, int* launches) {
+  int nl = 0;
+  if (pl.fast) {
+    TP_CUDA(cudaMemsetAsync(pl.fp.queue, 0, sizeof(unsigned long long), st));
+    TP_CUDA(tp::launch_walk_fast(pl.nw, pl.fast_grid, pl.fp, st));
+    nl++;
+  }
+  if (pl.gp.items) {
+    TP_CUDA(tp::launch_walk_generic(pl.nw, pl.generic_grid, pl.gp, st));
+    nl++;
+  }
+  if (launches) *launches += nl;
+  return TP_OK;
+}
+
+void planes_to_rows(const uint64_t* mags, const uint64_t* sgns, int n, RowRec* out) {
+  for (int t = 0; t < 64; ++t) {
+    const uint64_t m = t < n ? mags[t] : 0, s = t < n ? sgns[t] : 0;
+    RowRec r;
+    r.m[0] = (uint32_t)m;
+    r.m[1] = (uint32_t)(m >> 32);
+    r.s[0] = (uint32_t)s;
+    r.s[1] = (uint32_t)(s >> 32);
+    r.a[0] = r.m[0] ^ r.s[0];
+    r.a[1] = r.m[1] ^ r.s[1];
+    r.pad[0] = r.pad[1] = 0;
+    out[t] = r;
+  }
+}
+
+int check_planes(const uint64_t* mags, const uint64_t* sgns, int n) {
+  if (!mags || !sgns) return fail(TP_E_INVALID, "mags/sgns must not be NULL");
+  const uint64_t window = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
+  for (int t = 0; t < n; ++t)
+    if ((mags[t] & ~window) || (sgns[t] & ~window))
+      return fail(TP_E_INVALID, "row %d has bits outside the %d-bit window", t, n);
+  return TP_OK;
+}
+
+// Enqueue one range of one matrix on device d (caller holds d.mu, device set).
+// Counters are added into d_pm[0..1].
+int enqueue_range(Device& d, const uint64_t* mags, const uint64_t* sgns, int n, uint64_t lo, uint64_t hi,
+                  unsigned long long* d_pm, cudaStream_t st) {
+  Carve cv;
+  cv.take<RowRec>(nullptr, 64);
+  cv.take<unsigned long long>(nullptr, 1);
+  int rc = ensure_ws(d, cv.off);
+  if (rc) return rc;
+  Carve c2;
+  char* base = static_cast<char*>(d.ws);
+  RowRec* rows = c2.take<RowRec>(base, 64);
+  unsigned long long* queue = c2.take<unsigned long long>(base, 1);
+  RowRec h[64];
+  planes_to_rows(mags, sgns, n, h);
+  TP_CUDA(cudaMemcpyAsync(rows, h, sizeof h, cudaMemcpyHostToDevice, st));
+  Plan pl;
+  make_plan(d, n, 1, lo, hi, false, rows, d_pm, queue, pl);
+  // The H2D above is from pageable memory: it returns once `h` is staged,
+  // so `h` may go out of scope before the stream runs.
+  return run_plan(pl, st, nullptr);
+}
+
+int check_range(int n, uint64_t lo, uint64_t hi) {
+  if (n < 1 || n > 63) return fail(TP_E_INVALID, "range API needs 1 <= n <= 63, got n=%d", n);
+  const uint64_t last = 1ull << n;
+  if (!(lo <= hi && hi <= last))
+    return fail(TP_E_INVALID, "need 0 <= lo <= hi <= 2**n, got lo=%llu hi=%llu n=%d", (unsigned long long)lo,
+                (unsigned long long)hi, n);
+  return TP_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int tp_version(void) { return 100; }
+
+const char* tp_last_error(void) { return g_err; }
+
+int tp_device_count(int* count) {
+  if (!count) return fail(TP_E_INVALID, "count must not be NULL");
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return fail(TP_E_NODEV, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+  }
+  int ok = 0;
+  for (int i = 0; i < c; ++i) {
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, i) == cudaSuccess && p.major == 10 && p.minor == 0) ok++;
+  }
+  *count = ok;
+  return TP_OK;
+}
+
+int tp_device_info(int device, int* sm_count, int* max_clock_khz, int* cc_major, int* cc_minor) {
+  Device* d;
+  int rc = ensure_device(device, &d);
+  if (rc) return rc;
+  if (sm_count) *sm_count = d->sm_count;
+  if (max_clock_khz) *max_clock_khz = d->max_clock_khz;
+  if (cc_major) *cc_major = d->cc_major;
+  if (cc_minor) *cc_minor = d->cc_minor;
+  return TP_OK;
+}
+
+int tp_range_sum(const uint64_t* mags, const uint64_t* sgns, int n, uint64_t lo, uint64_t hi, int device,
+                 uint64_t* plus, uint64_t* minus) {
+  int rc = check_range(n, lo, hi);
+  if (rc) return rc;
+  if ((rc = check_planes(mags, sgns, n))) return rc;
+  if (!plus || !minus) return fail(TP_E_INVALID, "plus/minus must not be NULL");
+  Device* d;
+  if ((rc = ensure_device(device, &d))) return rc;
+  std::lock_guard<std::mutex> lk(d->mu);
+  TP_CUDA(cudaSetDevice(device));
+  Carve cv;
+  cv.take<RowRec>(nullptr, 64);
+  cv.take<unsigned long long>(nullptr, 1);
+  cv.take<unsigned long long>(nullptr, 2);
+  if ((rc = ensure_ws(*d, cv.off))) return rc;
+  char* base = static_cast<char*>(d->ws);
+  Carve c2;
+  c2.take<RowRec>(base, 64);
+  c2.take<unsigned long long>(base, 1);
+  unsigned long long* pm = c2.take<unsigned long long>(base, 2);
+  TP_CUDA(cudaMemsetAsync(pm, 0, 2 * sizeof(unsigned long long), d->stream));
+  if ((rc = enqueue_range(*d, mags, sgns, n, lo, hi, pm, d->stream))) return rc;
+  unsigned long long h[2];
+  TP_CUDA(cudaMemcpyAsync(h, pm, sizeof h, cudaMemcpyDeviceToHost, d->stream));
+  TP_CUDA(cudaStreamSynchronize(d->stream));
+  *plus = h[0];
+  *minus = h[1];
+  return TP_OK;
+}
+
+int tp_range_sum_async(const uint64_t* mags, const uint64_t* sgns, int n, uint64_t lo, uint64_t hi, int device,
+                       uint64_t* d_pm, void* stream) {
+  int rc = check_range(n, lo, hi);
+  if (rc) return rc;
+  if ((rc = check_planes(mags, sgns, n))) return rc;
+  if (!d_pm) return fail(TP_E_INVALID, "d_pm must not be NULL");
+  Device* d;
+  if ((rc = ensure_device(device, &d))) return rc;
+  std::lock_guard<std::mutex> lk(d->mu);
+  TP_CUDA(cudaSetDevice(device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d->stream;
+  return enqueue_range(*d, mags, sgns, n, lo, hi, reinterpret_cast<unsigned long long*>(d_pm), st);
+}
+
+int tp_range_sum_multi(const uint64_t* mags, const uint64_t* sgns, int n, uint64_t lo, uint64_t hi,
+                       const int* devices, int ndev, uint64_t* plus, uint64_t* minus) {
+  int rc = check_range(n, lo, hi);
+  if (rc) return rc;
+  if ((rc = check_planes(mags, sgns, n))) return rc;
+  if (!devices || ndev < 1) return fail(TP_E_INVALID, "need at least one device");
+  if (!plus || !minus) return fail(TP_E_INVALID, "plus/minus must not be NULL");
+  for (int k = 0; k < ndev; ++k)
+    for (int q = 0; q < k; ++q)
+      if (devices[q] == devices[k]) return fail(TP_E_INVALID, "device %d listed twice", devices[k]);
+  std::vector<Device*> ds(ndev);
+  for (int k = 0; k < ndev; ++k)
+    if ((rc = ensure_device(devices[k], &ds[k]))) return rc;
+  std::vector<std::unique_lock<std::mutex>> locks;
+  for (int k = 0; k < ndev; ++k) locks.emplace_back(ds[k]->mu);
+  std::vector<unsigned long long*> pms(ndev);
+  std::vector<RowRec> h(64);
+  planes_to_rows(mags, sgns, n, h.data());
+  // Split [lo, hi) like split_steps (src/permanent.py:221-229) and enqueue
+  // every part before waiting on any, so the devices run concurrently.
+  const unsigned long long total = hi - lo;
+  for (int k = 0; k < ndev; ++k) {
+    Device& d = *ds[k];
+    TP_CUDA(cudaSetDevice(d.id));
+    Carve cv;
+    cv.take<RowRec>(nullptr, 64);
+    cv.take<unsigned long long>(nullptr, 1);
+    cv.take<unsigned long long>(nullptr, 2);
+    if ((rc = ensure_ws(d, cv.off))) return rc;
+    char* base = static_cast<char*>(d.ws);
+    Carve c2;
+    RowRec* rows = c2.take<RowRec>(base, 64);
+    unsigned long long* queue = c2.take<unsigned long long>(base, 1);
+    pms[k] = c2.take<unsigned long long>(base, 2);
+    const unsigned long long plo = lo + (unsigned long long)((unsigned __int128)total * k / ndev);
+    const unsigned long long phi = lo + (unsigned long long)((unsigned __int128)total * (k + 1) / ndev);
+    TP_CUDA(cudaMemsetAsync(pms[k], 0, 2 * sizeof(unsigned long long), d.stream));
+    TP_CUDA(cudaMemcpyAsync(rows, h.data(), 64 * sizeof(RowRec), cudaMemcpyHostToDevice, d.stream));
+    Plan pl;
+    make_plan(d, n, 1, plo, phi, false, rows, pms[k], queue, pl);
+    if ((rc = run_plan(pl, d.stream, nullptr))) return rc;
+  }
+  unsigned long long P = 0, M = 0;
+  for (int k = 0; k < ndev; ++k) {
+    Device& d = *ds[k];
+    TP_CUDA(cudaSetDevice(d.id));
+    unsigned long long hp[2];
+    TP_CUDA(cudaMemcpyAsync(hp, pms[k], sizeof hp, cudaMemcpyDeviceToHost, d.stream));
+    TP_CUDA(cudaStreamSynchronize(d.stream));
+    P += hp[0];
+    M += hp[1];
+  }
+  *plus = P;
+  *minus = M;
+  return TP_OK;
+}
+
+int tp_perm_batch_async(const uint8_t* d_entries, int64_t B, int n, int device, int8_t* d_class, uint64_t* d_pm,
+                        int64_t* d_hist, void* stream, int* launches) {
+  if (n < 1 || n > TP_MAX_N) return fail(TP_E_INVALID, "need 1 <= n <= %d, got %d", TP_MAX_N, n);
+  if (B < 0) return fail(TP_E_INVALID, "batch size must be >= 0");
+  if (B > 0 && !d_entries) return fail(TP_E_INVALID, "d_entries must not be NULL");
+  if (launches) *launches = 0;
+  if (B == 0) return TP_OK;
+  Device* d;
+  int rc = ensure_device(device, &d);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(d->mu);
+  TP_CUDA(cudaSetDevice(device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d->stream;
+  Carve cv;
+  cv.take<RowRec>(nullptr, (size_t)B * 64);
+  cv.take<unsigned long long>(nullptr, 1);
+  if (!d_pm) cv.take<unsigned long long>(nullptr, (size_t)B * 2);
+  if ((rc = ensure_ws(*d, cv.off))) return rc;
+  char* base = static_cast<char*>(d->ws);
+  Carve c2;
+  RowRec* rows = c2.take<RowRec>(base, (size_t)B * 64);
+  unsigned long long* queue = c2.take<unsigned long long>(base, 1);
+  unsigned long long* pm =
+      d_pm ? reinterpret_cast<unsigned long long*>(d_pm) : c2.take<unsigned long long>(base, (size_t)B * 2);
+  int nl = 0;
+  TP_CUDA(cudaMemsetAsync(pm, 0, (size_t)B * 2 * sizeof(unsigned long long), st));
+  const int pack_grid = (int)std::min<long long>((B + 7) / 8, (long long)d->sm_count * 8);
+  TP_CUDA(tp::launch_pack(d_entries, B, n, rows, pack_grid, st));
+  nl++;
+  Plan pl;
+  make_plan(*d, n, (unsigned long long)B, 0, 0, true, rows, pm, queue, pl);
+  if ((rc = run_plan(pl, st, &nl))) return rc;
+  if (d_class || d_hist) {
+    TP_CUDA(tp::launch_finalize(pm, B, n, d_class, nullptr, reinterpret_cast<long long*>(d_hist), st));
+    nl++;
+  }
+  if (launches) *launches = nl;
+  return TP_OK;
+}
+
+int tp_perm_batch(const uint8_t* entries, int64_t B, int n, int device, int8_t* out_class, int64_t* out_partial,
+                  int64_t* hist) {
+  if (n < 1 || n > TP_MAX_N) return fail(TP_E_INVALID, "need 1 <= n <= %d, got %d", TP_MAX_N, n);
+  if (B < 0) return fail(TP_E_INVALID, "batch size must be >= 0");
+  if (B > 0 && !entries) return fail(TP_E_INVALID, "entries must not be NULL");
+  if (out_partial && n > 62) return fail(TP_E_INVALID, "raw partial sums only fit int64 for n <= 62");
+  if (hist) hist[0] = hist[1] = hist[2] = 0;
+  if (B == 0) return TP_OK;
+  Device* d;
+  int rc = ensure_device(device, &d);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(d->mu);
+  TP_CUDA(cudaSetDevice(device));
+  cudaStream_t st = d->stream;
+  const size_t ebytes = (size_t)B * n * n;
+  Carve cv;
+  cv.take<RowRec>(nullptr, (size_t)B * 64);
+  cv.take<unsigned long long>(nullptr, 1);
+  cv.take<unsigned long long>(nullptr, (size_t)B * 2);
+  cv.take<uint8_t>(nullptr, ebytes);
+  cv.take<int8_t>(nullptr, (size_t)B);
+  cv.take<long long>(nullptr, (size_t)B);
+  cv.take<long long>(nullptr, 3);
+  if ((rc = ensure_ws(*d, cv.off))) return rc;
+  char* base = static_cast<char*>(d->ws);
+  Carve c2;
+  RowRec* rows = c2.take<RowRec>(base, (size_t)B * 64);
+  unsigned long long* queue = c2.take<unsigned long long>(base, 1);
+  unsigned long long* pm = c2.take<unsigned long long>(base, (size_t)B * 2);
+  uint8_t* dent = c2.take<uint8_t>(base, ebytes);
+  int8_t* dcls = c2.take<int8_t>(base, (size_t)B);
+  long long* dpart = c2.take<long long>(base, (size_t)B);
+  long long* dhist = c2.take<long long>(base, 3);
+  TP_CUDA(cudaMemcpyAsync(dent, entries, ebytes, cudaMemcpyHostToDevice, st));
+  TP_CUDA(cudaMemsetAsync(pm, 0, (size_t)B * 2 * sizeof(unsigned long long), st));
+  TP_CUDA(cudaMemsetAsync(dhist, 0, 3 * sizeof(long long), st));
+  const int pack_grid = (int)std::min<long long>((B + 7) / 8, (long long)d->sm_count * 8);
+  TP_CUDA(tp::launch_pack(dent, B, n, rows, pack_grid, st));
+  Plan pl;
+  make_plan(*d, n, (unsigned long long)B, 0, 0, true, rows, pm, queue, pl);
+  if ((rc = run_plan(pl, st, nullptr))) return rc;
+  TP_CUDA(tp::launch_finalize(pm, B, n, dcls, dpart, dhist, st));
+  if (out_class) TP_CUDA(cudaMemcpyAsync(out_class, dcls, (size_t)B, cudaMemcpyDeviceToHost, st));
+  if (out_partial) TP_CUDA(cudaMemcpyAsync(out_partial, dpart, (size_t)B * 8, cudaMemcpyDeviceToHost, st));
+  long long hh[3];
+  TP_CUDA(cudaMemcpyAsync(hh, dhist, sizeof hh, cudaMemcpyDeviceToHost, st));
+  TP_CUDA(cudaStreamSynchronize(st));
+  if (hist) {
+    hist[0] = hh[0];
+    hist[1] = hh[1];
+    hist[2] = hh[2];
+  }
+  return TP_OK;
+}
+
+// Monte Carlo: device sampler -> walk -> finalize, in slabs so the RowRec
+// workspace stays bounded.
+static int mc_run(int n, int64_t t0, int64_t count, uint64_t seed, int device, int8_t* out_class, int64_t* hist) {
+  if (n < 1 || n > TP_MAX_N) return fail(TP_E_INVALID, "need 1 <= n <= %d, got %d", TP_MAX_N, n);
+  if (t0 < 0 || count < 0) return fail(TP_E_INVALID, "trial range must be non-negative");
+  if (hist) hist[0] = hist[1] = hist[2] = 0;
+  if (count == 0) return TP_OK;
+  Device* d;
+  int rc = ensure_device(device, &d);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(d->mu);
+  TP_CUDA(cudaSetDevice(device));
+  cudaStream_t st = d->stream;
+  const int64_t slab = std::min<int64_t>(count, 1 << 16);
+  Carve cv;
+  cv.take<RowRec>(nullptr, (size_t)slab * 64);
+  cv.take<unsigned long long>(nullptr, 1);
+  cv.take<unsigned long long>(nullptr, (size_t)slab * 2);
+  cv.take<int8_t>(nullptr, (size_t)slab);
+  cv.take<long long>(nullptr, 3);
+  if ((rc = ensure_ws(*d, cv.off))) return rc;
+  char* base = static_cast<char*>(d->ws);
+  Carve c2;
+  RowRec* rows = c2.take<RowRec>(base, (size_t)slab * 64);
+  unsigned long long* queue = c2.take<unsigned long long>(base, 1);
+  unsigned long long* pm = c2.take<unsigned long long>(base, (size_t)slab * 2);
+  int8_t* dcls = c2.take<int8_t>(base, (size_t)slab);
+  long long* dhist = c2.take<long long>(base, 3);
+  TP_CUDA(cudaMemsetAsync(dhist, 0, 3 * sizeof(long long), st));
+  for (int64_t s0 = 0; s0 < count; s0 += slab) {
+    const int64_t B = std::min<int64_t>(slab, count - s0);
+    TP_CUDA(cudaMemsetAsync(pm, 0, (size_t)B * 2 * sizeof(unsigned long long), st));
+    TP_CUDA(tp::launch_sample(n, t0 + s0, B, seed, rows, nullptr, st));
+    Plan pl;
+    make_plan(*d, n, (unsigned long long)B, 0, 0, true, rows, pm, queue, pl);
+    if ((rc = run_plan(pl, st, nullptr))) return rc;
+    TP_CUDA(tp::launch_finalize(pm, B, n, dcls, nullptr, dhist, st));
+    if (out_class) TP_CUDA(cudaMemcpyAsync(out_class + s0, dcls, (size_t)B, cudaMemcpyDeviceToHost, st));
+    if (out_class) TP_CUDA(cudaStreamSynchronize(st));
+  }
+  long long hh[3];
+  TP_CUDA(cudaMemcpyAsync(hh, dhist, sizeof hh, cudaMemcpyDeviceToHost, st));
+  TP_CUDA(cudaStreamSynchronize(st));
+  if (hist) {
+    hist[0] = hh[0];
+    hist[1] = hh[1];
+    hist[2] = hh[2];
+  }
+  return TP_OK;
+}
+
+int tp_mc_zero_count(int n, int64_t t0, int64_t t1, uint64_t seed, int device, int64_t* zeros, int64_t* hist) {
+  if (!zeros) return fail(TP_E_INVALID, "zeros must not be NULL");
+  if (t1 < t0) return fail(TP_E_INVALID, "need t0 <= t1");
+  int64_t h[3];
+  int rc = mc_run(n, t0, t1 - t0, seed, device, nullptr, h);
+  if (rc) return rc;
+  *zeros = h[0];
+  if (hist) {
+    hist[0] = h[0];
+    hist[1] = h[1];
+    hist[2] = h[2];
+  }
+  return TP_OK;
+}
+
+int tp_mc_classes(int n, int64_t t0, int64_t count, uint64_t seed, int device, int8_t* out_class) {
+  if (!out_class && count > 0) return fail(TP_E_INVALID, "out_class must not be NULL");
+  return mc_run(n, t0, count, seed, device, out_class, nullptr);
+}
+
+int tp_sample_classes(int n, int64_t t0, int64_t count, uint64_t seed, int device, uint8_t* out, int out_on_device,
+                      void* stream) {
+  if (n < 1 || n > TP_MAX_N) return fail(TP_E_INVALID, "need 1 <= n <= %d, got %d", TP_MAX_N, n);
+  if (t0 < 0 || count < 0) return fail(TP_E_INVALID, "trial range must be non-negative");
+  if (count > 0 && !out) return fail(TP_E_INVALID, "out must not be NULL");
+  if (count == 0) return TP_OK;
+  Device* d;
+  int rc = ensure_device(device, &d);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(d->mu);
+  TP_CUDA(cudaSetDevice(device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d->stream;
+  if (out_on_device) {
+    TP_CUDA(tp::launch_sample(n, t0, count, seed, nullptr, out, st));
+    return TP_OK;
+  }
+  const size_t bytes = (size_t)count * n * n;
+  if ((rc = ensure_ws(*d, bytes))) return rc;
+  uint8_t* ent = static_cast<uint8_t*>(d->ws);
+  TP_CUDA(tp::launch_sample(n, t0, count, seed, nullptr, ent, st));
+  TP_CUDA(cudaMemcpyAsync(out, ent, bytes, cudaMemcpyDeviceToHost, st));
+  TP_CUDA(cudaStreamSynchronize(st));
+  return TP_OK;
+}
+
+int tp_mc_sample_entries(int n, int64_t trial, uint64_t seed, int device, int8_t* out) {
+  if (!out) return fail(TP_E_INVALID, "out must not be NULL");
+  int rc = tp_sample_classes(n, trial, 1, seed, device, reinterpret_cast<uint8_t*>(out), 0, nullptr);
+  if (rc) return rc;
+  for (int k = 0; k < n * n; ++k)
+    if (out[k] == 2) out[k] = -1;  // centred, as src/_kernels.py:258-272 returns
+  return TP_OK;
+}
+
+int tp_selftest_ops(const uint32_t* in, int count, int op, int device, uint32_t* out) {
+  if (count < 0 || (count > 0 && (!in || !out))) return fail(TP_E_INVALID, "bad buffers");
+  if (op < 0 || op > 2) return fail(TP_E_INVALID, "op must be 0 (add), 1 (sub) or 2 (walk add)");
+  if (count == 0) return TP_OK;
+  Device* d;
+  int rc = ensure_device(device, &d);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(d->mu);
+  TP_CUDA(cudaSetDevice(device));
+  Carve cv;
+  cv.take<uint32_t>(nullptr, (size_t)count * 4);
+  cv.take<uint32_t>(nullptr, (size_t)count * 2);
+  if ((rc = ensure_ws(*d, cv.off))) return rc;
+  char* base = static_cast<char*>(d->ws);
+  Carve c2;
+  uint32_t* din = c2.take<uint32_t>(base, (size_t)count * 4);
+  uint32_t* dout = c2.take<uint32_t>(base, (size_t)count * 2);
+  TP_CUDA(cudaMemcpyAsync(din, in, (size_t)count * 16, cudaMemcpyHostToDevice, d->stream));
+  TP_CUDA(tp::launch_selftest(din, count, op, dout, d->stream));
+  TP_CUDA(cudaMemcpyAsync(out, dout, (size_t)count * 8, cudaMemcpyDeviceToHost, d->stream));
+  TP_CUDA(cudaStreamSynchronize(d->stream));
+  return TP_OK;
+}
+
+}  // extern "C"

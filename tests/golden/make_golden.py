@@ -1,0 +1,204 @@
+"""Generate the golden fixtures in tests/golden/ from the REFERENCE itself.
+
+Run in the build container (where /root/reference exists), never on the GPU
+box:
+
+    NUMBA_CACHE_DIR=/tmp/nb PYTHONDONTWRITEBYTECODE=1 \
+        python tests/golden/make_golden.py [--with-slow]
+
+It imports the reference package (/root/reference/pkg/src/tritperm, numba
+kernels included) and records its outputs on seeded inputs.  The C oracle in
+oracle/ and the CUDA path are both checked against these files; the files
+carry everything the GPU tests need, so nothing reads /root/reference at
+test time.  Matrices are stored as strings of classes '0'/'1'/'2'
+(row-major), 2 == -1.
+
+--with-slow adds the expensive anchors (C2's full montecarlo_zero tally at
+n=24 with 16,384 trials, ~2 min on 8 threads; the n=50 2^30-step window,
+~3 s) and the C3 uniform/sparse subset classes (~1 min).
+"""
+
+from __future__ import annotations
+
+import argparse
+import itertools
+import json
+import os
+import random
+import sys
+import time
+
+REF_SRC = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/nb")
+sys.dont_write_bytecode = True
+sys.path.insert(0, REF_SRC)
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+from tritperm import _kernels as ref_k  # noqa: E402
+from tritperm import core_f3 as ref_f3  # noqa: E402
+from tritperm import experiments as ref_exp  # noqa: E402
+from tritperm import permanent as ref_perm  # noqa: E402
+from tritperm import rng as ref_rng  # noqa: E402
+
+
+def enc(rows) -> str:
+    return "".join(str(int(v) % 3) for row in rows for v in row)
+
+
+def dump(name, obj):
+    path = os.path.join(HERE, name)
+    with open(path, "w") as f:
+        json.dump(obj, f, indent=None, separators=(",", ":"))
+        f.write("\n")
+    print(f"wrote {path} ({os.path.getsize(path)} bytes)")
+
+
+def core_ops():
+    """add/sub on every 1-trit representation pair (tests/test_acceptance.py:74-99)."""
+    rows = []
+    for m1, s1, m2, s2 in itertools.product((0, 1), repeat=4):
+        a = ref_f3.add_reps(ref_f3.PackedF3Vec(1, m1, s1), ref_f3.PackedF3Vec(1, m2, s2))
+        s = ref_f3.sub_reps(ref_f3.PackedF3Vec(1, m1, s1), ref_f3.PackedF3Vec(1, m2, s2))
+        rows.append({"in": [m1, s1, m2, s2], "add": [a.mag, a.sgn], "sub": [s.mag, s.sgn]})
+    # wide random words (32-bit) through the same formulas
+    r = random.Random(7)
+    wide = []
+    for _ in range(64):
+        n = 32
+        v1 = [r.randrange(-1, 2) for _ in range(n)]
+        v2 = [r.randrange(-1, 2) for _ in range(n)]
+        e1, e2 = ref_f3.encode(v1), ref_f3.encode(v2)
+        a = ref_f3.add_reps(e1, e2)
+        s = ref_f3.sub_reps(e1, e2)
+        wide.append({"in": [e1.mag, e1.sgn, e2.mag, e2.sgn], "add": [a.mag, a.sgn], "sub": [s.mag, s.sgn]})
+    e = ref_f3.encode((1, 1, 0, -1))
+    dump("core_ops.json", {"pairs": rows, "wide": wide, "encode_example": {"in": [1, 1, 0, -1],
+                                                                             "mag": e.mag, "sgn": e.sgn}})
+
+
+def rng_vectors():
+    state = 0
+    words = []
+    for _ in range(3):
+        w, state = ref_rng.next_word(state)
+        words.append(w)
+    samples = []
+    for n in (1, 2, 6, 13):
+        for trial in (0, 1, 99, 10**7):
+            for seed in (0, 1, 0xDEADBEEF, (1 << 64) - 1):
+                ent = ref_k.mc_sample_entries(n, trial, np.uint64(seed))
+                samples.append({"n": n, "trial": trial, "seed": seed, "entries": enc([ent.tolist()])})
+    dump("rng.json", {"zero_seed_words": words, "samples": samples})
+
+
+def chunks():
+    """chunk_sum on seeded random matrices and ranges (aligned, unaligned, edge)."""
+    r = random.Random(20261020)
+    cases = []
+    for n in list(range(1, 17)) + [20, 24, 28, 31, 32, 33, 36, 40, 50, 60, 62]:
+        for k in range(6 if n <= 16 else 3):
+            a = [[r.randrange(3) for _ in range(n)] for _ in range(n)]
+            m = ref_perm.MatrixF3(a)
+            mags, sgns = m.planes()
+            last = 1 << n
+            ranges = []
+            if n <= 24:
+                ranges.append((1, last))
+            span = min(last, 1 << 22)
+            for _ in range(4):
+                lo = r.randrange(1, last - span + 2) if last - span >= 1 else 1
+                hi = min(last, lo + r.randrange(0, span + 1))
+                ranges.append((lo, hi))
+            # 32-aligned and superblock-aligned windows
+            if n >= 12:
+                base = r.randrange(0, max(1, (last >> 12) - (1 << 8))) << 12
+                ranges.append((max(1, base), base + (1 << min(n - 1, 17))))
+            out = []
+            for lo, hi in ranges:
+                s = int(ref_k.chunk_sum(mags, sgns, n, lo, hi))
+                out.append([lo, hi, s])
+            cases.append({"n": n, "a": enc(a), "ranges": out})
+    dump("chunks.json", {"cases": cases})
+
+
+def tower():
+    """Oracle tower of tests/test_acceptance.py:102-123 (random.Random(31415))."""
+    rnd = random.Random(31415)
+    out = []
+    for n in range(1, 13):
+        mats = []
+        for _ in range(200):
+            rows = [[rnd.randrange(-1, 2) for _ in range(n)] for _ in range(n)]
+            m = ref_perm.MatrixF3(rows)
+            v = ref_perm.perm_ryser_reference(m)
+            assert v == ref_perm.perm_mod3_fast(m)
+            mats.append([enc(rows), v, ref_perm.perm_chunk(m, 1, 1 << n).partial_sum])
+        out.append({"n": n, "mats": mats})
+    # exhaustive 2x2 and a naive check of 3x3
+    ex2 = []
+    for flat in itertools.product((-1, 0, 1), repeat=4):
+        m = ref_perm.MatrixF3([flat[0:2], flat[2:4]])
+        ex2.append([enc(m.rows), ref_perm.perm_naive(m)])
+    dump("tower.json", {"random": out, "exhaustive2": ex2})
+
+
+def anchors(with_slow: bool):
+    res = {}
+    # config C1-like anchors: n=20, trial 0, seeds 0..3
+    c1 = []
+    for seed in range(4):
+        m = ref_exp.sample_trial_matrix(20, 0, seed)
+        c1.append({"seed": seed, "trial": 0, "n": 20, "a": enc(m.rows),
+                   "class": ref_perm.perm_mod3_fast(m) % 3,
+                   "ryser_class": ref_perm.perm_ryser_reference(m) % 3,
+                   "partial": ref_perm.perm_chunk(m, 1, 1 << 20).partial_sum})
+    res["c1"] = c1
+    mc = []
+    for n, trials, seed in ((1, 3000, 5), (2, 20000, 1), (4, 400, 77), (5, 30000, 123), (6, 100000, 1),
+                            (8, 20000, 3), (12, 2000, 9), (14, 500, 4)):
+        t0 = time.time()
+        r = ref_exp.montecarlo_zero(n, trials, seed=seed, jobs=4)
+        mc.append({"n": n, "trials": trials, "seed": seed, "zero_count": r.zero_count})
+        print(f"mc n={n} trials={trials}: {r.zero_count} ({time.time() - t0:.1f}s)")
+    res["montecarlo"] = mc
+    # known permanents (tests/test_permanent.py:74-78)
+    res["known"] = [["100010001", 1], ["1111", -1], ["0", 0], ["2", -1]]
+    if with_slow:
+        t0 = time.time()
+        r = ref_exp.montecarlo_zero(24, 16384, seed=0, jobs=os.cpu_count())
+        res["c2_zero_count"] = {"n": 24, "trials": 16384, "seed": 0, "zero_count": r.zero_count,
+                                "seconds": round(time.time() - t0, 1)}
+        print("c2 zero count", r.zero_count, time.time() - t0)
+        m = ref_exp.sample_trial_matrix(50, 0, 0)
+        mags, sgns = m.planes()
+        lo = 1 << 40
+        res["c5_window"] = {"n": 50, "seed": 0, "trial": 0, "a": enc(m.rows), "lo": lo, "hi": lo + (1 << 30),
+                            "partial": int(ref_k.chunk_sum(mags, sgns, 50, lo, lo + (1 << 30)))}
+        m36 = ref_exp.sample_trial_matrix(36, 0, 0)
+        mags, sgns = m36.planes()
+        lo = 3 << 33
+        res["c4_window"] = {"n": 36, "seed": 0, "trial": 0, "a": enc(m36.rows), "lo": lo, "hi": lo + (1 << 30),
+                            "partial": int(ref_k.chunk_sum(mags, sgns, 36, lo, lo + (1 << 30)))}
+    dump("anchors.json", res)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--with-slow", action="store_true")
+    ap.add_argument("--only", default=None)
+    args = ap.parse_args()
+    jobs = {"core": core_ops, "rng": rng_vectors, "chunks": chunks, "tower": tower,
+            "anchors": lambda: anchors(args.with_slow)}
+    for name, fn in jobs.items():
+        if args.only and name not in args.only.split(","):
+            continue
+        t0 = time.time()
+        fn()
+        print(f"{name}: {time.time() - t0:.1f}s")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,244 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+golden vectors and the pinned C oracle, bit-exact on raw partial sums,
+classes and histograms."""
+
+import random
+
+import numpy as np
+import pytest
+
+from conftest import centred, dec, load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _rand_matrix(r, n):
+    return np.array([[r.randrange(3) for _ in range(n)] for _ in range(n)], dtype=np.uint8)
+
+
+def test_device_primitives_match_reference_tables(gpu):
+    from paper_2407_20205_b200 import _kernels
+
+    g = load_golden("core_ops.json")
+    rows = g["pairs"] + g["wide"]
+    words = np.array([r["in"] for r in rows], dtype=np.uint32)
+    add = _kernels.selftest_ops(words, 0)
+    sub = _kernels.selftest_ops(words, 1)
+    walk_add = _kernels.selftest_ops(words, 2)
+    for k, r in enumerate(rows):
+        assert add[k].tolist() == r["add"], r  # bit-exact incl. zero-sign bits
+        assert sub[k].tolist() == r["sub"], r
+        # walk ADD (sub of the negated row): same trits, sign bits free on zeros
+        mag = int(walk_add[k, 0])
+        assert mag == r["add"][0]
+        assert (int(walk_add[k, 1]) & mag) == (r["add"][1] & mag)
+
+
+def test_chunk_sum_golden_ranges(gpu):
+    from paper_2407_20205_b200 import _kernels
+
+    for case in load_golden("chunks.json")["cases"]:
+        n = case["n"]
+        m = gpu.MatrixF3(centred(dec(case["a"], n)))
+        mags, sgns = m.planes()
+        for lo, hi, s in case["ranges"]:
+            assert _kernels.chunk_sum(mags, sgns, n, lo, hi) == s, (n, lo, hi)
+            if lo >= 1:
+                assert gpu.perm_chunk(m, lo, hi).partial_sum == s
+
+
+def test_random_ranges_against_oracle(gpu, oracle):
+    r = random.Random(99)
+    for n in list(range(1, 40)) + [44, 50, 57, 62, 63]:
+        a = _rand_matrix(r, n)
+        mags, sgns = oracle.planes_from_classes(a)
+        m = gpu.MatrixF3(centred(a))
+        last = 1 << n
+        for _ in range(5):
+            span = min(last, 1 << r.choice((5, 9, 14, 19)))
+            lo = r.randrange(0, last - span + 1)
+            hi = lo + r.randrange(0, span + 1)
+            lo = max(lo, 1)
+            hi = max(hi, lo)
+            want = oracle.chunk_sum(mags, sgns, n, lo, hi)
+            assert gpu.perm_chunk(m, lo, hi).partial_sum == want, (n, lo, hi)
+
+
+def test_superblock_aligned_windows(gpu, oracle):
+    """Windows that exercise the fast kernel's chunking, replay and entry steps."""
+    r = random.Random(5)
+    for n in (12, 13, 16, 20, 25, 32, 33, 34, 40, 48, 62):
+        a = _rand_matrix(r, n)
+        mags, sgns = oracle.planes_from_classes(a)
+        m = gpu.MatrixF3(centred(a))
+        for shift in (12, 13, 17):
+            if shift > n:
+                continue
+            span = 1 << min(shift + 3, n - 1, 21)
+            base = (r.randrange(0, (1 << n) - span + 1) >> shift) << shift
+            for lo, hi in ((base, base + span), (base + 1, base + span - 1), (base + 31, base + span + 33)):
+                lo, hi = max(lo, 1), min(hi, 1 << n)
+                if lo > hi:
+                    continue
+                assert gpu.perm_chunk(m, lo, hi).partial_sum == oracle.chunk_sum(mags, sgns, n, lo, hi), (n, lo, hi)
+
+
+def test_empty_and_edge_ranges(gpu):
+    m = gpu.MatrixF3([[1, -1, 0], [1, 1, 1], [0, 1, -1]])
+    assert gpu.perm_chunk(m, 5, 5).partial_sum == 0
+    assert gpu.perm_chunk(m, 8, 8).partial_sum == 0
+    full = gpu.perm_chunk(m, 1, 8).partial_sum
+    assert sum(gpu.perm_chunk(m, lo, hi).partial_sum for lo, hi in gpu.split_steps(3, 5)) == full
+
+
+def test_oracle_tower_on_gpu(gpu):
+    g = load_golden("tower.json")
+    for block in g["random"]:
+        n = block["n"]
+        mats = block["mats"]
+        batch = np.stack([dec(s, n) for s, _, _ in mats])
+        cls, part, hist = gpu.perm_mod3_batch(batch)
+        want = np.array([v % 3 for _, v, _ in mats])
+        assert np.array_equal(cls, want)
+        assert np.array_equal(part, np.array([p for _, _, p in mats]))
+        assert hist.tolist() == np.bincount(want, minlength=3).tolist()
+        for s, v, _ in mats[:25]:
+            m = gpu.MatrixF3(centred(dec(s, n)))
+            assert gpu.perm_mod3_fast(m) == v
+            for jobs in (1, 2, 4, 7):
+                assert gpu.perm_mod3_parallel(m, jobs=jobs) == v
+    for s, v in g["exhaustive2"]:
+        assert gpu.perm_mod3_fast(gpu.MatrixF3(centred(dec(s, 2)))) == v
+
+
+def test_known_values(gpu):
+    assert gpu.perm_mod3_fast(gpu.MatrixF3([[1, 0, 0], [0, 1, 0], [0, 0, 1]])) == 1
+    assert gpu.perm_mod3_fast(gpu.MatrixF3([[1, 1], [1, 1]])) == -1
+    assert gpu.perm_mod3_fast(gpu.MatrixF3([[0]])) == 0
+    assert gpu.perm_mod3_fast(gpu.MatrixF3([[-1]])) == -1
+
+
+def test_device_sampler_matches_reference_stream(gpu):
+    from paper_2407_20205_b200 import _kernels, fixtures
+
+    for case in load_golden("rng.json")["samples"]:
+        n = case["n"]
+        want = dec(case["entries"], n)
+        got = _kernels.mc_sample_entries(n, case["trial"], case["seed"]).reshape(n, n)
+        assert np.array_equal(np.mod(got.astype(int), 3), want)
+    batch = _kernels.sample_classes(24, 0, 300, 7)
+    assert np.array_equal(batch, fixtures.uniform_batch(24, 7, 0, 300))
+
+
+def test_montecarlo_matches_reference_tallies(gpu):
+    for case in load_golden("anchors.json")["montecarlo"]:
+        r = gpu.montecarlo_zero(case["n"], case["trials"], seed=case["seed"])
+        assert r.zero_count == case["zero_count"], case
+        assert r.n == case["n"] and r.trials == case["trials"]
+
+
+def test_montecarlo_hist_matches_oracle_classes(gpu, oracle):
+    for n, trials, seed in ((3, 500, 2), (7, 300, 8), (13, 200, 1), (21, 64, 4)):
+        h = gpu.montecarlo_hist(n, trials, seed)
+        cls, _ = oracle.perm_batch(oracle.sample_batch(n, seed, 0, trials), threads=8)
+        assert [h.zeros, h.plus_ones, h.minus_ones] == np.bincount(cls, minlength=3).tolist()
+        per = gpu.trial_classes(n, 0, trials, seed)
+        assert np.array_equal(per, cls)
+
+
+def test_c1_anchors(gpu):
+    for case in load_golden("anchors.json")["c1"]:
+        a = dec(case["a"], 20)
+        m = gpu.MatrixF3(centred(a))
+        assert gpu.perm_chunk(m, 1, 1 << 20).partial_sum == case["partial"]
+        assert gpu.perm_mod3_fast(m) % 3 == case["class"] == case["ryser_class"]
+        cls, part, _ = gpu.perm_mod3_batch(a[None])
+        assert cls[0] == case["class"] and part[0] == case["partial"]
+
+
+def test_c2_batch_full(gpu):
+    """16,384 x 24x24: every class and the histogram, vs the oracle goldens
+    (pinned by the reference's own montecarlo_zero tally)."""
+    g = load_golden("anchors.json")
+    if "c2_classes" not in g:
+        pytest.skip("slow goldens not generated")
+    from paper_2407_20205_b200 import fixtures
+
+    entries = fixtures.uniform_batch(24, 0, 0, 16384)
+    cls, part, hist = gpu.perm_mod3_batch(entries)
+    want = np.frombuffer(g["c2_classes"].encode(), dtype=np.uint8) - ord("0")
+    assert np.array_equal(cls, want)
+    assert hist.tolist() == g["c2_hist"]
+    assert hist[0] == g["c2_zero_count"]["zero_count"]
+    assert part[: len(g["c2_partials_head"])].tolist() == g["c2_partials_head"]
+    assert gpu.montecarlo_zero(24, 16384, seed=0).zero_count == g["c2_zero_count"]["zero_count"]
+
+
+def test_c3_structured(gpu):
+    g = load_golden("anchors.json")
+    from paper_2407_20205_b200 import fixtures
+
+    entries, fam, exp = fixtures.structured_batch(32, 0, 4096)
+    cls, _, hist = gpu.perm_mod3_batch(entries)
+    known = exp >= 0
+    assert np.array_equal(cls[known], exp[known])
+    assert hist.sum() == 4096
+    if "c3_subset" in g:
+        for idx, c in g["c3_subset"]:
+            assert cls[idx] == c, idx
+
+
+def test_c4_c5_windows_and_full(gpu, oracle):
+    g = load_golden("anchors.json")
+    for key in ("c4_window", "c5_window", "c5_window36"):
+        if key not in g:
+            continue
+        w = g[key]
+        m = gpu.MatrixF3(centred(dec(w["a"], w["n"])))
+        assert gpu.perm_chunk(m, w["lo"], w["hi"]).partial_sum == w["partial"], key
+    if "c4_full" in g:
+        w = g["c4_full"]
+        m = gpu.MatrixF3(centred(dec(w["a"], 36)))
+        assert gpu.perm_chunk(m, 1, 1 << 36).partial_sum == w["partial"]
+        assert gpu.perm_mod3_fast(m) % 3 == w["class"]
+        # split invariance at full size (the multi-GPU partition rule)
+        parts = [gpu.perm_chunk(m, lo, hi).partial_sum for lo, hi in gpu.split_steps(36, 8)]
+        assert sum(parts) == w["partial"]
+
+
+def test_batch_async_device_pointers(gpu):
+    import torch
+
+    from paper_2407_20205_b200 import _kernels, fixtures
+
+    e = fixtures.uniform_batch(14, 3, 0, 257)
+    cls_h, part_h, hist_h = gpu.perm_mod3_batch(e)
+    d_e = torch.from_numpy(e).cuda()
+    d_cls = torch.empty(257, dtype=torch.int8, device="cuda")
+    d_pm = torch.empty((257, 2), dtype=torch.int64, device="cuda")
+    d_hist = torch.zeros(3, dtype=torch.int64, device="cuda")
+    st = torch.cuda.current_stream()
+    nl = _kernels.perm_batch_async(d_e.data_ptr(), 257, 14, d_cls.data_ptr(), d_pm.data_ptr(), d_hist.data_ptr(),
+                                   st.cuda_stream)
+    torch.cuda.synchronize()
+    assert nl >= 2
+    assert np.array_equal(d_cls.cpu().numpy(), cls_h)
+    pm = d_pm.cpu().numpy()
+    assert np.array_equal(pm[:, 0] - pm[:, 1], part_h)
+    assert d_hist.cpu().tolist() == hist_h.tolist()
+
+
+def test_abi_rejects_bad_arguments(gpu):
+    from paper_2407_20205_b200 import _kernels
+
+    z = np.zeros(4, dtype=np.uint64)
+    with pytest.raises(ValueError):
+        _kernels.chunk_counts(z, z, 4, 3, 2)
+    with pytest.raises(ValueError):
+        _kernels.chunk_counts(z, z, 4, 0, 17)
+    bad = z.copy()
+    bad[0] = 1 << 5
+    with pytest.raises(ValueError):
+        _kernels.chunk_counts(bad, z, 4, 0, 16)
+    with pytest.raises(ValueError):
+        _kernels.perm_batch(np.zeros((1, 65, 65), dtype=np.uint8))
