@@ -1,0 +1,419 @@
+#!/usr/bin/env python
+"""Benchmark of the Gray-code Ryser permanent mod 3 on B200.
+
+Default workload (N=1) = BASELINE.json configs[1], the config the metric is
+quoted on: a Monte Carlo batch of 16,384 independent 24x24 F3 matrices
+(entries iid uniform {0,1,2}, the reference's own per-trial splitmix64 stream
+with seed 0), each perm mod 3 + the histogram over {0,1,2}.  One step = one
+pass over the batch: pack -> Gray walk -> finalize (+ the histogram
+all-reduce when N > 1).  Metric: Gray-code subset terms/s = 2^n * matrices/s.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c1|c3|c4|c5]
+  python bench.py --impl reference ...   # the reference's CPU path (oracle port)
+
+Under torchrun (N > 1) every rank takes its own 16,384 trials (weak scaling)
+and the 3-bin histogram meets in one NCCL all-reduce per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+WORKLOADS = {
+    # name: (n, batch, description)
+    "c1": (20, 1, "C1: single 20x20 uniform F3 matrix (reference trial stream, seed 0, trial 0)"),
+    "c2": (24, 16384, "C2: Monte Carlo batch, 16384 x 24x24 uniform F3 (reference trial stream, seed 0)"),
+    "c3": (32, 4096, "C3: 4096 x 32x32 structured (uniform|sparse p0=0.8|all-ones|perturbed permutation), seed 0"),
+    "c4": (36, 1, "C4: single 36x36 uniform F3 matrix (seed 0, trial 0), 2^36 subsets"),
+    "c5": (50, 1, "C5: single 50x50 uniform F3 matrix (seed 0, trial 0), 2^50 subsets"),
+}
+SEED = 0
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--c5-log2-steps", type=int, default=44,
+                    help="c5: subset terms per step (a 2^k window of the 2^50 range)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample time")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# inputs
+# ---------------------------------------------------------------------------
+
+def make_entries(workload: str, rank: int):
+    from paper_2407_20205_b200 import fixtures
+
+    n, B, _ = WORKLOADS[workload]
+    if workload == "c3":
+        e, _, _ = fixtures.structured_batch(n, SEED + rank, B)
+        return e
+    return fixtures.uniform_batch(n, SEED, rank * B, B)
+
+
+def terms_per_step(workload: str, args) -> int:
+    n, B, _ = WORKLOADS[workload]
+    if workload == "c5":
+        return 1 << args.c5_log2_steps
+    return B * (1 << n)
+
+
+# ---------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.06)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        loaded = [v for v in sm if v > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference path (oracle port, the reference's chunk_sum restated in C)
+# ---------------------------------------------------------------------------
+
+def cpu_rate(workload: str, target_s: float, threads: int):
+    """(terms/s, sample description, terms, seconds) of the oracle on a bounded sample."""
+    from oracle import oracle
+
+    oracle.build()
+    n, B, _ = WORKLOADS[workload]
+    if workload in ("c2", "c3"):
+        e = make_entries(workload, 0)
+        # calibrate on a few matrices, then size the sample to ~target_s
+        t0 = time.perf_counter()
+        probe = max(1, min(B, threads))
+        oracle.perm_batch(e[:probe], threads=threads)
+        dt = time.perf_counter() - t0
+        count = int(max(probe, min(B, probe * target_s / max(dt, 1e-6))))
+        t0 = time.perf_counter()
+        oracle.perm_batch(e[:count], threads=threads)
+        dt = time.perf_counter() - t0
+        terms = count * (1 << n)
+        return terms / dt, f"first {count} of {B} matrices of the workload, full 2^{n} traversal each", terms, dt
+    a = oracle.sample_classes(n, SEED, 0)
+    mags, sgns = oracle.planes_from_classes(a)
+    lo = 1 if workload in ("c1", "c4") else (1 << 40)
+    span = 1 << 22
+    t0 = time.perf_counter()
+    oracle.chunk_sum_mt(mags, sgns, n, lo, lo + span, threads)
+    dt = time.perf_counter() - t0
+    span = min((1 << n) - lo, max(span, int(span * target_s / max(dt, 1e-6))))
+    span = 1 << max(10, int(math.log2(span)))
+    t0 = time.perf_counter()
+    oracle.chunk_sum_mt(mags, sgns, n, lo, lo + span, threads)
+    dt = time.perf_counter() - t0
+    return span / dt, f"steps [{lo}, {lo}+2^{int(math.log2(span))}) of the matrix, split over {threads} threads", span, dt
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n, B, desc = WORKLOADS[args.workload]
+    per_step = max(1.0, min(6.0, 120.0 / max(1, args.steps + args.warmup)))
+    rates = []
+    sample = None
+    for k in range(args.warmup + args.steps):
+        rate, sample, _, _ = cpu_rate(args.workload, per_step, threads)
+        if k >= args.warmup:
+            rates.append(rate)
+    value = statistics.median(rates)
+    line = {
+        "impl": "reference",
+        "metric": "gray_code_subset_terms_per_s",
+        "value": value,
+        "unit": "terms/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": terms_per_step(args.workload, args) / value * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u32",
+        "data": "synthetic (reference trial stream)",
+        "config": {"workload": desc, "n": n, "batch": B, "seed": SEED},
+        "cpu_baseline": {"value": value, "unit": "terms/s", "cores": threads, "kind": "port",
+                         "sample": f"oracle/oracle.c chunk_sum (restatement of src/_kernels.py:90-128), {sample}"},
+        "e2e": {"value": value, "unit": "terms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+# B200 path
+# ---------------------------------------------------------------------------
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2407_20205_b200 as tp
+    from paper_2407_20205_b200 import _kernels
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    os.environ[_kernels.ENV_DEVICE] = str(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    wl = args.workload
+    n, B, desc = WORKLOADS[wl]
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    launches = 0
+    walk_ms = []
+    step_ms = []
+
+    if wl == "c5" or wl in ("c1", "c4"):
+        # single matrix: the step range is split across ranks (strong scaling)
+        a = make_entries(wl, 0)[0]
+        m = tp.MatrixF3(a.astype(np.int64))
+        mags, sgns = m.planes()
+        span = terms_per_step(wl, args)
+        lo0 = (1 << 40) if wl == "c5" else 0
+        part = (span * rank // world, span * (rank + 1) // world)
+        d_pm = torch.zeros(2, dtype=torch.int64, device=dev)
+
+        def step():
+            nonlocal launches
+            d_pm.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            _kernels.chunk_counts_async(mags, sgns, n, lo0 + part[0], lo0 + part[1], d_pm.data_ptr(), sptr)
+            e1.record(stream)
+            launches += 1 if span >= (1 << 12) else 2
+            if world > 1:
+                dist.all_reduce(d_pm)
+            return e0, e1
+        per_rank_terms = span // world
+        scaling = "strong"
+    else:
+        entries_h = make_entries(wl, rank)
+        d_e = torch.from_numpy(entries_h).to(dev)
+        d_rows = torch.empty((B, _kernels.ROWREC_BYTES), dtype=torch.uint8, device=dev)
+        d_pm = torch.zeros((B, 2), dtype=torch.int64, device=dev)
+        d_cls = torch.empty(B, dtype=torch.int8, device=dev)
+        d_hist = torch.zeros(3, dtype=torch.int64, device=dev)
+
+        def step():
+            nonlocal launches
+            d_pm.zero_()
+            d_hist.zero_()
+            _kernels.pack_async(d_e.data_ptr(), B, n, d_rows.data_ptr(), sptr)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            nl = _kernels.walk_async(d_rows.data_ptr(), B, n, d_pm.data_ptr(), sptr)
+            e1.record(stream)
+            _kernels.finalize_async(d_pm.data_ptr(), B, n, d_cls.data_ptr(), d_hist.data_ptr(), sptr)
+            launches += 2 + nl
+            if world > 1:
+                dist.all_reduce(d_hist)
+            return e0, e1
+        per_rank_terms = B * (1 << n)
+        scaling = "weak"
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches = 0
+
+    # timed region: K steps, L2 flushed (memset of 256 MiB) between steps,
+    # each step bracketed by CUDA events on the launching stream
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        evs = []
+        for _ in range(args.steps):
+            flush.zero_()
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            w = step()
+            s1.record(stream)
+            evs.append((s0, s1, w))
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    for s0, s1, (w0, w1) in evs:
+        step_ms.append(s0.elapsed_time(s1))
+        walk_ms.append(w0.elapsed_time(w1))
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    job_terms = per_rank_terms * world if scaling == "weak" else terms_per_step(wl, args)
+    value = job_terms / (ms_per_step * 1e-3)
+
+    # ALU roofline of the walk kernel: 3 LOP3 per 32 columns per subset term
+    words = 1 if n <= 32 else 2
+    ops_per_term = 3 * words
+    walk_avg = sum(walk_ms) / len(walk_ms)
+    achieved = per_rank_terms * ops_per_term / (walk_avg * 1e-3)
+    peak, _ = _kernels.alu_peak(local)
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "walk_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(wl)
+        except Exception:
+            traffic = None
+
+    # end-to-end through the public API with host buffers (rank-local batch)
+    e2e = None
+    if scaling == "weak":
+        pinned = torch.from_numpy(make_entries(wl, rank)).pin_memory()
+        host = pinned.numpy()
+        tp.perm_mod3_batch(host)  # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        reps = max(3, min(args.steps, 10))
+        for _ in range(reps):
+            cls, part, hist = tp.perm_mod3_batch(host)
+        e2e_s = (time.perf_counter() - t0) / reps
+        if world > 1:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": per_rank_terms * world / e2e_s, "unit": "terms/s",
+               "h2d_bytes_per_step": int(B * n * n),
+               "d2h_bytes_per_step": int(B + B * 8 + 3 * 8),
+               "api": "paper_2407_20205_b200.perm_mod3_batch(pinned uint8 [B,n,n]) -> tp_perm_batch"}
+    else:
+        m_obj = tp.MatrixF3(make_entries(wl, 0)[0].astype(np.int64))
+        lo = (1 << 40) if wl == "c5" else 1
+        span = terms_per_step(wl, args)
+        tp.perm_chunk(m_obj, lo, lo + min(span, 1 << 20))
+        t0 = time.perf_counter()
+        tp.perm_chunk(m_obj, lo, min(lo + span, 1 << n))
+        e2e_s = time.perf_counter() - t0
+        e2e = {"value": span / e2e_s, "unit": "terms/s", "h2d_bytes_per_step": 64 * 32,
+               "d2h_bytes_per_step": 16, "api": "paper_2407_20205_b200.perm_chunk -> tp_range_sum"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        rate, sample, _, _ = cpu_rate(wl, args.cpu_seconds, threads)
+        cpu = {"value": rate, "unit": "terms/s", "cores": threads, "kind": "port",
+               "sample": f"oracle/oracle.c chunk_sum (restatement of src/_kernels.py:90-128), {sample}"}
+
+    csum = clk.summary()
+    if rank == 0:
+        line = {
+            "metric": "gray_code_subset_terms_per_s",
+            "value": value,
+            "unit": "terms/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": scaling,
+            "vs_baseline": None,
+            "dtype": "u32",
+            "data": "synthetic (reference per-trial splitmix64 stream; no dataset involved)",
+            "config": {"workload": desc, "n": n, "batch": B, "seed": SEED, "parallelism": f"dp{world}",
+                       "l2": "flushed between steps (256 MiB memset, untimed by the walk events)",
+                       "terms_per_step": job_terms},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "LOP3 ops/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "k_walk_fast (tp_kernels.cu)",
+                         "ops_per_term": ops_per_term,
+                         "peak_source": "LOP3 chain probe (tp_alu_peak) on this GPU in this run; "
+                                        "nominal 148 SM x 64 lanes x clock",
+                         "walk_ms_avg": walk_avg,
+                         "terms_per_s_walk": per_rank_terms / (walk_avg * 1e-3)},
+            "clocks": csum,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -33,8 +33,11 @@
  * failure; tp_last_error() returns a thread-local message.  Validation that
  * the reference does in Python (ValueError) is repeated here so a caller that
  * skips the Python layer still gets a clean error instead of a fault.
- * Calls are synchronous unless named *_async; the library owns one stream and
- * a cached workspace per device and serialises calls per device.
+ * Calls are synchronous unless named *_async; synchronous calls run on a
+ * library-owned stream and a cached workspace per device and are serialised
+ * per device.  *_async calls enqueue on the caller's `stream` argument, a
+ * cudaStream_t with the usual CUDA meaning (NULL/0 = the legacy default
+ * stream), and return without synchronising.
  */
 #ifndef TRITPERM_H
 #define TRITPERM_H
@@ -72,8 +75,7 @@ int tp_range_sum(const uint64_t *mags, const uint64_t *sgns, int n,
                  uint64_t *plus, uint64_t *minus);
 
 /* Same, asynchronous: the counters {plus, minus} are ADDED into the device
- * buffer d_pm[2] on `stream` (a cudaStream_t; NULL = the library stream of
- * `device`).  Used by the one-process-per-GPU path, which all-reduces d_pm
+ * buffer d_pm[2] on `stream`.  Used by the one-process-per-GPU path, which all-reduces d_pm
  * with NCCL. */
 int tp_range_sum_async(const uint64_t *mags, const uint64_t *sgns, int n,
                        uint64_t lo, uint64_t hi, int device,
@@ -93,7 +95,7 @@ int tp_range_sum_multi(const uint64_t *mags, const uint64_t *sgns, int n,
 int tp_perm_batch(const uint8_t *entries, int64_t B, int n, int device,
                   int8_t *out_class, int64_t *out_partial, int64_t *hist);
 
-/* Device-pointer variant, asynchronous on `stream` (NULL = library stream).
+/* Device-pointer variant, asynchronous on `stream`.
  * d_entries: device uint8 [B][n][n].  d_class (int8[B]), d_pm (uint64[B][2]
  * plus/minus) and d_hist (int64[3]) are device buffers, each may be NULL;
  * d_hist is accumulated into (caller zeroes it).  Returns the number of
@@ -101,6 +103,28 @@ int tp_perm_batch(const uint8_t *entries, int64_t B, int n, int device,
 int tp_perm_batch_async(const uint8_t *d_entries, int64_t B, int n, int device,
                         int8_t *d_class, uint64_t *d_pm, int64_t *d_hist,
                         void *stream, int *launches);
+
+/* The three stages of tp_perm_batch_async as separate calls (for callers
+ * that keep packed rows resident, and for per-stage timing).  All are
+ * asynchronous on `stream`.
+ *   tp_pack_async:     d_entries uint8 [B][n][n] -> d_rows (B * TP_ROWREC_BYTES
+ *                      bytes; the kernels' packed row records, 64 per matrix).
+ *   tp_walk_async:     full Gray walk of every matrix; ADDS (plus, minus) into
+ *                      d_pm uint64 [B][2] (caller zeroes it first).
+ *   tp_finalize_async: d_pm -> d_class int8 [B] (may be NULL), d_hist int64[3]
+ *                      accumulated (may be NULL). */
+#define TP_ROWREC_BYTES 2048
+int tp_pack_async(const uint8_t *d_entries, int64_t B, int n, int device,
+                  void *d_rows, void *stream);
+int tp_walk_async(const void *d_rows, int64_t B, int n, int device,
+                  uint64_t *d_pm, void *stream, int *launches);
+int tp_finalize_async(const uint64_t *d_pm, int64_t B, int n, int device,
+                      int8_t *d_class, int64_t *d_hist, void *stream);
+
+/* Diagnostics: measured LOP3 throughput of `device` (ops/s, the ALU-pipe
+ * roofline denominator) from a register-resident lop3 chain kernel timed
+ * with CUDA events, and the kernel's duration in ms. */
+int tp_alu_peak(int device, double *lop3_ops_per_s, double *ms);
 
 /* Monte Carlo tally over trials [t0, t1) with the reference's per-trial
  * splitmix64 streams (src/rng.py, src/_kernels.py:212-242), sampled on the

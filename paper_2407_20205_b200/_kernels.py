@@ -63,7 +63,16 @@ SIGNATURES = {
                                          ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
     "tp_mc_sample_entries": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int, _i8p]),
     "tp_selftest_ops": (ctypes.c_int, [_u32p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _u32p]),
+    "tp_pack_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                     ctypes.c_void_p]),
+    "tp_walk_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                     ctypes.c_void_p, _ip]),
+    "tp_finalize_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "tp_alu_peak": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
 }
+
+ROWREC_BYTES = 2048  # TP_ROWREC_BYTES: packed row records per matrix
 
 
 class TritpermError(RuntimeError):
@@ -191,6 +200,37 @@ def perm_batch_async(d_entries_ptr: int, B: int, n: int, d_class_ptr: int, d_pm_
                                      ctypes.c_void_p(d_pm_ptr), ctypes.c_void_p(d_hist_ptr),
                                      ctypes.c_void_p(stream_ptr), ctypes.byref(nl)))
     return int(nl.value)
+
+
+def pack_async(d_entries_ptr: int, B: int, n: int, d_rows_ptr: int, stream_ptr: int,
+               device: Optional[int] = None) -> None:
+    dev = default_device() if device is None else device
+    _check(lib().tp_pack_async(ctypes.c_void_p(d_entries_ptr), B, n, dev, ctypes.c_void_p(d_rows_ptr),
+                               ctypes.c_void_p(stream_ptr)))
+
+
+def walk_async(d_rows_ptr: int, B: int, n: int, d_pm_ptr: int, stream_ptr: int, device: Optional[int] = None) -> int:
+    dev = default_device() if device is None else device
+    nl = ctypes.c_int(0)
+    _check(lib().tp_walk_async(ctypes.c_void_p(d_rows_ptr), B, n, dev, ctypes.c_void_p(d_pm_ptr),
+                               ctypes.c_void_p(stream_ptr), ctypes.byref(nl)))
+    return int(nl.value)
+
+
+def finalize_async(d_pm_ptr: int, B: int, n: int, d_class_ptr: int, d_hist_ptr: int, stream_ptr: int,
+                   device: Optional[int] = None) -> None:
+    dev = default_device() if device is None else device
+    _check(lib().tp_finalize_async(ctypes.c_void_p(d_pm_ptr), B, n, dev, ctypes.c_void_p(d_class_ptr),
+                                   ctypes.c_void_p(d_hist_ptr), ctypes.c_void_p(stream_ptr)))
+
+
+def alu_peak(device: Optional[int] = None) -> Tuple[float, float]:
+    """(measured LOP3 ops/s, probe duration ms) of the device."""
+    dev = default_device() if device is None else device
+    ops = ctypes.c_double()
+    ms = ctypes.c_double()
+    _check(lib().tp_alu_peak(dev, ctypes.byref(ops), ctypes.byref(ms)))
+    return float(ops.value), float(ms.value)
 
 
 def mc_zero_count(n: int, t0: int, t1: int, seed: int) -> int:

@@ -33,10 +33,11 @@ namespace tp {
 // of the same step parity in one lane, or -- for NW=2 -- any primary event).
 // abase is even, so the parity of step abase+j is j&1.
 // ---------------------------------------------------------------------------
+// Returns ev | odd << 32.
 template <int NW>
-__device__ __noinline__ void replay_block(const RowRec* R, uint32_t ze0, uint32_t ze1, uint32_t ge0,
-                                          uint32_t ge1, unsigned long long abase, int len, uint32_t lanepar,
-                                          uint32_t* ev_out, uint32_t* odd_out) {
+__device__ __noinline__ unsigned long long replay_block(const RowRec* R, uint32_t ze0, uint32_t ze1, uint32_t ge0,
+                                                        uint32_t ge1, unsigned long long abase, int len,
+                                                        uint32_t lanepar) {
   uint32_t z[2] = {ze0, ze1}, g[2] = {ge0, ge1};
   uint32_t ev = 0, odd = 0;
   for (int j = 0; j < len; ++j) {
@@ -46,8 +47,7 @@ __device__ __noinline__ void replay_block(const RowRec* R, uint32_t ze0, uint32_
       odd += (sign_parity<NW>(g) ^ (uint32_t)(j & 1) ^ lanepar) & 1u;
     }
   }
-  *ev_out = ev;
-  *odd_out = odd;
+  return (unsigned long long)ev | ((unsigned long long)odd << 32);
 }
 
 __device__ __forceinline__ void warp_flush(unsigned long long* pm, uint32_t plus, uint32_t minus, uint32_t lane) {
@@ -149,7 +149,11 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk_fast(FastParams p) {
         } else {
           need_replay = true;
         }
-        if (need_replay) replay_block<NW>(R, ze0, ze1, ge0, ge1, B << V, 1 << V, lanepar, &bev, &bodd);
+        if (need_replay) {
+          const unsigned long long r = replay_block<NW>(R, ze0, ze1, ge0, ge1, B << V, 1 << V, lanepar);
+          bev = (uint32_t)r;
+          bodd = (uint32_t)(r >> 32);
+        }
         ev += bev;
         odd += bodd;
       }
@@ -335,22 +339,77 @@ __global__ void k_selftest_ops(const uint32_t* __restrict__ in, int count, int o
 }
 
 // ---------------------------------------------------------------------------
+// ALU roofline probe: 8 independent lop3 chains per thread, register
+// resident; measures the LOP3 issue rate the walk is bounded by.
+// ---------------------------------------------------------------------------
+constexpr int kPeakInner = 16;
+__global__ void __launch_bounds__(256) k_alu_peak(uint32_t* out, int iters, uint32_t b, uint32_t c) {
+  uint32_t a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = threadIdx.x * 8u + (uint32_t)k + blockIdx.x;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < kPeakInner; ++u)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) TP_LOP3(a[k], a[k], b, c, 0x96);
+  }
+  uint32_t r = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r ^= a[k];
+  if (r == 0x12345678u) out[blockIdx.x] = r;  // keep the chains live
+}
+
+cudaError_t run_alu_peak(int sm_count, uint32_t* scratch, cudaStream_t st, double* ops_per_s, double* ms) {
+  const int grid = sm_count * 8, iters = 2048;
+  cudaEvent_t e0, e1;
+  cudaError_t e;
+  if ((e = cudaEventCreate(&e0)) != cudaSuccess) return e;
+  if ((e = cudaEventCreate(&e1)) != cudaSuccess) return e;
+  k_alu_peak<<<grid, 256, 0, st>>>(scratch, 64, 0x5a5a5a5au, 0x3c3c3c3cu);  // warm-up
+  cudaEventRecord(e0, st);
+  k_alu_peak<<<grid, 256, 0, st>>>(scratch, iters, 0x5a5a5a5au, 0x3c3c3c3cu);
+  cudaEventRecord(e1, st);
+  if ((e = cudaEventSynchronize(e1)) != cudaSuccess) return e;
+  float t = 0;
+  cudaEventElapsedTime(&t, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const double ops = (double)grid * 256 * iters * kPeakInner * 8;
+  *ops_per_s = ops / (t * 1e-3);
+  *ms = t;
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // Host-side launch wrappers (called by the runtime in tp_runtime.cu).
 // ---------------------------------------------------------------------------
+// Fast-walk variants: (words per plane, superblock log2).
 template <int NW, int V>
 static const void* fast_fn() {
   return reinterpret_cast<const void*>(&k_walk_fast<NW, V>);
 }
 
-const void* walk_fast_symbol(int nw) { return nw == 1 ? fast_fn<1, kV1>() : fast_fn<2, kV2>(); }
+const void* walk_fast_symbol(int variant) {
+  switch (variant) {
+    case kFast1V7: return fast_fn<1, 7>();
+    case kFast1V8: return fast_fn<1, 8>();
+    case kFast2V6: return fast_fn<2, 6>();
+    default: return fast_fn<2, 7>();
+  }
+}
+
 const void* walk_generic_symbol(int nw) {
   return nw == 1 ? reinterpret_cast<const void*>(&k_walk_generic<1>)
                  : reinterpret_cast<const void*>(&k_walk_generic<2>);
 }
 
-cudaError_t launch_walk_fast(int nw, int grid, const FastParams& p, cudaStream_t st) {
-  if (nw == 1) k_walk_fast<1, kV1><<<grid, kWalkThreads, 0, st>>>(p);
-  else k_walk_fast<2, kV2><<<grid, kWalkThreads, 0, st>>>(p);
+cudaError_t launch_walk_fast(int variant, int grid, const FastParams& p, cudaStream_t st) {
+  switch (variant) {
+    case kFast1V7: k_walk_fast<1, 7><<<grid, kWalkThreads, 0, st>>>(p); break;
+    case kFast1V8: k_walk_fast<1, 8><<<grid, kWalkThreads, 0, st>>>(p); break;
+    case kFast2V6: k_walk_fast<2, 6><<<grid, kWalkThreads, 0, st>>>(p); break;
+    default: k_walk_fast<2, 7><<<grid, kWalkThreads, 0, st>>>(p); break;
+  }
   return cudaGetLastError();
 }
 

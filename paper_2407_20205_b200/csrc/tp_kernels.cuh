@@ -8,8 +8,10 @@
 namespace tp {
 
 constexpr int kWalkThreads = 256;  // 8 warps per CTA
-constexpr int kV1 = 7;             // superblock = 2^7 high steps for n <= 32
-constexpr int kV2 = 6;             // superblock = 2^6 high steps for 33 <= n <= 64
+// Fast-walk variants (words per plane NW, superblock = 2^V high steps).
+enum FastVariant { kFast1V7 = 0, kFast1V8 = 1, kFast2V6 = 2, kFast2V7 = 3, kNumFast = 4 };
+constexpr int fast_nw(int v) { return v <= kFast1V8 ? 1 : 2; }
+constexpr int fast_v(int v) { return v == kFast1V7 ? 7 : v == kFast1V8 ? 8 : v == kFast2V6 ? 6 : 7; }
 
 // Fast walk over [F0, F1) high steps (multiples of 2^V) of every matrix,
 // chunked into items of L high steps.
@@ -36,15 +38,16 @@ struct GenericParams {
   uint32_t z0_init, z1_init;
 };
 
-const void* walk_fast_symbol(int nw);
+const void* walk_fast_symbol(int variant);
 const void* walk_generic_symbol(int nw);
-cudaError_t launch_walk_fast(int nw, int grid, const FastParams& p, cudaStream_t st);
+cudaError_t launch_walk_fast(int variant, int grid, const FastParams& p, cudaStream_t st);
 cudaError_t launch_walk_generic(int nw, int grid, const GenericParams& p, cudaStream_t st);
 cudaError_t launch_pack(const uint8_t* entries, long long B, int n, RowRec* rows, int grid, cudaStream_t st);
 cudaError_t launch_sample(int n, long long t0, long long count, unsigned long long seed, RowRec* rows,
                           uint8_t* entries_out, cudaStream_t st);
 cudaError_t launch_finalize(const unsigned long long* pm, long long B, int n, int8_t* cls, long long* partial,
                             long long* hist, cudaStream_t st);
+cudaError_t run_alu_peak(int sm_count, uint32_t* scratch, cudaStream_t st, double* ops_per_s, double* ms);
 cudaError_t launch_selftest(const uint32_t* in, int count, int op, uint32_t* out, cudaStream_t st);
 
 }  // namespace tp

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -44,11 +45,16 @@ struct Device {
   int sm_count = 0;
   int max_clock_khz = 0;
   int cc_major = 0, cc_minor = 0;
-  int fast_blocks_per_sm[3] = {0, 0, 0};  // indexed by NW
+  int fast_blocks_per_sm[tp::kNumFast] = {};  // indexed by FastVariant
   int generic_blocks_per_sm[3] = {0, 0, 0};
   cudaStream_t stream = nullptr;
   void* ws = nullptr;  // grow-only workspace
   size_t ws_size = 0;
+  // Work-queue counters for the fast walk, used round-robin so that walks
+  // enqueued on different streams never share a counter.
+  static constexpr int kQueues = 64;
+  unsigned long long* queues = nullptr;
+  int next_queue = 0;
   std::mutex mu;
 };
 
@@ -75,15 +81,18 @@ int ensure_device(int dev, Device** out) {
     TP_CUDA(cudaDeviceGetAttribute(&d.max_clock_khz, cudaDevAttrClockRate, dev));
     d.cc_major = prop.major;
     d.cc_minor = prop.minor;
-    for (int nw = 1; nw <= 2; ++nw) {
-      TP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.fast_blocks_per_sm[nw], tp::walk_fast_symbol(nw),
+    for (int v = 0; v < tp::kNumFast; ++v) {
+      TP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.fast_blocks_per_sm[v], tp::walk_fast_symbol(v),
                                                             tp::kWalkThreads, 0));
+      if (d.fast_blocks_per_sm[v] < 1) return fail(TP_E_CUDA, "walk kernels cannot be resident on device %d", dev);
+    }
+    for (int nw = 1; nw <= 2; ++nw) {
       TP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.generic_blocks_per_sm[nw],
                                                             tp::walk_generic_symbol(nw), tp::kWalkThreads, 0));
-      if (d.fast_blocks_per_sm[nw] < 1 || d.generic_blocks_per_sm[nw] < 1)
-        return fail(TP_E_CUDA, "walk kernels cannot be resident on device %d", dev);
+      if (d.generic_blocks_per_sm[nw] < 1) return fail(TP_E_CUDA, "walk kernels cannot be resident on device %d", dev);
     }
     TP_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+    TP_CUDA(cudaMalloc(&d.queues, Device::kQueues * sizeof(unsigned long long)));
     d.ready = true;
   }
   *out = &d;
@@ -94,7 +103,7 @@ int ensure_device(int dev, Device** out) {
 int ensure_ws(Device& d, size_t bytes) {
   if (d.ws_size >= bytes) return TP_OK;
   if (d.ws) {
-    TP_CUDA(cudaStreamSynchronize(d.stream));
+    TP_CUDA(cudaDeviceSynchronize());  // async callers may use ws on their own streams
     TP_CUDA(cudaFree(d.ws));
     d.ws = nullptr;
     d.ws_size = 0;
@@ -130,19 +139,42 @@ uint32_t zmask(int bits) {
 // ---------------------------------------------------------------------------
 struct Plan {
   int nw = 1;
+  int variant = 0;
   bool fast = false;
   tp::FastParams fp{};
   tp::GenericParams gp{};
   int fast_grid = 0, generic_grid = 0;
 };
 
+// Superblock size per n: longer superblocks amortise the per-block work, but
+// raise the chance that one lane sees two events of the same step parity in a
+// block (which forces an exact replay); events have probability (2/3)^n.
+// Override with TRITPERM_FAST_VARIANT for measurements.
+int choose_variant(int n) {
+  static int forced = -2;
+  if (forced == -2) {
+    const char* e = getenv("TRITPERM_FAST_VARIANT");
+    forced = e ? atoi(e) : -1;
+  }
+  if (forced >= 0 && forced < tp::kNumFast && (tp::fast_nw(forced) == 1) == (n <= 32)) return forced;
+  if (n <= 32) return n >= 22 ? tp::kFast1V8 : tp::kFast1V7;
+  return tp::kFast2V7;
+}
+
+unsigned long long* take_queue(Device& d) {
+  unsigned long long* q = d.queues + d.next_queue;
+  d.next_queue = (d.next_queue + 1) % Device::kQueues;
+  return q;
+}
+
 // full = true: the whole range [0, 2^n) of every matrix (n <= 64), planned
 // directly in high steps so n = 64 does not overflow; lo/hi are then unused.
-void make_plan(const Device& d, int n, unsigned long long B, unsigned long long lo, unsigned long long hi, bool full,
-               const RowRec* rows, unsigned long long* pm, unsigned long long* queue, Plan& pl) {
+void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, unsigned long long hi, bool full,
+               const RowRec* rows, unsigned long long* pm, Plan& pl) {
   pl = Plan();
   pl.nw = n <= 32 ? 1 : 2;
-  const int V = pl.nw == 1 ? tp::kV1 : tp::kV2;
+  pl.variant = choose_variant(n);
+  const int V = tp::fast_v(pl.variant);
   const unsigned long long SB = 1ull << V;
   const uint32_t z0 = zmask(std::min(n, 32)), z1 = zmask(n - 32);
 
@@ -187,7 +219,7 @@ void make_plan(const Device& d, int n, unsigned long long B, unsigned long long 
     // two multiple of the superblock, capped so per-item counters stay 32-bit.
     const unsigned long long total = F1 - F0;
     const unsigned long long warps =
-        (unsigned long long)d.sm_count * d.fast_blocks_per_sm[pl.nw] * (tp::kWalkThreads / 32);
+        (unsigned long long)d.sm_count * d.fast_blocks_per_sm[pl.variant] * (tp::kWalkThreads / 32);
     const unsigned long long want_items = warps * 8;
     unsigned long long L = SB;
     const unsigned long long Lmax = 1ull << 20;
@@ -195,7 +227,7 @@ void make_plan(const Device& d, int n, unsigned long long B, unsigned long long 
     pl.fast = true;
     pl.fp.rows = rows;
     pl.fp.pm = pm;
-    pl.fp.queue = queue;
+    pl.fp.queue = take_queue(d);
     pl.fp.F0 = F0;
     pl.fp.F1 = F1;
     pl.fp.L = L;
@@ -205,7 +237,7 @@ void make_plan(const Device& d, int n, unsigned long long B, unsigned long long 
     pl.fp.z0_init = z0;
     pl.fp.z1_init = z1;
     pl.fp.one = 1u;
-    const unsigned long long max_grid = (unsigned long long)d.sm_count * d.fast_blocks_per_sm[pl.nw];
+    const unsigned long long max_grid = (unsigned long long)d.sm_count * d.fast_blocks_per_sm[pl.variant];
     const unsigned long long need = (pl.fp.items + 7) / 8;
     pl.fast_grid = (int)std::max<unsigned long long>(1, std::min(max_grid, need));
   } else {
@@ -224,7 +256,7 @@ int run_plan(const Plan& pl, cudaStream_t st, int* launches) {
   int nl = 0;
   if (pl.fast) {
     TP_CUDA(cudaMemsetAsync(pl.fp.queue, 0, sizeof(unsigned long long), st));
-    TP_CUDA(tp::launch_walk_fast(pl.nw, pl.fast_grid, pl.fp, st));
+    TP_CUDA(tp::launch_walk_fast(pl.variant, pl.fast_grid, pl.fp, st));
     nl++;
   }
   if (pl.gp.items) {
@@ -271,12 +303,11 @@ int enqueue_range(Device& d, const uint64_t* mags, const uint64_t* sgns, int n, 
   Carve c2;
   char* base = static_cast<char*>(d.ws);
   RowRec* rows = c2.take<RowRec>(base, 64);
-  unsigned long long* queue = c2.take<unsigned long long>(base, 1);
   RowRec h[64];
   planes_to_rows(mags, sgns, n, h);
   TP_CUDA(cudaMemcpyAsync(rows, h, sizeof h, cudaMemcpyHostToDevice, st));
   Plan pl;
-  make_plan(d, n, 1, lo, hi, false, rows, d_pm, queue, pl);
+  make_plan(d, n, 1, lo, hi, false, rows, d_pm, pl);
   // The H2D above is from pageable memory: it returns once `h` is staged,
   // so `h` may go out of scope before the stream runs.
   return run_plan(pl, st, nullptr);
@@ -370,7 +401,7 @@ int tp_range_sum_async(const uint64_t* mags, const uint64_t* sgns, int n, uint64
   if ((rc = ensure_device(device, &d))) return rc;
   std::lock_guard<std::mutex> lk(d->mu);
   TP_CUDA(cudaSetDevice(device));
-  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d->stream;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);  // 0 = legacy default stream, as in CUDA
   return enqueue_range(*d, mags, sgns, n, lo, hi, reinterpret_cast<unsigned long long*>(d_pm), st);
 }
 
@@ -406,14 +437,13 @@ int tp_range_sum_multi(const uint64_t* mags, const uint64_t* sgns, int n, uint64
     char* base = static_cast<char*>(d.ws);
     Carve c2;
     RowRec* rows = c2.take<RowRec>(base, 64);
-    unsigned long long* queue = c2.take<unsigned long long>(base, 1);
     pms[k] = c2.take<unsigned long long>(base, 2);
     const unsigned long long plo = lo + (unsigned long long)((unsigned __int128)total * k / ndev);
     const unsigned long long phi = lo + (unsigned long long)((unsigned __int128)total * (k + 1) / ndev);
     TP_CUDA(cudaMemsetAsync(pms[k], 0, 2 * sizeof(unsigned long long), d.stream));
     TP_CUDA(cudaMemcpyAsync(rows, h.data(), 64 * sizeof(RowRec), cudaMemcpyHostToDevice, d.stream));
     Plan pl;
-    make_plan(d, n, 1, plo, phi, false, rows, pms[k], queue, pl);
+    make_plan(d, n, 1, plo, phi, false, rows, pms[k], pl);
     if ((rc = run_plan(pl, d.stream, nullptr))) return rc;
   }
   unsigned long long P = 0, M = 0;
@@ -443,7 +473,7 @@ int tp_perm_batch_async(const uint8_t* d_entries, int64_t B, int n, int device, 
   if (rc) return rc;
   std::lock_guard<std::mutex> lk(d->mu);
   TP_CUDA(cudaSetDevice(device));
-  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d->stream;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);  // 0 = legacy default stream, as in CUDA
   Carve cv;
   cv.take<RowRec>(nullptr, (size_t)B * 64);
   cv.take<unsigned long long>(nullptr, 1);
@@ -452,7 +482,6 @@ int tp_perm_batch_async(const uint8_t* d_entries, int64_t B, int n, int device, 
   char* base = static_cast<char*>(d->ws);
   Carve c2;
   RowRec* rows = c2.take<RowRec>(base, (size_t)B * 64);
-  unsigned long long* queue = c2.take<unsigned long long>(base, 1);
   unsigned long long* pm =
       d_pm ? reinterpret_cast<unsigned long long*>(d_pm) : c2.take<unsigned long long>(base, (size_t)B * 2);
   int nl = 0;
@@ -461,13 +490,79 @@ int tp_perm_batch_async(const uint8_t* d_entries, int64_t B, int n, int device, 
   TP_CUDA(tp::launch_pack(d_entries, B, n, rows, pack_grid, st));
   nl++;
   Plan pl;
-  make_plan(*d, n, (unsigned long long)B, 0, 0, true, rows, pm, queue, pl);
+  make_plan(*d, n, (unsigned long long)B, 0, 0, true, rows, pm, pl);
   if ((rc = run_plan(pl, st, &nl))) return rc;
   if (d_class || d_hist) {
     TP_CUDA(tp::launch_finalize(pm, B, n, d_class, nullptr, reinterpret_cast<long long*>(d_hist), st));
     nl++;
   }
   if (launches) *launches = nl;
+  return TP_OK;
+}
+
+int tp_pack_async(const uint8_t* d_entries, int64_t B, int n, int device, void* d_rows, void* stream) {
+  if (n < 1 || n > TP_MAX_N) return fail(TP_E_INVALID, "need 1 <= n <= %d, got %d", TP_MAX_N, n);
+  if (B < 0) return fail(TP_E_INVALID, "batch size must be >= 0");
+  if (B > 0 && (!d_entries || !d_rows)) return fail(TP_E_INVALID, "buffers must not be NULL");
+  if (B == 0) return TP_OK;
+  Device* d;
+  int rc = ensure_device(device, &d);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(d->mu);
+  TP_CUDA(cudaSetDevice(device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);  // 0 = legacy default stream, as in CUDA
+  const int pack_grid = (int)std::min<long long>((B + 7) / 8, (long long)d->sm_count * 8);
+  TP_CUDA(tp::launch_pack(d_entries, B, n, static_cast<RowRec*>(d_rows), pack_grid, st));
+  return TP_OK;
+}
+
+int tp_walk_async(const void* d_rows, int64_t B, int n, int device, uint64_t* d_pm, void* stream, int* launches) {
+  if (n < 1 || n > TP_MAX_N) return fail(TP_E_INVALID, "need 1 <= n <= %d, got %d", TP_MAX_N, n);
+  if (B < 0) return fail(TP_E_INVALID, "batch size must be >= 0");
+  if (B > 0 && (!d_rows || !d_pm)) return fail(TP_E_INVALID, "buffers must not be NULL");
+  if (launches) *launches = 0;
+  if (B == 0) return TP_OK;
+  Device* d;
+  int rc = ensure_device(device, &d);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(d->mu);
+  TP_CUDA(cudaSetDevice(device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);  // 0 = legacy default stream, as in CUDA
+  Plan pl;
+  make_plan(*d, n, (unsigned long long)B, 0, 0, true, static_cast<const RowRec*>(d_rows),
+            reinterpret_cast<unsigned long long*>(d_pm), pl);
+  return run_plan(pl, st, launches);
+}
+
+int tp_finalize_async(const uint64_t* d_pm, int64_t B, int n, int device, int8_t* d_class, int64_t* d_hist,
+                      void* stream) {
+  if (n < 1 || n > TP_MAX_N) return fail(TP_E_INVALID, "need 1 <= n <= %d, got %d", TP_MAX_N, n);
+  if (B < 0) return fail(TP_E_INVALID, "batch size must be >= 0");
+  if (B > 0 && !d_pm) return fail(TP_E_INVALID, "d_pm must not be NULL");
+  if (B == 0) return TP_OK;
+  Device* d;
+  int rc = ensure_device(device, &d);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(d->mu);
+  TP_CUDA(cudaSetDevice(device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);  // 0 = legacy default stream, as in CUDA
+  TP_CUDA(tp::launch_finalize(reinterpret_cast<const unsigned long long*>(d_pm), B, n, d_class, nullptr,
+                              reinterpret_cast<long long*>(d_hist), st));
+  return TP_OK;
+}
+
+int tp_alu_peak(int device, double* lop3_ops_per_s, double* ms) {
+  if (!lop3_ops_per_s) return fail(TP_E_INVALID, "lop3_ops_per_s must not be NULL");
+  Device* d;
+  int rc = ensure_device(device, &d);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(d->mu);
+  TP_CUDA(cudaSetDevice(device));
+  if ((rc = ensure_ws(*d, 1 << 20))) return rc;
+  double ops = 0, t = 0;
+  TP_CUDA(tp::run_alu_peak(d->sm_count, static_cast<uint32_t*>(d->ws), d->stream, &ops, &t));
+  *lop3_ops_per_s = ops;
+  if (ms) *ms = t;
   return TP_OK;
 }
 
@@ -498,7 +593,6 @@ int tp_perm_batch(const uint8_t* entries, int64_t B, int n, int device, int8_t* 
   char* base = static_cast<char*>(d->ws);
   Carve c2;
   RowRec* rows = c2.take<RowRec>(base, (size_t)B * 64);
-  unsigned long long* queue = c2.take<unsigned long long>(base, 1);
   unsigned long long* pm = c2.take<unsigned long long>(base, (size_t)B * 2);
   uint8_t* dent = c2.take<uint8_t>(base, ebytes);
   int8_t* dcls = c2.take<int8_t>(base, (size_t)B);
@@ -510,7 +604,7 @@ int tp_perm_batch(const uint8_t* entries, int64_t B, int n, int device, int8_t* 
   const int pack_grid = (int)std::min<long long>((B + 7) / 8, (long long)d->sm_count * 8);
   TP_CUDA(tp::launch_pack(dent, B, n, rows, pack_grid, st));
   Plan pl;
-  make_plan(*d, n, (unsigned long long)B, 0, 0, true, rows, pm, queue, pl);
+  make_plan(*d, n, (unsigned long long)B, 0, 0, true, rows, pm, pl);
   if ((rc = run_plan(pl, st, nullptr))) return rc;
   TP_CUDA(tp::launch_finalize(pm, B, n, dcls, dpart, dhist, st));
   if (out_class) TP_CUDA(cudaMemcpyAsync(out_class, dcls, (size_t)B, cudaMemcpyDeviceToHost, st));
@@ -550,7 +644,6 @@ static int mc_run(int n, int64_t t0, int64_t count, uint64_t seed, int device, i
   char* base = static_cast<char*>(d->ws);
   Carve c2;
   RowRec* rows = c2.take<RowRec>(base, (size_t)slab * 64);
-  unsigned long long* queue = c2.take<unsigned long long>(base, 1);
   unsigned long long* pm = c2.take<unsigned long long>(base, (size_t)slab * 2);
   int8_t* dcls = c2.take<int8_t>(base, (size_t)slab);
   long long* dhist = c2.take<long long>(base, 3);
@@ -560,7 +653,7 @@ static int mc_run(int n, int64_t t0, int64_t count, uint64_t seed, int device, i
     TP_CUDA(cudaMemsetAsync(pm, 0, (size_t)B * 2 * sizeof(unsigned long long), st));
     TP_CUDA(tp::launch_sample(n, t0 + s0, B, seed, rows, nullptr, st));
     Plan pl;
-    make_plan(*d, n, (unsigned long long)B, 0, 0, true, rows, pm, queue, pl);
+    make_plan(*d, n, (unsigned long long)B, 0, 0, true, rows, pm, pl);
     if ((rc = run_plan(pl, st, nullptr))) return rc;
     TP_CUDA(tp::launch_finalize(pm, B, n, dcls, nullptr, dhist, st));
     if (out_class) TP_CUDA(cudaMemcpyAsync(out_class + s0, dcls, (size_t)B, cudaMemcpyDeviceToHost, st));
@@ -608,7 +701,7 @@ int tp_sample_classes(int n, int64_t t0, int64_t count, uint64_t seed, int devic
   if (rc) return rc;
   std::lock_guard<std::mutex> lk(d->mu);
   TP_CUDA(cudaSetDevice(device));
-  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d->stream;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);  // 0 = legacy default stream, as in CUDA
   if (out_on_device) {
     TP_CUDA(tp::launch_sample(n, t0, count, seed, nullptr, out, st));
     return TP_OK;

@@ -185,6 +185,66 @@ def anchors(with_slow: bool):
     dump("anchors.json", res)
 
 
+def oracle_goldens():
+    """Large goldens computed by the C oracle (oracle/oracle.c), which the
+    cheap goldens above pin against the reference; each block is
+    additionally cross-pinned to a reference output where one exists."""
+    from oracle import oracle as orc
+    from paper_2407_20205_b200 import fixtures
+
+    orc.build()
+    path = os.path.join(HERE, "anchors.json")
+    with open(path) as f:
+        res = json.load(f)
+    threads = os.cpu_count() or 1
+    # C2: all 16,384 classes of the reference stream at n=24, seed 0
+    t0 = time.time()
+    e = fixtures.uniform_batch(24, 0, 0, 16384)
+    for t in (0, 1, 16383):  # fixture == reference sampler
+        assert enc(np.mod(np.array(ref_rng.sample_square(0, t, 24)), 3)) == enc(e[t])
+    cls, part = orc.perm_batch(e, threads=threads)
+    hist = np.bincount(cls, minlength=3).tolist()
+    assert hist[0] == res["c2_zero_count"]["zero_count"], (hist, res["c2_zero_count"])  # pinned by the reference
+    for t in range(8):  # and by the reference's own kernel on the first matrices
+        m = ref_perm.MatrixF3(ref_rng.sample_square(0, t, 24))
+        assert ref_perm.perm_chunk(m, 1, 1 << 24).partial_sum == part[t]
+    res["c2_classes"] = "".join(str(int(c)) for c in cls)
+    res["c2_hist"] = hist
+    res["c2_partials_head"] = [int(v) for v in part[:64]]
+    print(f"c2 oracle: {time.time() - t0:.1f}s hist={hist}")
+    # C3: oracle classes of a seeded subset of the uniform and sparse families
+    t0 = time.time()
+    entries, fam, exp = fixtures.structured_batch(32, 0, 4096)
+    idx = [int(i) for i in list(range(0, 24)) + list(range(1024, 1048))]
+    sub_cls, _ = orc.perm_batch(entries[idx], threads=threads)
+    res["c3_subset"] = [[i, int(c)] for i, c in zip(idx, sub_cls)]
+    res["c3_entries_sha256"] = __import__("hashlib").sha256(entries.tobytes()).hexdigest()
+    print(f"c3 oracle subset: {time.time() - t0:.1f}s")
+    # C4: full n=36 traversal, cross-pinned to the reference's parallel engine
+    t0 = time.time()
+    w = res["c4_window"]
+    a = np.frombuffer(w["a"].encode(), dtype=np.uint8).reshape(36, 36) - ord("0")
+    mags, sgns = orc.planes_from_classes(a)
+    full = orc.chunk_sum_mt(mags, sgns, 36, 1, 1 << 36, threads)
+    ref_val = ref_perm.perm_mod3_parallel(ref_perm.MatrixF3(ref_rng.sample_square(0, 0, 36)), jobs=threads)
+    assert orc.finalize(36, full) == ref_val
+    res["c4_full"] = {"n": 36, "seed": 0, "trial": 0, "a": w["a"], "partial": int(full),
+                      "class": int(orc.finalize(36, full)) % 3}
+    print(f"c4 full: {time.time() - t0:.1f}s partial={full}")
+    # C5: a 2^36-step window of the n=50 matrix (SURVEY appendix B: -5)
+    t0 = time.time()
+    w = res["c5_window"]
+    a = np.frombuffer(w["a"].encode(), dtype=np.uint8).reshape(50, 50) - ord("0")
+    mags, sgns = orc.planes_from_classes(a)
+    lo = 1 << 40
+    assert orc.chunk_sum(mags, sgns, 50, w["lo"], w["hi"]) == w["partial"]
+    s36 = orc.chunk_sum_mt(mags, sgns, 50, lo, lo + (1 << 36), threads)
+    res["c5_window36"] = {"n": 50, "seed": 0, "trial": 0, "a": w["a"], "lo": lo, "hi": lo + (1 << 36),
+                          "partial": int(s36)}
+    print(f"c5 window36: {time.time() - t0:.1f}s partial={s36}")
+    dump("anchors.json", res)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--with-slow", action="store_true")
@@ -192,6 +252,8 @@ def main():
     args = ap.parse_args()
     jobs = {"core": core_ops, "rng": rng_vectors, "chunks": chunks, "tower": tower,
             "anchors": lambda: anchors(args.with_slow)}
+    if args.with_slow:
+        jobs["oracle"] = oracle_goldens
     for name, fn in jobs.items():
         if args.only and name not in args.only.split(","):
             continue
