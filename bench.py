@@ -327,9 +327,9 @@ def main():
     job_terms = per_rank_terms * world if scaling == "weak" else terms_per_step(wl, args)
     value = job_terms / (ms_per_step * 1e-3)
 
-    # ALU roofline of the walk kernel: 3 LOP3 per 32 columns per subset term
-    words = 1 if n <= 32 else 2
-    ops_per_term = 3 * words
+    # ALU roofline of the walk kernel: 3 LOP3 per subset term for every n
+    # (n > 32 walks only the 32 primary columns)
+    ops_per_term = 3
     walk_avg = sum(walk_ms) / len(walk_ms)
     achieved = per_rank_terms * ops_per_term / (walk_avg * 1e-3)
     peak, _ = _kernels.alu_peak(local)
@@ -337,7 +337,7 @@ def main():
     tpath = os.path.join(REPO, "profiles", "walk_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(wl)
+            traffic = json.load(open(tpath)).get(wl, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
 
@@ -365,7 +365,7 @@ def main():
         m_obj = tp.MatrixF3(make_entries(wl, 0)[0].astype(np.int64))
         lo = (1 << 40) if wl == "c5" else 1
         span = terms_per_step(wl, args)
-        tp.perm_chunk(m_obj, lo, lo + min(span, 1 << 20))
+        tp.perm_chunk(m_obj, lo, min(lo + min(span, 1 << 20), 1 << n))
         t0 = time.perf_counter()
         tp.perm_chunk(m_obj, lo, min(lo + span, 1 << n))
         e2e_s = time.perf_counter() - t0
@@ -399,7 +399,7 @@ def main():
                        "terms_per_step": job_terms},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "LOP3 ops/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_walk_fast (tp_kernels.cu)",
+                         "kernel": ("k_walk_lane" if n <= 32 else "k_walk_wide") + " (csrc/tp_kernels.cu)",
                          "ops_per_term": ops_per_term,
                          "peak_source": "LOP3 chain probe (tp_alu_peak) on this GPU in this run; "
                                         "nominal 148 SM x 64 lanes x clock",

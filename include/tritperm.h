@@ -126,6 +126,11 @@ int tp_finalize_async(const uint64_t *d_pm, int64_t B, int n, int device,
  * with CUDA events, and the kernel's duration in ms. */
 int tp_alu_peak(int device, double *lop3_ops_per_s, double *ms);
 
+/* Debug: when d_trace != NULL, every later fast-walk launch records per warp
+ * (SM id, clock64 at start, clock64 at end, items) into the device buffer
+ * d_trace[4 * warp] (uint64).  NULL switches tracing off. */
+int tp_debug_trace(void *d_trace);
+
 /* Monte Carlo tally over trials [t0, t1) with the reference's per-trial
  * splitmix64 streams (src/rng.py, src/_kernels.py:212-242), sampled on the
  * device.  *zeros == mc_zero_count(n, t0, t1, seed); hist[3] (may be NULL)

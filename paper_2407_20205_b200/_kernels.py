@@ -69,6 +69,7 @@ SIGNATURES = {
                                      ctypes.c_void_p, _ip]),
     "tp_finalize_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "tp_debug_trace": (ctypes.c_int, [ctypes.c_void_p]),
     "tp_alu_peak": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
 }
 

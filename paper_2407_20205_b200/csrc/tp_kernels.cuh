@@ -8,32 +8,56 @@
 namespace tp {
 
 constexpr int kWalkThreads = 256;  // 8 warps per CTA
-// Fast-walk variants (words per plane NW, superblock = 2^V high steps).
-enum FastVariant { kFast1V7 = 0, kFast1V8 = 1, kFast2V6 = 2, kFast2V7 = 3, kNumFast = 4 };
-constexpr int fast_nw(int v) { return v <= kFast1V8 ? 1 : 2; }
-constexpr int fast_v(int v) { return v == kFast1V7 ? 7 : v == kFast1V8 ? 8 : v == kFast2V6 ? 6 : 7; }
+// Fast-walk variants.  Lane walk (n <= 32): one subset per lane, superblock
+// 2^V high steps of 32 reference steps.  Wide walk (n > 32): 2^KB subsets per
+// lane, superblock 2^V high steps of 32 * 2^KB reference steps.
+// Variant = (kind, KB, V, warps per CTA); each warp takes its own items.
+// The unrolled superblock body is (2^V - 1) * 2^KB steps: keep it <= ~20 KB of
+// SASS so it stays resident in the instruction cache.
+enum FastVariant {
+  kLaneV7W4 = 0,
+  kLaneV8W4 = 1,
+  kWideK2V7W4 = 2,
+  kWideK4V6W4 = 3,
+  kWideK8V5W4 = 4,
+  kWideK8V6W4 = 5,
+  kNumFast = 6
+};
+constexpr bool fast_is_lane(int v) { return v <= kLaneV8W4; }
+constexpr int fast_v(int v) {
+  return v == kLaneV7W4 ? 7 : v == kLaneV8W4 ? 8 : v == kWideK2V7W4 ? 7 : v == kWideK4V6W4 ? 6 : v == kWideK8V5W4 ? 5 : 6;
+}
+constexpr int fast_kb(int v) {
+  return fast_is_lane(v) ? 0 : v == kWideK2V7W4 ? 1 : v == kWideK4V6W4 ? 2 : 3;
+}
+constexpr int fast_warps(int) { return 4; }
 
-// Fast walk over [F0, F1) high steps (multiples of 2^V) of every matrix,
-// chunked into items of L high steps.
+// Fast walk: items are L-aligned chunks [F0 + c*L, F0 + (c+1)*L) of every
+// matrix's fast region, in fast units (32 * 2^KB reference steps); L =
+// nblk * 2^V, nblk a power of two >= 2, F0 a multiple of L.
 struct FastParams {
   const RowRec* rows;           // [B][64]
   unsigned long long* pm;       // [B][2] (plus, minus) accumulators
   unsigned long long* queue;    // dynamic work counter (zeroed before launch)
-  unsigned long long F0, F1, L, chunks, items;
+  unsigned long long F0, L, chunks, items;
+  uint32_t nblk;                // superblocks per item
+  int lognblk;
   int n;
   uint32_t z0_init, z1_init;    // zero-indicator of an empty vector (padding = 0)
   uint32_t one;                 // runtime 1
+  unsigned long long* trace;    // optional per-warp trace (smid, t_start, t_end, items); nullptr = off
 };
 
-constexpr int kMaxSeg = 4;
+// Generic walk: regions [reg_a0[r], reg_a1[r]) of 32-step high steps, cut
+// into pieces of glen high steps; one warp per (matrix, piece).
 struct GenericParams {
   const RowRec* rows;
   unsigned long long* pm;
-  unsigned long long seg_a0[kMaxSeg], seg_a1[kMaxSeg];
+  unsigned long long reg_a0[2], reg_a1[2], pieces[2];
+  unsigned long long glen;
   unsigned long long lo, hi;    // reference step range for lane masking
-  int masked;                   // 0: every lane of every segment is in range
-  unsigned long long items;     // B * nseg
-  int nseg;
+  int masked;                   // 0: every lane of every piece is in range
+  unsigned long long items;     // B * (pieces[0] + pieces[1])
   int n;
   uint32_t z0_init, z1_init;
 };

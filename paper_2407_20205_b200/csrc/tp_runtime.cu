@@ -83,7 +83,7 @@ int ensure_device(int dev, Device** out) {
     d.cc_minor = prop.minor;
     for (int v = 0; v < tp::kNumFast; ++v) {
       TP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.fast_blocks_per_sm[v], tp::walk_fast_symbol(v),
-                                                            tp::kWalkThreads, 0));
+                                                            32 * tp::fast_warps(v), 0));
       if (d.fast_blocks_per_sm[v] < 1) return fail(TP_E_CUDA, "walk kernels cannot be resident on device %d", dev);
     }
     for (int nw = 1; nw <= 2; ++nw) {
@@ -156,10 +156,13 @@ int choose_variant(int n) {
     const char* e = getenv("TRITPERM_FAST_VARIANT");
     forced = e ? atoi(e) : -1;
   }
-  if (forced >= 0 && forced < tp::kNumFast && (tp::fast_nw(forced) == 1) == (n <= 32)) return forced;
-  if (n <= 32) return n >= 22 ? tp::kFast1V8 : tp::kFast1V7;
-  return tp::kFast2V7;
+  if (forced >= 0 && forced < tp::kNumFast && tp::fast_is_lane(forced) == (n <= 32)) return forced;
+  if (n <= 32) return n >= 22 ? tp::kLaneV8W4 : tp::kLaneV7W4;
+  return tp::kWideK4V6W4;
 }
+
+// Optional CTA trace buffer for the fast walks (tp_debug_trace).
+unsigned long long* g_trace = nullptr;
 
 unsigned long long* take_queue(Device& d) {
   unsigned long long* q = d.queues + d.next_queue;
@@ -169,13 +172,20 @@ unsigned long long* take_queue(Device& d) {
 
 // full = true: the whole range [0, 2^n) of every matrix (n <= 64), planned
 // directly in high steps so n = 64 does not overflow; lo/hi are then unused.
+// Otherwise the reference step range [lo, hi) (hi <= 2^63).
+//
+// Layout: the fast kernel takes the L-aligned part of the fully covered fast
+// units; the generic kernel takes the rest (range heads/tails, small n) in
+// pieces of kGenericPiece high steps so it parallelises.
+constexpr unsigned long long kGenericPiece = 64;
+
 void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, unsigned long long hi, bool full,
                const RowRec* rows, unsigned long long* pm, Plan& pl) {
   pl = Plan();
   pl.nw = n <= 32 ? 1 : 2;
   pl.variant = choose_variant(n);
   const int V = tp::fast_v(pl.variant);
-  const unsigned long long SB = 1ull << V;
+  const int U = tp::fast_kb(pl.variant);  // log2(fast unit / 32 reference steps)
   const uint32_t z0 = zmask(std::min(n, 32)), z1 = zmask(n - 32);
 
   pl.gp.rows = rows;
@@ -183,8 +193,8 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
   pl.gp.n = n;
   pl.gp.z0_init = z0;
   pl.gp.z1_init = z1;
-  pl.gp.nseg = 0;
-  unsigned long long a_lo, a_hi, A0, A1;
+  pl.gp.glen = kGenericPiece;
+  unsigned long long a_lo, a_hi, A0, A1;  // touched / fully covered high steps (32-step units)
   if (full) {
     const unsigned long long H = n >= 5 ? (1ull << (n - 5)) : 1ull;
     a_lo = A0 = 0;
@@ -194,56 +204,74 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
     pl.gp.masked = n < 5 ? 1 : 0;
   } else {
     if (lo >= hi) return;
+    if (lo == 1) lo = 0;  // step 0 (the empty subset) contributes 0 for n >= 1
     a_lo = lo >> 5;
-    a_hi = (hi + 31) >> 5;  // high steps touched (hi <= 2^63)
+    a_hi = (hi + 31) >> 5;
     A0 = (lo + 31) >> 5;
-    A1 = hi >> 5;  // fully covered high steps [A0, A1)
+    A1 = hi >> 5;
     pl.gp.lo = lo;
     pl.gp.hi = hi;
     pl.gp.masked = 1;
   }
   if (B == 0) return;
-  const unsigned long long F0 = (A0 + SB - 1) / SB * SB, F1 = A1 / SB * SB;
-  const bool fast = (n >= 5 + V) && F0 < F1;
-  auto add_seg = [&](unsigned long long a0, unsigned long long a1) {
-    if (a0 < a1) {
-      pl.gp.seg_a0[pl.gp.nseg] = a0;
-      pl.gp.seg_a1[pl.gp.nseg] = a1;
-      pl.gp.nseg++;
+
+  // Fast region, in fast units of 2^U high steps, superblocks of 2^V units.
+  const unsigned long long A0u = (A0 + (1ull << U) - 1) >> U, A1u = A1 >> U;
+  const unsigned long long SBu = 1ull << V;
+  unsigned long long F0 = 0, F1 = 0, L = 0;
+  if (n >= 5 + U + V + 1 && A0u < A1u) {
+    const int bps = d.fast_blocks_per_sm[pl.variant];
+    const unsigned long long warps = (unsigned long long)d.sm_count * bps * tp::fast_warps(pl.variant);
+    const unsigned long long want_items = warps * 32;  // dynamic queue: a few dozen per warp
+    const unsigned long long Lmax = 1ull << (20 - U);   // per-item counters stay 32-bit
+    auto aligned_chunks = [&](unsigned long long Lc) {
+      const unsigned long long f0 = (A0u + Lc - 1) / Lc * Lc, f1 = A1u / Lc * Lc;
+      return f1 > f0 ? (f1 - f0) / Lc : 0ull;
+    };
+    L = 2 * SBu;
+    if (aligned_chunks(L) == 0) L = 0;
+    while (L && 2 * L <= Lmax && aligned_chunks(2 * L) * B >= want_items) L <<= 1;
+    if (L) {
+      F0 = (A0u + L - 1) / L * L;
+      F1 = A1u / L * L;
     }
-  };
-  if (fast) {
-    add_seg(a_lo, F0);
-    add_seg(F1, a_hi);
-    // Chunking: enough items for a few per resident warp, chunks a power of
-    // two multiple of the superblock, capped so per-item counters stay 32-bit.
-    const unsigned long long total = F1 - F0;
-    const unsigned long long warps =
-        (unsigned long long)d.sm_count * d.fast_blocks_per_sm[pl.variant] * (tp::kWalkThreads / 32);
-    const unsigned long long want_items = warps * 8;
-    unsigned long long L = SB;
-    const unsigned long long Lmax = 1ull << 20;
-    while (L < Lmax && (total + 2 * L - 1) / (2 * L) * B >= want_items) L <<= 1;
+  }
+  unsigned long long g0a = a_lo, g0b = a_hi, g1a = 0, g1b = 0;  // generic regions (32-step units)
+  if (L) {
+    g0b = F0 << U;
+    g1a = F1 << U;
+    g1b = a_hi;
     pl.fast = true;
     pl.fp.rows = rows;
     pl.fp.pm = pm;
     pl.fp.queue = take_queue(d);
     pl.fp.F0 = F0;
-    pl.fp.F1 = F1;
     pl.fp.L = L;
-    pl.fp.chunks = (total + L - 1) / L;
+    pl.fp.chunks = (F1 - F0) / L;
     pl.fp.items = pl.fp.chunks * B;
+    pl.fp.nblk = (uint32_t)(L >> V);
+    pl.fp.lognblk = 0;
+    while ((1u << pl.fp.lognblk) < pl.fp.nblk) pl.fp.lognblk++;
     pl.fp.n = n;
     pl.fp.z0_init = z0;
     pl.fp.z1_init = z1;
     pl.fp.one = 1u;
-    const unsigned long long max_grid = (unsigned long long)d.sm_count * d.fast_blocks_per_sm[pl.variant];
-    const unsigned long long need = (pl.fp.items + 7) / 8;
-    pl.fast_grid = (int)std::max<unsigned long long>(1, std::min(max_grid, need));
-  } else {
-    add_seg(a_lo, a_hi);
+    pl.fp.trace = g_trace;
+    const int bps = d.fast_blocks_per_sm[pl.variant];
+    const unsigned long long ctas = (unsigned long long)d.sm_count * bps;
+    const unsigned long long wpc = tp::fast_warps(pl.variant);
+    pl.fast_grid = (int)std::max<unsigned long long>(1, std::min(ctas, (pl.fp.items + wpc - 1) / wpc));
   }
-  pl.gp.items = (unsigned long long)pl.gp.nseg * B;
+  auto pieces = [&](unsigned long long x0, unsigned long long x1) {
+    return x1 > x0 ? (x1 - x0 + kGenericPiece - 1) / kGenericPiece : 0ull;
+  };
+  pl.gp.reg_a0[0] = g0a;
+  pl.gp.reg_a1[0] = g0b;
+  pl.gp.pieces[0] = pieces(g0a, g0b);
+  pl.gp.reg_a0[1] = g1a;
+  pl.gp.reg_a1[1] = g1b;
+  pl.gp.pieces[1] = pieces(g1a, g1b);
+  pl.gp.items = (pl.gp.pieces[0] + pl.gp.pieces[1]) * B;
   if (pl.gp.items) {
     const unsigned long long max_grid = (unsigned long long)d.sm_count * d.generic_blocks_per_sm[pl.nw];
     const unsigned long long need = (pl.gp.items + 7) / 8;
@@ -548,6 +576,13 @@ int tp_finalize_async(const uint64_t* d_pm, int64_t B, int n, int device, int8_t
   cudaStream_t st = static_cast<cudaStream_t>(stream);  // 0 = legacy default stream, as in CUDA
   TP_CUDA(tp::launch_finalize(reinterpret_cast<const unsigned long long*>(d_pm), B, n, d_class, nullptr,
                               reinterpret_cast<long long*>(d_hist), st));
+  return TP_OK;
+}
+
+// Debug: when d_trace != NULL, fast-walk launches record per warp
+// (smid, clock64 start, clock64 end, items) into d_trace[4*warp].
+int tp_debug_trace(void* d_trace) {
+  g_trace = static_cast<unsigned long long*>(d_trace);
   return TP_OK;
 }
 
