@@ -160,31 +160,62 @@ __global__ void __launch_bounds__(32 * WARPS) k_walk_lane(FastParams p) {
     uint32_t ev = 0, odd = 0;
     uint32_t cnt0 = 0, cnt1 = 0, slot0 = 0, slot1 = 0;
     record_slot(z[0], g[0], cnt0, slot0, one);
+    bool dense = false;  // warp-uniform: exact accumulation mode for event-dense inputs
     for (uint32_t kb = 0; kb < p.nblk; ++kb) {
       const uint32_t ze = z[0], ge = g[0];
       // row 5+V-1 flips at j = 2^(V-1); it leaves iff bit 0 of B0+kb (= of kb) is set
       const uint32_t SX = (kb & 1u) ? SS[V - 1] : SA[V - 1];
+      if (!dense) {
 #pragma unroll
-      for (int j = 1; j < (1 << V); ++j) {
-        const int t = ctz_c(j);
-        const bool leave = (t + 1 < V) ? (((j >> (t + 1)) & 1) != 0) : false;
-        const uint32_t sop = (t == V - 1) ? SX : (leave ? SS[t] : SA[t]);
-        sub_word(z[0], g[0], SM[t], sop);
-        if (j & 1) record_slot(z[0], g[0], cnt1, slot1, one);
-        else record_slot(z[0], g[0], cnt0, slot0, one);
-      }
-      // fold this superblock's events in exactly
-      if (__any_sync(FULL, (cnt0 | cnt1) != 0)) {
+        for (int j = 1; j < (1 << V); ++j) {
+          const int t = ctz_c(j);
+          const bool leave = (t + 1 < V) ? (((j >> (t + 1)) & 1) != 0) : false;
+          const uint32_t sop = (t == V - 1) ? SX : (leave ? SS[t] : SA[t]);
+          sub_word(z[0], g[0], SM[t], sop);
+          if (j & 1) record_slot(z[0], g[0], cnt1, slot1, one);
+          else record_slot(z[0], g[0], cnt0, slot0, one);
+        }
+        // fold this superblock's events in exactly
+        if (__any_sync(FULL, (cnt0 | cnt1) != 0)) {
+          uint32_t bev = 0, bodd = 0;
+          if (cnt0 == 1) { bev += 1; bodd += (__popc(slot0) ^ lanepar) & 1u; }
+          if (cnt1 == 1) { bev += 1; bodd += (__popc(slot1) ^ 1u ^ lanepar) & 1u; }
+          if (__any_sync(FULL, cnt0 > 1 || cnt1 > 1)) {
+            const unsigned long long r = replay_block<1>(R, ze, 0u, ge, 0u, (B0 + kb) << V, 1 << V, lanepar);
+            bev = (uint32_t)r;
+            bodd = (uint32_t)(r >> 32);
+            dense = true;  // events are dense here: accumulate exactly from now on
+          }
+          ev += bev;
+          odd += bodd;
+        }
+      } else {
+        // Exact block for event-dense matrices (e.g. all-ones rows): every
+        // full step is folded in as it happens.  Two halves of 2^(V-1)
+        // steps keep the unrolled body small; the middle step flips row
+        // 5+V-1 (direction SX), and in half h the step j' = 2^(V-2) flips
+        // row 5+V-2, leaving iff h == 1.
         uint32_t bev = 0, bodd = 0;
-        if (cnt0 == 1) { bev += 1; bodd += (__popc(slot0) ^ lanepar) & 1u; }
-        if (cnt1 == 1) { bev += 1; bodd += (__popc(slot1) ^ 1u ^ lanepar) & 1u; }
-        if (__any_sync(FULL, cnt0 > 1 || cnt1 > 1)) {
-          const unsigned long long r = replay_block<1>(R, ze, 0u, ge, 0u, (B0 + kb) << V, 1 << V, lanepar);
-          bev = (uint32_t)r;
-          bodd = (uint32_t)(r >> 32);
+        if (cnt0 == 1) { bev += 1; bodd += (__popc(slot0) ^ lanepar) & 1u; }  // entry step
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          if (h == 1) {
+            sub_word(z[0], g[0], SM[V - 1], SX);
+            if (z[0] == 0) { bev += 1; bodd += (__popc(g[0]) ^ lanepar) & 1u; }
+          }
+          const uint32_t SH = h ? SS[V - 2] : SA[V - 2];
+#pragma unroll
+          for (int j = 1; j < (1 << (V - 1)); ++j) {
+            const int t = ctz_c(j);
+            const bool leave = (t + 2 < V) ? (((j >> (t + 1)) & 1) != 0) : false;
+            const uint32_t sop = (t == V - 2) ? SH : (leave ? SS[t] : SA[t]);
+            sub_word(z[0], g[0], SM[t], sop);
+            if (z[0] == 0) { bev += 1; bodd += (__popc(g[0]) ^ (uint32_t)(j & 1) ^ lanepar) & 1u; }
+          }
         }
         ev += bev;
         odd += bodd;
+        dense = __any_sync(FULL, bev >= 4);
       }
       cnt0 = cnt1 = 0;
       if (kb + 1 < p.nblk) {
