@@ -242,3 +242,32 @@ def test_abi_rejects_bad_arguments(gpu):
         _kernels.chunk_counts(bad, z, 4, 0, 16)
     with pytest.raises(ValueError):
         _kernels.perm_batch(np.zeros((1, 65, 65), dtype=np.uint8))
+
+
+def test_integration_binding_from_markdown(gpu):
+    """The reference-side ctypes binding shown in INTEGRATION.md works as written."""
+    import os
+    import re
+
+    from conftest import REPO
+    from paper_2407_20205_b200 import _kernels
+
+    md = open(os.path.join(REPO, "INTEGRATION.md")).read()
+    code = re.search(r"```python\n(# tritperm/_kernels_b200.py.*?)```", md, flags=re.S).group(1)
+    os.environ["TRITPERM_B200_LIB"] = _kernels.LIB_PATH
+    ns = {}
+    exec(compile(code, "_kernels_b200.py", "exec"), ns)
+    for case in load_golden("chunks.json")["cases"][:40]:
+        n = case["n"]
+        m = gpu.MatrixF3(centred(dec(case["a"], n)))
+        mags, sgns = m.planes()
+        for lo, hi, s in case["ranges"]:
+            if lo >= 1:
+                assert ns["chunk_sum"](mags, sgns, n, lo, hi) == s
+                assert ns["chunk_sum_devices"](mags, sgns, n, lo, hi, [0]) == s
+    for case in load_golden("anchors.json")["montecarlo"][:5]:
+        assert ns["mc_zero_count"](case["n"], 0, case["trials"], case["seed"]) == case["zero_count"]
+    for case in load_golden("rng.json")["samples"][:8]:
+        n = case["n"]
+        got = ns["mc_sample_entries"](n, case["trial"], case["seed"]).reshape(n, n)
+        assert np.array_equal(np.mod(got.astype(int), 3), dec(case["entries"], n))
