@@ -271,3 +271,36 @@ def test_integration_binding_from_markdown(gpu):
         n = case["n"]
         got = ns["mc_sample_entries"](n, case["trial"], case["seed"]).reshape(n, n)
         assert np.array_equal(np.mod(got.astype(int), 3), dec(case["entries"], n))
+
+
+def test_distributed_path_single_rank_nccl(gpu, oracle):
+    """parallel.py on the device with a real NCCL process group (world size 1:
+    the only size a 1-GPU box allows); the 2-rank partition is covered by
+    tests/test_parallel_gloo.py."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2407_20205_b200 import parallel
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        case = load_golden("anchors.json")["c1"][1]
+        a = dec(case["a"], 20)
+        m = gpu.MatrixF3(centred(a))
+        p, q = parallel.distributed_counts(m)
+        assert p - q == case["partial"]
+        assert parallel.perm_mod3_distributed(m) % 3 == case["class"]
+        h = parallel.distributed_hist([3, 4, 5])
+        assert h.tolist() == [3, 4, 5]
+    finally:
+        dist.destroy_process_group()
