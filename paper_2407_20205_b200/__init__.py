@@ -26,6 +26,7 @@ from .experiments import (
     sample_trial_matrix,
     trial_classes,
 )
+from .pi import pi_digit, pi_matrix
 from .permanent import (
     ChunkResult,
     MatrixF3,
@@ -59,6 +60,8 @@ __all__ = [
     "perm_mod3_batch",
     "perm_mod3_fast",
     "perm_mod3_parallel",
+    "pi_digit",
+    "pi_matrix",
     "resolve_gpus",
     "resolve_jobs",
     "sample_trial_matrix",

@@ -245,12 +245,34 @@ def oracle_goldens():
     dump("anchors.json", res)
 
 
+def pi_goldens():
+    """pi_matrix rows and Pi_50 windows from the reference (src/experiments.py:193-213)."""
+    out = {"pi_matrix": [], "windows": []}
+    for n in (1, 3, 6, 20, 50):
+        for skip in (False, True):
+            m = ref_exp.pi_matrix(n, skip_integer_part=skip)
+            rec = {"n": n, "skip_integer_part": skip, "a": enc(m.rows)}
+            if n <= 20:
+                rec["perm"] = ref_perm.perm_mod3_fast(m)
+                rec["partial"] = ref_perm.perm_chunk(m, 1, 1 << n).partial_sum
+            out["pi_matrix"].append(rec)
+    for skip in (False, True):
+        m = ref_exp.pi_matrix(50, skip_integer_part=skip)
+        mags, sgns = m.planes()
+        lo = 1 << 40
+        t0 = time.time()
+        s30 = int(ref_k.chunk_sum(mags, sgns, 50, lo, lo + (1 << 30)))
+        out["windows"].append({"skip_integer_part": skip, "lo": lo, "hi": lo + (1 << 30), "partial": s30})
+        print(f"pi50 skip={skip} window 2^30: {s30} ({time.time() - t0:.1f}s)")
+    dump("pi.json", out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--with-slow", action="store_true")
     ap.add_argument("--only", default=None)
     args = ap.parse_args()
-    jobs = {"core": core_ops, "rng": rng_vectors, "chunks": chunks, "tower": tower,
+    jobs = {"core": core_ops, "rng": rng_vectors, "chunks": chunks, "tower": tower, "pi": pi_goldens,
             "anchors": lambda: anchors(args.with_slow)}
     if args.with_slow:
         jobs["oracle"] = oracle_goldens

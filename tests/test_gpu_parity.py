@@ -304,3 +304,15 @@ def test_distributed_path_single_rank_nccl(gpu, oracle):
         assert h.tolist() == [3, 4, 5]
     finally:
         dist.destroy_process_group()
+
+
+def test_pi_matrices_and_pi50_windows(gpu):
+    g = load_golden("pi.json")
+    for rec in g["pi_matrix"]:
+        if "perm" in rec:
+            m = gpu.pi_matrix(rec["n"], skip_integer_part=rec["skip_integer_part"])
+            assert gpu.perm_mod3_fast(m) == rec["perm"]
+            assert gpu.perm_chunk(m, 1, 1 << rec["n"]).partial_sum == rec["partial"]
+    for w in g["windows"]:
+        m = gpu.pi_matrix(50, skip_integer_part=w["skip_integer_part"])
+        assert gpu.perm_chunk(m, w["lo"], w["hi"]).partial_sum == w["partial"]

@@ -187,3 +187,26 @@ def test_library_fails_loudly_without_a_gpu():
         _kernels.chunk_sum(np.zeros(3, np.uint64), np.zeros(3, np.uint64), 3, 1, 8)
     with pytest.raises(RuntimeError):
         tp.perm_mod3_parallel(tp.MatrixF3([[1, 1], [1, 1]]), jobs=2)
+
+
+def test_pi_matrix_matches_reference():
+    for rec in load_golden("pi.json")["pi_matrix"]:
+        n = rec["n"]
+        m = tp.pi_matrix(n, skip_integer_part=rec["skip_integer_part"])
+        assert np.array_equal(m.classes(), dec(rec["a"], n)), (n, rec["skip_integer_part"])
+    assert tp.pi_matrix(3).rows == ((0, 1, 1), (1, -1, 0), (-1, 0, -1))
+    with pytest.raises(ValueError):
+        tp.pi_matrix(0)
+    with pytest.raises(ValueError):
+        tp.pi_matrix(101)
+    assert tp.pi_matrix(100).n == 100
+    with pytest.raises(ValueError):
+        tp.pi_matrix(100, skip_integer_part=True)
+
+
+def test_pi_digits_spot_values():
+    from paper_2407_20205_b200 import pi
+
+    d = pi.pi_digits()
+    assert len(d) == 10000 and d.startswith("314159265358979323846")
+    assert pi.pi_digit(1) == 3 and pi.pi_digit(2) == 1
