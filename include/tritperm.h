@@ -121,6 +121,12 @@ int tp_walk_async(const void *d_rows, int64_t B, int n, int device,
 int tp_finalize_async(const uint64_t *d_pm, int64_t B, int n, int device,
                       int8_t *d_class, int64_t *d_hist, void *stream);
 
+/* Exact census over all 3^(n^2) matrices, 1 <= n <= 6: counts of
+ * perm mod 3 = 0, +1, -1.  Replaces exact_count_kernel (src/_kernels.py:164-209,
+ * which enumerates and stops at n = 4); here two Laplace expansions reduce
+ * it to 3^((n-2) n) rank computations over F3 (see csrc/tp_census.cu). */
+int tp_exact_census(int n, int device, int64_t *zeros, int64_t *plus, int64_t *minus);
+
 /* Diagnostics: measured LOP3 throughput of `device` (ops/s, the ALU-pipe
  * roofline denominator) from a register-resident lop3 chain kernel timed
  * with CUDA events, and the kernel's duration in ms. */

@@ -19,8 +19,10 @@ from .core_f3 import (
     sub_reps,
 )
 from .experiments import (
+    ExactCountResult,
     McHistogram,
     McResult,
+    exact_zero_count,
     montecarlo_hist,
     montecarlo_zero,
     sample_trial_matrix,
@@ -44,6 +46,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "ChunkResult",
+    "ExactCountResult",
     "MatrixF3",
     "McHistogram",
     "McResult",
@@ -52,6 +55,7 @@ __all__ = [
     "cmod3",
     "decode",
     "encode",
+    "exact_zero_count",
     "is_full_magnitude",
     "montecarlo_hist",
     "montecarlo_zero",

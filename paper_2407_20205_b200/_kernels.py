@@ -70,6 +70,7 @@ SIGNATURES = {
     "tp_finalize_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "tp_debug_trace": (ctypes.c_int, [ctypes.c_void_p]),
+    "tp_exact_census": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _i64p, _i64p, _i64p]),
     "tp_alu_peak": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
 }
 
@@ -232,6 +233,13 @@ def alu_peak(device: Optional[int] = None) -> Tuple[float, float]:
     ms = ctypes.c_double()
     _check(lib().tp_alu_peak(dev, ctypes.byref(ops), ctypes.byref(ms)))
     return float(ops.value), float(ms.value)
+
+
+def exact_census(n: int) -> Tuple[int, int, int]:
+    """(zeros, plus_ones, minus_ones) of perm mod 3 over all n x n matrices."""
+    z, p, m = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().tp_exact_census(n, default_device(), ctypes.byref(z), ctypes.byref(p), ctypes.byref(m)))
+    return int(z.value), int(p.value), int(m.value)
 
 
 def mc_zero_count(n: int, t0: int, t1: int, seed: int) -> int:

@@ -72,6 +72,7 @@ cudaError_t launch_sample(int n, long long t0, long long count, unsigned long lo
 cudaError_t launch_finalize(const unsigned long long* pm, long long B, int n, int8_t* cls, long long* partial,
                             long long* hist, cudaStream_t st);
 cudaError_t run_alu_peak(int sm_count, uint32_t* scratch, cudaStream_t st, double* ops_per_s, double* ms);
+cudaError_t launch_census(int n, int grid, unsigned long long configs, unsigned long long* n0, cudaStream_t st);
 cudaError_t launch_selftest(const uint32_t* in, int count, int op, uint32_t* out, cudaStream_t st);
 
 }  // namespace tp

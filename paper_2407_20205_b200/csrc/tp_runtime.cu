@@ -586,6 +586,37 @@ int tp_debug_trace(void* d_trace) {
   return TP_OK;
 }
 
+int tp_exact_census(int n, int device, int64_t* zeros, int64_t* plus, int64_t* minus) {
+  if (n < 1 || n > 6) return fail(TP_E_INVALID, "exact census supports 1 <= n <= 6, got n=%d", n);
+  if (!zeros || !plus || !minus) return fail(TP_E_INVALID, "outputs must not be NULL");
+  if (n == 1) {  // perm = the entry
+    *zeros = *plus = *minus = 1;
+    return TP_OK;
+  }
+  Device* d;
+  int rc = ensure_device(device, &d);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(d->mu);
+  TP_CUDA(cudaSetDevice(device));
+  if ((rc = ensure_ws(*d, 256))) return rc;
+  unsigned long long* n0 = static_cast<unsigned long long*>(d->ws);
+  unsigned long long configs = 1;
+  for (int e = 0; e < (n - 2) * n; ++e) configs *= 3ull;
+  TP_CUDA(cudaMemsetAsync(n0, 0, sizeof(unsigned long long), d->stream));
+  const unsigned long long blocks = (configs + 255) / 256;
+  const int grid = (int)std::min<unsigned long long>(blocks, (unsigned long long)d->sm_count * 16);
+  TP_CUDA(tp::launch_census(n, grid, configs, n0, d->stream));
+  unsigned long long N0 = 0;
+  TP_CUDA(cudaMemcpyAsync(&N0, n0, sizeof N0, cudaMemcpyDeviceToHost, d->stream));
+  TP_CUDA(cudaStreamSynchronize(d->stream));
+  unsigned long long p3 = 1, q3 = 1;  // 3^(n-1), 3^(n(n-1))
+  for (int e = 0; e < n - 1; ++e) p3 *= 3ull;
+  for (int e = 0; e < n * (n - 1); ++e) q3 *= 3ull;
+  *zeros = (int64_t)(p3 * q3 + 2ull * p3 * N0);
+  *plus = *minus = (int64_t)(p3 * (q3 - N0));
+  return TP_OK;
+}
+
 int tp_alu_peak(int device, double* lop3_ops_per_s, double* ms) {
   if (!lop3_ops_per_s) return fail(TP_E_INVALID, "lop3_ops_per_s must not be NULL");
   Device* d;

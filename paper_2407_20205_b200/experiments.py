@@ -21,6 +21,33 @@ from . import _kernels, rng
 from .permanent import MAX_N, MatrixF3, resolve_jobs
 
 MC_MAX_N = 63  # the reference's guard (src/experiments.py:39); the kernels go to MAX_N
+EXACT_MAX_N = 6  # the reference stops at 4 (src/experiments.py:37)
+
+
+@dataclass(frozen=True)
+class ExactCountResult:
+    """Exact census of perm mod 3 over all n x n trit matrices (src/experiments.py:41-60)."""
+
+    n: int
+    z: int
+    plus_ones: int
+    minus_ones: int
+    total: int
+
+    @property
+    def ratio(self) -> float:
+        return self.z / self.total
+
+
+def exact_zero_count(n: int) -> ExactCountResult:
+    """Census of permanent values over all 3**(n*n) matrices, n <= 6, on the GPU
+    (tp_exact_census; the reference enumerates and refuses n > 4)."""
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    if n > EXACT_MAX_N:
+        raise ValueError(f"exact census supports n <= {EXACT_MAX_N} (3**{(n - 2) * n} rank computations)")
+    z, p, m = _kernels.exact_census(n)
+    return ExactCountResult(n=n, z=z, plus_ones=p, minus_ones=m, total=3 ** (n * n))
 
 
 @dataclass(frozen=True)

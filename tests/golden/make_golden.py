@@ -267,12 +267,27 @@ def pi_goldens():
     dump("pi.json", out)
 
 
+def census_goldens():
+    """exact_zero_count(1..4) from the reference (src/experiments.py:113-140);
+    z(5) is the paper's published value (Table 3), which the
+    reference refuses to compute."""
+    out = []
+    for n in (1, 2, 3, 4):
+        t0 = time.time()
+        r = ref_exp.exact_zero_count(n)
+        out.append({"n": n, "z": r.z, "plus": r.plus_ones, "minus": r.minus_ones, "total": r.total,
+                    "source": "reference exact_zero_count"})
+        print(f"census n={n}: {r.z} ({time.time() - t0:.1f}s)")
+    out.append({"n": 5, "z": 317193401763, "total": 3 ** 25, "source": "PAPER.md:245 (Table 3)"})
+    dump("census.json", {"census": out})
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--with-slow", action="store_true")
     ap.add_argument("--only", default=None)
     args = ap.parse_args()
-    jobs = {"core": core_ops, "rng": rng_vectors, "chunks": chunks, "tower": tower, "pi": pi_goldens,
+    jobs = {"core": core_ops, "rng": rng_vectors, "chunks": chunks, "tower": tower, "pi": pi_goldens, "census": census_goldens,
             "anchors": lambda: anchors(args.with_slow)}
     if args.with_slow:
         jobs["oracle"] = oracle_goldens

@@ -316,3 +316,15 @@ def test_pi_matrices_and_pi50_windows(gpu):
     for w in g["windows"]:
         m = gpu.pi_matrix(50, skip_integer_part=w["skip_integer_part"])
         assert gpu.perm_chunk(m, w["lo"], w["hi"]).partial_sum == w["partial"]
+
+
+def test_exact_census_matches_reference_and_paper(gpu):
+    """z(1..4) and the +-1 split from the reference's exact_zero_count; z(5)
+    from the paper's Table 3 (the reference refuses n = 5)."""
+    for rec in load_golden("census.json")["census"]:
+        r = gpu.exact_zero_count(rec["n"])
+        assert r.z == rec["z"] and r.total == rec["total"], rec
+        assert r.z + r.plus_ones + r.minus_ones == r.total
+        assert r.plus_ones == r.minus_ones
+        if "plus" in rec:
+            assert (r.plus_ones, r.minus_ones) == (rec["plus"], rec["minus"])

@@ -210,3 +210,10 @@ def test_pi_digits_spot_values():
     d = pi.pi_digits()
     assert len(d) == 10000 and d.startswith("314159265358979323846")
     assert pi.pi_digit(1) == 3 and pi.pi_digit(2) == 1
+
+
+def test_exact_census_guards():
+    with pytest.raises(ValueError):
+        tp.exact_zero_count(0)
+    with pytest.raises(ValueError):
+        tp.exact_zero_count(7)
