@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--c5-log2-steps", type=int, default=44,
                     help="c5: subset terms per step (a 2^k window of the 2^50 range)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", type=int, default=None,
+                    help="replay each step from a CUDA graph (default: on for the single small matrix c1)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample time")
     return ap.parse_args()
 
@@ -213,6 +215,8 @@ def run_reference(args):
 
 def main():
     args = parse()
+    if args.graph is None:
+        args.graph = 1 if args.workload == "c1" else 0
     if args.impl == "reference":
         run_reference(args)
         return
@@ -243,24 +247,30 @@ def main():
     step_ms = []
 
     if wl == "c5" or wl in ("c1", "c4"):
-        # single matrix: the step range is split across ranks (strong scaling)
+        # single matrix: the step range is split across ranks (strong scaling);
+        # entries resident in HBM, packed and walked every step
         a = make_entries(wl, 0)[0]
-        m = tp.MatrixF3(a.astype(np.int64))
-        mags, sgns = m.planes()
         span = terms_per_step(wl, args)
         lo0 = (1 << 40) if wl == "c5" else 0
         part = (span * rank // world, span * (rank + 1) // world)
+        d_e = torch.from_numpy(np.ascontiguousarray(a[None])).to(dev)
+        d_rows = torch.empty((1, _kernels.ROWREC_BYTES), dtype=torch.uint8, device=dev)
         d_pm = torch.zeros(2, dtype=torch.int64, device=dev)
 
-        def step():
+        def step(timed_walk=True):
             nonlocal launches
+            s = torch.cuda.current_stream().cuda_stream
             d_pm.zero_()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            _kernels.chunk_counts_async(mags, sgns, n, lo0 + part[0], lo0 + part[1], d_pm.data_ptr(), sptr)
-            e1.record(stream)
-            launches += 1 if span >= (1 << 12) else 2
+            _kernels.pack_async(d_e.data_ptr(), 1, n, d_rows.data_ptr(), s)
+            e0 = e1 = None
+            if timed_walk:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+            nl = _kernels.walk_range_async(d_rows.data_ptr(), n, lo0 + part[0], lo0 + part[1], d_pm.data_ptr(), s)
+            if timed_walk:
+                e1.record()
+            launches += 1 + nl
             if world > 1:
                 dist.all_reduce(d_pm)
             return e0, e1
@@ -274,17 +284,21 @@ def main():
         d_cls = torch.empty(B, dtype=torch.int8, device=dev)
         d_hist = torch.zeros(3, dtype=torch.int64, device=dev)
 
-        def step():
+        def step(timed_walk=True):
             nonlocal launches
+            s = torch.cuda.current_stream().cuda_stream
             d_pm.zero_()
             d_hist.zero_()
-            _kernels.pack_async(d_e.data_ptr(), B, n, d_rows.data_ptr(), sptr)
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            nl = _kernels.walk_async(d_rows.data_ptr(), B, n, d_pm.data_ptr(), sptr)
-            e1.record(stream)
-            _kernels.finalize_async(d_pm.data_ptr(), B, n, d_cls.data_ptr(), d_hist.data_ptr(), sptr)
+            _kernels.pack_async(d_e.data_ptr(), B, n, d_rows.data_ptr(), s)
+            e0 = e1 = None
+            if timed_walk:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+            nl = _kernels.walk_async(d_rows.data_ptr(), B, n, d_pm.data_ptr(), s)
+            if timed_walk:
+                e1.record()
+            _kernels.finalize_async(d_pm.data_ptr(), B, n, d_cls.data_ptr(), d_hist.data_ptr(), s)
             launches += 2 + nl
             if world > 1:
                 dist.all_reduce(d_hist)
@@ -295,6 +309,23 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+
+    # Launch-bound steps (single small matrices) are replayed from a CUDA
+    # graph of the whole step (pack -> walk -> finalize); the walk kernel's own
+    # time for the roofline then comes from a separate evented loop.
+    graph = None
+    if args.graph and world == 1:
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            step(timed_walk=False)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step(timed_walk=False)
+        torch.cuda.synchronize()
+    per_step_launches = None
     launches = 0
 
     # timed region: K steps, L2 flushed (memset of 256 MiB) between steps,
@@ -308,16 +339,30 @@ def main():
             flush.zero_()
             s0 = torch.cuda.Event(enable_timing=True)
             s1 = torch.cuda.Event(enable_timing=True)
-            s0.record(stream)
-            w = step()
-            s1.record(stream)
+            s0.record()
+            if graph is not None:
+                graph.replay()
+                w = (None, None)
+            else:
+                w = step()
+            s1.record()
             evs.append((s0, s1, w))
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     for s0, s1, (w0, w1) in evs:
         step_ms.append(s0.elapsed_time(s1))
-        walk_ms.append(w0.elapsed_time(w1))
+        if w0 is not None:
+            walk_ms.append(w0.elapsed_time(w1))
+    if graph is not None:
+        launches = 0
+        wev = []
+        for _ in range(args.steps):
+            wev.append(step())
+        torch.cuda.synchronize()
+        per_step_launches = launches // args.steps
+        launches = per_step_launches * args.steps
+        walk_ms = [a.elapsed_time(b) for a, b in wev]
     total_ms = sum(step_ms)
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -396,6 +441,7 @@ def main():
             "data": "synthetic (reference per-trial splitmix64 stream; no dataset involved)",
             "config": {"workload": desc, "n": n, "batch": B, "seed": SEED, "parallelism": f"dp{world}",
                        "l2": "flushed between steps (256 MiB memset, untimed by the walk events)",
+                       "cuda_graph": bool(graph is not None),
                        "terms_per_step": job_terms},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "LOP3 ops/s",
                          "frac": achieved / peak, "traffic": traffic,

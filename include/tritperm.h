@@ -118,6 +118,11 @@ int tp_pack_async(const uint8_t *d_entries, int64_t B, int n, int device,
                   void *d_rows, void *stream);
 int tp_walk_async(const void *d_rows, int64_t B, int n, int device,
                   uint64_t *d_pm, void *stream, int *launches);
+/* Range walk [lo, hi) of ONE matrix whose rows are already packed on the
+ * device (d_rows from tp_pack_async with B = 1); ADDS {plus, minus} into
+ * d_pm[2].  Same contract as tp_range_sum_async without the host planes. */
+int tp_walk_range_async(const void *d_rows, int n, uint64_t lo, uint64_t hi, int device,
+                        uint64_t *d_pm, void *stream, int *launches);
 int tp_finalize_async(const uint64_t *d_pm, int64_t B, int n, int device,
                       int8_t *d_class, int64_t *d_hist, void *stream);
 

@@ -67,6 +67,8 @@ SIGNATURES = {
                                      ctypes.c_void_p]),
     "tp_walk_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
                                      ctypes.c_void_p, _ip]),
+    "tp_walk_range_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64,
+                                           ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, _ip]),
     "tp_finalize_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "tp_debug_trace": (ctypes.c_int, [ctypes.c_void_p]),
@@ -216,6 +218,16 @@ def walk_async(d_rows_ptr: int, B: int, n: int, d_pm_ptr: int, stream_ptr: int, 
     nl = ctypes.c_int(0)
     _check(lib().tp_walk_async(ctypes.c_void_p(d_rows_ptr), B, n, dev, ctypes.c_void_p(d_pm_ptr),
                                ctypes.c_void_p(stream_ptr), ctypes.byref(nl)))
+    return int(nl.value)
+
+
+def walk_range_async(d_rows_ptr: int, n: int, lo: int, hi: int, d_pm_ptr: int, stream_ptr: int,
+                     device: Optional[int] = None) -> int:
+    """Range walk of one device-packed matrix; returns the kernel launches."""
+    dev = default_device() if device is None else device
+    nl = ctypes.c_int(0)
+    _check(lib().tp_walk_range_async(ctypes.c_void_p(d_rows_ptr), n, lo, hi, dev, ctypes.c_void_p(d_pm_ptr),
+                                     ctypes.c_void_p(stream_ptr), ctypes.byref(nl)))
     return int(nl.value)
 
 

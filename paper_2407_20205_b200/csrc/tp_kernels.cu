@@ -634,6 +634,7 @@ cudaError_t run_alu_peak(int sm_count, uint32_t* scratch, cudaStream_t st, doubl
 // ---------------------------------------------------------------------------
 // Walk variants (see tp_kernels.cuh FastVariant).
 #define TP_FAST_VARIANTS(X)              \
+  X(kLaneV5W4, k_walk_lane<5, 4>)        \
   X(kLaneV7W4, k_walk_lane<7, 4>)        \
   X(kLaneV8W4, k_walk_lane<8, 4>)        \
   X(kWideK2V7W4, k_walk_wide<1, 7, 4>)   \

@@ -21,11 +21,18 @@ enum FastVariant {
   kWideK4V6W4 = 3,
   kWideK8V5W4 = 4,
   kWideK8V6W4 = 5,
-  kNumFast = 6
+  kLaneV5W4 = 6,
+  kNumFast = 7
 };
-constexpr bool fast_is_lane(int v) { return v <= kLaneV8W4; }
+constexpr bool fast_is_lane(int v) { return v <= kLaneV8W4 || v == kLaneV5W4; }
 constexpr int fast_v(int v) {
-  return v == kLaneV7W4 ? 7 : v == kLaneV8W4 ? 8 : v == kWideK2V7W4 ? 7 : v == kWideK4V6W4 ? 6 : v == kWideK8V5W4 ? 5 : 6;
+  return v == kLaneV5W4 ? 5
+       : v == kLaneV7W4 ? 7
+       : v == kLaneV8W4 ? 8
+       : v == kWideK2V7W4 ? 7
+       : v == kWideK4V6W4 ? 6
+       : v == kWideK8V5W4 ? 5
+                          : 6;
 }
 constexpr int fast_kb(int v) {
   return fast_is_lane(v) ? 0 : v == kWideK2V7W4 ? 1 : v == kWideK4V6W4 ? 2 : 3;

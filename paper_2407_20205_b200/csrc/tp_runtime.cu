@@ -157,7 +157,8 @@ int choose_variant(int n) {
     forced = e ? atoi(e) : -1;
   }
   if (forced >= 0 && forced < tp::kNumFast && tp::fast_is_lane(forced) == (n <= 32)) return forced;
-  if (n <= 32) return n >= 22 ? tp::kLaneV8W4 : tp::kLaneV7W4;
+  // short walks (n <= 21, <= 2^16 high steps) favour parallelism: more, smaller items
+  if (n <= 32) return n >= 22 ? tp::kLaneV8W4 : tp::kLaneV5W4;
   return tp::kWideK4V6W4;
 }
 
@@ -560,6 +561,22 @@ int tp_walk_async(const void* d_rows, int64_t B, int n, int device, uint64_t* d_
   make_plan(*d, n, (unsigned long long)B, 0, 0, true, static_cast<const RowRec*>(d_rows),
             reinterpret_cast<unsigned long long*>(d_pm), pl);
   return run_plan(pl, st, launches);
+}
+
+int tp_walk_range_async(const void* d_rows, int n, uint64_t lo, uint64_t hi, int device, uint64_t* d_pm,
+                        void* stream, int* launches) {
+  int rc = check_range(n, lo, hi);
+  if (rc) return rc;
+  if (!d_rows || !d_pm) return fail(TP_E_INVALID, "buffers must not be NULL");
+  if (launches) *launches = 0;
+  Device* d;
+  if ((rc = ensure_device(device, &d))) return rc;
+  std::lock_guard<std::mutex> lk(d->mu);
+  TP_CUDA(cudaSetDevice(device));
+  Plan pl;
+  make_plan(*d, n, 1, lo, hi, false, static_cast<const RowRec*>(d_rows), reinterpret_cast<unsigned long long*>(d_pm),
+            pl);
+  return run_plan(pl, static_cast<cudaStream_t>(stream), launches);
 }
 
 int tp_finalize_async(const uint64_t* d_pm, int64_t B, int n, int device, int8_t* d_class, int64_t* d_hist,
