@@ -328,3 +328,38 @@ def test_exact_census_matches_reference_and_paper(gpu):
         assert r.plus_ones == r.minus_ones
         if "plus" in rec:
             assert (r.plus_ones, r.minus_ones) == (rec["plus"], rec["minus"])
+
+
+def _ones_partial(n):
+    """Raw Gray partial sum of the all-ones n x n matrix in closed form:
+    v_S = |S| (1,...,1), so the term is 0, 1 or (-1)^n for |S| = 0, 1, 2 mod 3."""
+    from math import comb
+
+    s = 0
+    for k in range(n + 1):
+        if k % 3 == 1:
+            s += comb(n, k) * (-1) ** k
+        elif k % 3 == 2:
+            s += comb(n, k) * (-1) ** k * (-1) ** n
+    return s
+
+
+def test_event_dense_matrices_exact(gpu):
+    """All-ones matrices: 2/3 of all subsets are full-magnitude events, which
+    drives the lane walk's exact mode (n <= 32) and the wide walk's dense mode
+    (n > 32) through every superblock; raw partials must stay exact."""
+    for n in (14, 20, 24, 31, 32, 33, 34, 36):
+        m = gpu.MatrixF3([[1] * n for _ in range(n)])
+        assert gpu.perm_chunk(m, 1, 1 << n).partial_sum == _ones_partial(n), n
+        assert gpu.perm_mod3_fast(m) == (0 if n >= 3 else 1)
+    # dense and sparse matrices mixed in one batch
+    from paper_2407_20205_b200 import fixtures
+
+    e = np.concatenate([np.ones((3, 26, 26), np.uint8), fixtures.uniform_batch(26, 9, 0, 3)])
+    cls, part, _ = gpu.perm_mod3_batch(e)
+    assert part[0] == _ones_partial(26) and cls[0] == 0
+    from oracle import oracle as o
+
+    for b in range(3, 6):
+        mags, sgns = o.planes_from_classes(e[b])
+        assert part[b] == o.chunk_sum(mags, sgns, 26, 1, 1 << 26)
