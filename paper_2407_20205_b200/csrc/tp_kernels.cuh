@@ -8,6 +8,8 @@
 namespace tp {
 
 constexpr int kWalkThreads = 256;  // 8 warps per CTA
+constexpr int kSmallMaxN = 13;      // thread-per-matrix kernel (tp_small.cu) for n <= 13
+constexpr int kSmallThreads = 128;
 // Fast-walk variants.  Lane walk (n <= 32): one subset per lane, superblock
 // 2^V high steps of 32 reference steps.  Wide walk (n > 32): 2^KB subsets per
 // lane, superblock 2^V high steps of 32 * 2^KB reference steps.
@@ -79,6 +81,8 @@ cudaError_t launch_sample(int n, long long t0, long long count, unsigned long lo
 cudaError_t launch_finalize(const unsigned long long* pm, long long B, int n, int8_t* cls, long long* partial,
                             long long* hist, cudaStream_t st);
 cudaError_t run_alu_peak(int sm_count, uint32_t* scratch, cudaStream_t st, double* ops_per_s, double* ms);
+cudaError_t launch_small(int n, long long B, const uint8_t* entries, long long t0, unsigned long long seed,
+                         int8_t* cls, long long* partial, unsigned long long* pm, long long* hist, cudaStream_t st);
 cudaError_t launch_census(int n, int grid, unsigned long long configs, unsigned long long* n0, cudaStream_t st);
 cudaError_t launch_selftest(const uint32_t* in, int count, int op, uint32_t* out, cudaStream_t st);
 

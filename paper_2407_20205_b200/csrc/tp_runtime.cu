@@ -515,6 +515,11 @@ int tp_perm_batch_async(const uint8_t* d_entries, int64_t B, int n, int device, 
       d_pm ? reinterpret_cast<unsigned long long*>(d_pm) : c2.take<unsigned long long>(base, (size_t)B * 2);
   int nl = 0;
   TP_CUDA(cudaMemsetAsync(pm, 0, (size_t)B * 2 * sizeof(unsigned long long), st));
+  if (n <= tp::kSmallMaxN) {  // thread per matrix: pack + walk + finalise in one kernel
+    TP_CUDA(tp::launch_small(n, B, d_entries, 0, 0, d_class, nullptr, pm, reinterpret_cast<long long*>(d_hist), st));
+    if (launches) *launches = 1;
+    return TP_OK;
+  }
   const int pack_grid = (int)std::min<long long>((B + 7) / 8, (long long)d->sm_count * 8);
   TP_CUDA(tp::launch_pack(d_entries, B, n, rows, pack_grid, st));
   nl++;
@@ -682,14 +687,18 @@ int tp_perm_batch(const uint8_t* entries, int64_t B, int n, int device, int8_t* 
   long long* dpart = c2.take<long long>(base, (size_t)B);
   long long* dhist = c2.take<long long>(base, 3);
   TP_CUDA(cudaMemcpyAsync(dent, entries, ebytes, cudaMemcpyHostToDevice, st));
-  TP_CUDA(cudaMemsetAsync(pm, 0, (size_t)B * 2 * sizeof(unsigned long long), st));
   TP_CUDA(cudaMemsetAsync(dhist, 0, 3 * sizeof(long long), st));
-  const int pack_grid = (int)std::min<long long>((B + 7) / 8, (long long)d->sm_count * 8);
-  TP_CUDA(tp::launch_pack(dent, B, n, rows, pack_grid, st));
-  Plan pl;
-  make_plan(*d, n, (unsigned long long)B, 0, 0, true, rows, pm, pl);
-  if ((rc = run_plan(pl, st, nullptr))) return rc;
-  TP_CUDA(tp::launch_finalize(pm, B, n, dcls, dpart, dhist, st));
+  if (n <= tp::kSmallMaxN) {
+    TP_CUDA(tp::launch_small(n, B, dent, 0, 0, dcls, dpart, nullptr, dhist, st));
+  } else {
+    TP_CUDA(cudaMemsetAsync(pm, 0, (size_t)B * 2 * sizeof(unsigned long long), st));
+    const int pack_grid = (int)std::min<long long>((B + 7) / 8, (long long)d->sm_count * 8);
+    TP_CUDA(tp::launch_pack(dent, B, n, rows, pack_grid, st));
+    Plan pl;
+    make_plan(*d, n, (unsigned long long)B, 0, 0, true, rows, pm, pl);
+    if ((rc = run_plan(pl, st, nullptr))) return rc;
+    TP_CUDA(tp::launch_finalize(pm, B, n, dcls, dpart, dhist, st));
+  }
   if (out_class) TP_CUDA(cudaMemcpyAsync(out_class, dcls, (size_t)B, cudaMemcpyDeviceToHost, st));
   if (out_partial) TP_CUDA(cudaMemcpyAsync(out_partial, dpart, (size_t)B * 8, cudaMemcpyDeviceToHost, st));
   long long hh[3];
@@ -716,29 +725,34 @@ static int mc_run(int n, int64_t t0, int64_t count, uint64_t seed, int device, i
   std::lock_guard<std::mutex> lk(d->mu);
   TP_CUDA(cudaSetDevice(device));
   cudaStream_t st = d->stream;
-  const int64_t slab = std::min<int64_t>(count, 1 << 16);
+  const bool small = n <= tp::kSmallMaxN;  // thread-per-trial kernel needs no row table
+  const int64_t slab = std::min<int64_t>(count, small ? (1ll << 24) : (1ll << 16));
+  const size_t nrows = small ? 0 : (size_t)slab * 64, npm = small ? 0 : (size_t)slab * 2;
   Carve cv;
-  cv.take<RowRec>(nullptr, (size_t)slab * 64);
-  cv.take<unsigned long long>(nullptr, 1);
-  cv.take<unsigned long long>(nullptr, (size_t)slab * 2);
+  cv.take<RowRec>(nullptr, nrows);
+  cv.take<unsigned long long>(nullptr, npm);
   cv.take<int8_t>(nullptr, (size_t)slab);
   cv.take<long long>(nullptr, 3);
   if ((rc = ensure_ws(*d, cv.off))) return rc;
   char* base = static_cast<char*>(d->ws);
   Carve c2;
-  RowRec* rows = c2.take<RowRec>(base, (size_t)slab * 64);
-  unsigned long long* pm = c2.take<unsigned long long>(base, (size_t)slab * 2);
+  RowRec* rows = c2.take<RowRec>(base, nrows);
+  unsigned long long* pm = c2.take<unsigned long long>(base, npm);
   int8_t* dcls = c2.take<int8_t>(base, (size_t)slab);
   long long* dhist = c2.take<long long>(base, 3);
   TP_CUDA(cudaMemsetAsync(dhist, 0, 3 * sizeof(long long), st));
   for (int64_t s0 = 0; s0 < count; s0 += slab) {
     const int64_t B = std::min<int64_t>(slab, count - s0);
-    TP_CUDA(cudaMemsetAsync(pm, 0, (size_t)B * 2 * sizeof(unsigned long long), st));
-    TP_CUDA(tp::launch_sample(n, t0 + s0, B, seed, rows, nullptr, st));
-    Plan pl;
-    make_plan(*d, n, (unsigned long long)B, 0, 0, true, rows, pm, pl);
-    if ((rc = run_plan(pl, st, nullptr))) return rc;
-    TP_CUDA(tp::launch_finalize(pm, B, n, dcls, nullptr, dhist, st));
+    if (n <= tp::kSmallMaxN) {  // sample + walk + finalise, thread per trial
+      TP_CUDA(tp::launch_small(n, B, nullptr, t0 + s0, seed, out_class ? dcls : nullptr, nullptr, nullptr, dhist, st));
+    } else {
+      TP_CUDA(cudaMemsetAsync(pm, 0, (size_t)B * 2 * sizeof(unsigned long long), st));
+      TP_CUDA(tp::launch_sample(n, t0 + s0, B, seed, rows, nullptr, st));
+      Plan pl;
+      make_plan(*d, n, (unsigned long long)B, 0, 0, true, rows, pm, pl);
+      if ((rc = run_plan(pl, st, nullptr))) return rc;
+      TP_CUDA(tp::launch_finalize(pm, B, n, dcls, nullptr, dhist, st));
+    }
     if (out_class) TP_CUDA(cudaMemcpyAsync(out_class + s0, dcls, (size_t)B, cudaMemcpyDeviceToHost, st));
     if (out_class) TP_CUDA(cudaStreamSynchronize(st));
   }
