@@ -80,11 +80,12 @@ __device__ __forceinline__ int tz64(unsigned long long a) {
   return lo ? __ffs(lo) - 1 : 31 + __ffs((uint32_t)(a >> 32));
 }
 
-__device__ __forceinline__ void load_rows(RowRec* R, const RowRec* src, uint32_t lane) {
+// Copy rows 0..n-1 (two uint4 per 32-byte RowRec); rows >= n stay stale and
+// are never read by the walks (row indices are < n).
+__device__ __forceinline__ void load_rows(RowRec* R, const RowRec* src, uint32_t lane, int n) {
   const uint4* s = reinterpret_cast<const uint4*>(src);
   uint4* d = reinterpret_cast<uint4*>(R);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) d[lane + 32 * q] = s[lane + 32 * q];
+  for (int q = lane; q < 2 * n; q += 32) d[q] = s[q];
 }
 
 // Broadcast through REDUX (__reduce_or_sync), whose result lands in a
@@ -144,7 +145,7 @@ __global__ void __launch_bounds__(32 * WARPS) k_walk_lane(FastParams p) {
     const unsigned long long A0 = p.F0 + (item - b * p.chunks) * p.L;
     const unsigned long long B0 = A0 >> V;
     __syncwarp();
-    load_rows(R, p.rows + b * 64, lane);
+    load_rows(R, p.rows + b * 64, lane, p.n);
     __syncwarp();
 
     uint32_t SM[V], SS[V], SA[V];
@@ -329,7 +330,7 @@ __global__ void __launch_bounds__(32 * WARPS) k_walk_wide(FastParams p) {
     const unsigned long long A0 = p.F0 + (item - b * p.chunks) * p.L;
     const unsigned long long B0 = A0 >> V;
     __syncwarp();
-    load_rows(R, p.rows + b * 64, lane);
+    load_rows(R, p.rows + b * 64, lane, p.n);
     __syncwarp();
 
     uint32_t SM[V], SS[V], SA[V];
@@ -497,7 +498,7 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk_generic(GenericParams p) 
     const unsigned long long rend = r ? p.reg_a1[1] : p.reg_a1[0];
     const unsigned long long a1 = (a0 + p.glen < rend) ? a0 + p.glen : rend;
     __syncwarp();
-    load_rows(R, p.rows + b * 64, lane);
+    load_rows(R, p.rows + b * 64, lane, p.n);
     __syncwarp();
     uint32_t z[2], g[2];
     seed_state<NW>(R, p.n, a0, lane, p.z0_init, p.z1_init, z, g);

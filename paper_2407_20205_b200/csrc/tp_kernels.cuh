@@ -8,7 +8,7 @@
 namespace tp {
 
 constexpr int kWalkThreads = 256;  // 8 warps per CTA
-constexpr int kSmallMaxN = 13;      // thread-per-matrix kernel (tp_small.cu) for n <= 13
+constexpr int kSmallMaxN = 15;      // thread-per-matrix kernel (tp_small.cu) for n <= 15
 constexpr int kSmallThreads = 128;
 // Fast-walk variants.  Lane walk (n <= 32): one subset per lane, superblock
 // 2^V high steps of 32 reference steps.  Wide walk (n > 32): 2^KB subsets per

@@ -726,7 +726,8 @@ static int mc_run(int n, int64_t t0, int64_t count, uint64_t seed, int device, i
   TP_CUDA(cudaSetDevice(device));
   cudaStream_t st = d->stream;
   const bool small = n <= tp::kSmallMaxN;  // thread-per-trial kernel needs no row table
-  const int64_t slab = std::min<int64_t>(count, small ? (1ll << 24) : (1ll << 16));
+  // slabs large enough that mid-size n get whole-matrix items (row table 2 KB per trial)
+  const int64_t slab = std::min<int64_t>(count, small ? (1ll << 24) : n <= 22 ? (1ll << 20) : (1ll << 16));
   const size_t nrows = small ? 0 : (size_t)slab * 64, npm = small ? 0 : (size_t)slab * 2;
   Carve cv;
   cv.take<RowRec>(nullptr, nrows);

@@ -211,21 +211,22 @@ def test_batch_async_device_pointers(gpu):
 
     from paper_2407_20205_b200 import _kernels, fixtures
 
-    e = fixtures.uniform_batch(14, 3, 0, 257)
-    cls_h, part_h, hist_h = gpu.perm_mod3_batch(e)
-    d_e = torch.from_numpy(e).cuda()
-    d_cls = torch.empty(257, dtype=torch.int8, device="cuda")
-    d_pm = torch.empty((257, 2), dtype=torch.int64, device="cuda")
-    d_hist = torch.zeros(3, dtype=torch.int64, device="cuda")
-    st = torch.cuda.current_stream()
-    nl = _kernels.perm_batch_async(d_e.data_ptr(), 257, 14, d_cls.data_ptr(), d_pm.data_ptr(), d_hist.data_ptr(),
-                                   st.cuda_stream)
-    torch.cuda.synchronize()
-    assert nl >= 2
-    assert np.array_equal(d_cls.cpu().numpy(), cls_h)
-    pm = d_pm.cpu().numpy()
-    assert np.array_equal(pm[:, 0] - pm[:, 1], part_h)
-    assert d_hist.cpu().tolist() == hist_h.tolist()
+    for n, B, min_launches in ((14, 257, 1), (21, 65, 3)):  # thread-per-matrix path / pack+walk+finalize
+        e = fixtures.uniform_batch(n, 3, 0, B)
+        cls_h, part_h, hist_h = gpu.perm_mod3_batch(e)
+        d_e = torch.from_numpy(e).cuda()
+        d_cls = torch.empty(B, dtype=torch.int8, device="cuda")
+        d_pm = torch.empty((B, 2), dtype=torch.int64, device="cuda")
+        d_hist = torch.zeros(3, dtype=torch.int64, device="cuda")
+        st = torch.cuda.current_stream()
+        nl = _kernels.perm_batch_async(d_e.data_ptr(), B, n, d_cls.data_ptr(), d_pm.data_ptr(), d_hist.data_ptr(),
+                                       st.cuda_stream)
+        torch.cuda.synchronize()
+        assert nl >= min_launches
+        assert np.array_equal(d_cls.cpu().numpy(), cls_h)
+        pm = d_pm.cpu().numpy()
+        assert np.array_equal(pm[:, 0] - pm[:, 1], part_h)
+        assert d_hist.cpu().tolist() == hist_h.tolist()
 
 
 def test_abi_rejects_bad_arguments(gpu):
