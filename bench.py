@@ -372,9 +372,10 @@ def main():
     job_terms = per_rank_terms * world if scaling == "weak" else terms_per_step(wl, args)
     value = job_terms / (ms_per_step * 1e-3)
 
-    # ALU roofline of the walk kernel: 3 LOP3 per subset term for every n
-    # (n > 32 walks only the 32 primary columns)
-    ops_per_term = 3
+    # ALU roofline of the walk kernel: LOP3 per subset term of the kernel that
+    # served this n (2 for the pair walk, 3 for the lane/wide walks; n > 32
+    # tests only the 32 primary columns -- see DESIGN.md)
+    kernel_name, ops_per_term = _kernels.walk_info(n)
     walk_avg = sum(walk_ms) / len(walk_ms)
     achieved = per_rank_terms * ops_per_term / (walk_avg * 1e-3)
     peak, _ = _kernels.alu_peak(local)
@@ -445,7 +446,7 @@ def main():
                        "terms_per_step": job_terms},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "LOP3 ops/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": ("k_walk_lane" if n <= 32 else "k_walk_wide") + " (csrc/tp_kernels.cu)",
+                         "kernel": kernel_name + " (csrc/tp_kernels.cu)",
                          "ops_per_term": ops_per_term,
                          "peak_source": "LOP3 chain probe (tp_alu_peak) on this GPU in this run; "
                                         "nominal 148 SM x 64 lanes x clock",

@@ -475,6 +475,233 @@ __global__ void __launch_bounds__(32 * WARPS) k_walk_wide(FastParams p) {
 }
 
 // ---------------------------------------------------------------------------
+// Pair walk (meet in the middle), any n >= 5+KB+V+1.  Split the rows into
+// A = rows 0..h-1 (h = 5+KB: the lane bits and the K = 2^KB slot bits) and
+// B = rows h..n-1.  Every subset is S = S1 u S2 with v_S = v1 + v2; a lane
+// keeps its K A-side vectors v1 FIXED in registers and the warp walks only
+// the B-side vector v2 in Gray order.  The term is nonzero iff v1 + v2 has
+// no zero column, which is the first two LOP3 of the z-encoded sub of -v2:
+//     u2 = ~(z2 ^ g2)                     (once per step, shared by all pairs)
+//     d  = ~z1 & (g1 ^ u2)                lop3 0x06
+//     z' = ~d & ~(z1 ^ z2)                lop3 0x09, predicate z' != 0 free
+// and, only for a hit, the sign word is g' = d ^ g2.  So a subset costs 2
+// LOP3 (the walk costs 3) plus one predicated IMAD that adds
+// (id << 16) | 1 to a per-lane record: count in the low half, and the id of
+// the (step, slot) of a single hit in the high half.
+// n <= 32 (WIDE = false): the test is exact; the B-side states of the
+// superblock are kept in shared memory so a single hit's sign is
+// g' = d ^ g2(step) at the superblock end.  n > 32 (WIDE): the test covers
+// the 32 primary columns only; a hit is re-evaluated from scratch over all
+// n columns.  Two hits in one lane and superblock replay it exactly.
+// Subset of (lane l, slot k, high step a): S = (gray(a) << h) | (k << 5) | l,
+// the same indexing as the wide walk.
+// ---------------------------------------------------------------------------
+template <uint32_t IMM>
+__device__ __forceinline__ void pair_test(uint32_t z1, uint32_t g1, uint32_t z2, uint32_t u2, uint32_t& rec,
+                                          uint32_t one) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 d, zp;\n\t"
+      "lop3.b32 d, %1, %2, %4, 0x06;\n\t"
+      "lop3.b32 zp, d, %1, %3, 0x09;\n\t"
+      "setp.eq.u32 p, zp, 0;\n\t"
+      "@p mad.lo.u32 %0, %5, %6, %0;\n\t}"
+      : "+r"(rec)
+      : "r"(z1), "r"(g1), "r"(z2), "r"(u2), "r"(one), "n"(IMM));
+}
+
+__device__ __forceinline__ uint32_t pair_u2(uint32_t z2, uint32_t g2) {
+  uint32_t u;
+  TP_LOP3(u, z2, g2, 0u, 0xC3);
+  return u;
+}
+
+template <int KB, int V, int WARPS, bool WIDE>
+__global__ void __launch_bounds__(32 * WARPS) k_walk_pair(FastParams p) {
+  constexpr int K = 1 << KB;
+  constexpr int FIX = 5 + KB;
+  constexpr int SB = 1 << V;
+  __shared__ RowRec Rs[WARPS][64];
+  __shared__ uint2 Hs[WARPS][SB];  // B-side (z2, g2) at every step of the current superblock (n <= 32)
+  const uint32_t lane = threadIdx.x & 31u;
+  RowRec* R = Rs[threadIdx.x >> 5];
+  uint2* H = Hs[threadIdx.x >> 5];
+  const uint32_t lanepar = __popc(lane) & 1u;
+  const uint32_t one = p.one;
+  const uint32_t colmask = p.z0_init;  // real columns of the primary word
+  const unsigned long long t_start = p.trace ? clock64() : 0;
+  unsigned long long n_items = 0;
+
+  for (;;) {
+    const unsigned long long item = next_item(p.queue, lane);
+    if (item >= p.items) break;
+    ++n_items;
+    const unsigned long long b = item / p.chunks;
+    const unsigned long long A0 = p.F0 + (item - b * p.chunks) * p.L;
+    const unsigned long long B0 = A0 >> V;
+    __syncwarp();
+    load_rows(R, p.rows + b * 64, lane, p.n);
+    __syncwarp();
+
+    uint32_t SM[V], SS[V], SA[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      SM[v] = R[FIX + v].m[0];
+      SS[v] = R[FIX + v].s[0];
+      SA[v] = R[FIX + v].a[0];
+    }
+    // A side: v1 for S1 = (k << 5) | lane, k in Gray order (one row per slot)
+    uint32_t z1[K], g1[K];
+    {
+      uint32_t zz[2], gg[2];
+      wide_subset_state<KB>(R, p.n, 0ull, lane, p.z0_init, p.z1_init, zz, gg);
+      uint32_t zc = zz[0], gc = gg[0];
+      static_for<K>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        if constexpr (i > 0) {
+          constexpr int t = ctz_c(i);
+          constexpr bool leave = ((gray_c(i - 1) >> t) & 1) != 0;
+          sub_word(zc, gc, R[5 + t].m[0], leave ? R[5 + t].s[0] : R[5 + t].a[0]);
+        }
+        z1[gray_c(i)] = zc;
+        g1[gray_c(i)] = gc;
+      });
+    }
+    // B side: v2 for S2 = gray(A0) on rows >= h (low bits empty)
+    uint32_t z2, g2;
+    {
+      uint32_t zz[2], gg[2];
+      wide_subset_state<KB>(R, p.n, A0, 0u, p.z0_init, p.z1_init, zz, gg);
+      z2 = zz[0];
+      g2 = gg[0];
+    }
+    uint32_t ev = 0, odd = 0;
+    // Exact evaluation of every pair of the current superblock from the
+    // B-side history H (n <= 32): used for replays and in dense mode.
+    auto exact_block = [&](uint32_t& bev, uint32_t& bodd) {
+      bev = bodd = 0;
+      for (int j = 0; j < SB; ++j) {
+        const uint2 h = H[j];
+        const uint32_t u2 = pair_u2(h.x, h.y);
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+          uint32_t d, zp;
+          TP_LOP3(d, z1[q], g1[q], u2, 0x06);
+          TP_LOP3(zp, d, z1[q], h.x, 0x09);
+          if (zp == 0) {
+            bev += 1;
+            bodd += (__popc((d ^ h.y) & colmask) + (uint32_t)j + (uint32_t)__popc(q) + lanepar) & 1u;
+          }
+        }
+      }
+    };
+    bool dense = false;  // warp-uniform (n <= 32): skip the filter pass on event-dense matrices
+    for (uint32_t kb = 0; kb < p.nblk; ++kb) {
+      const unsigned long long B = B0 + kb;
+      const uint32_t SX = (kb & 1u) ? SS[V - 1] : SA[V - 1];
+      if (!WIDE && dense) {
+        // walk the B side only, recording its states, then evaluate exactly
+        __syncwarp();
+        if (lane == 0) H[0] = make_uint2(z2, g2);
+        static_for<SB - 1>([&](auto jc) {
+          constexpr int j = decltype(jc)::value + 1;
+          constexpr int t = ctz_c(j);
+          constexpr bool leave = (t + 1 < V) ? (((j >> (t + 1)) & 1) != 0) : false;
+          const uint32_t sop = (t == V - 1) ? SX : (leave ? SS[t] : SA[t]);
+          sub_word(z2, g2, SM[t], sop);
+          if (lane == 0) H[j] = make_uint2(z2, g2);
+        });
+        __syncwarp();
+        uint32_t bev, bodd;
+        exact_block(bev, bodd);
+        ev += bev;
+        odd += bodd;
+        dense = __any_sync(FULL, bev >= (uint32_t)K / 2);
+      } else {
+        uint32_t rec = 0;
+        if (!WIDE) {
+          __syncwarp();
+          if (lane == 0) H[0] = make_uint2(z2, g2);
+        }
+        {
+          const uint32_t u2 = pair_u2(z2, g2);
+          static_for<K>([&](auto kc) {
+            constexpr int k = decltype(kc)::value;
+            pair_test<(((uint32_t)k) << 16) | 1u>(z1[k], g1[k], z2, u2, rec, one);
+          });
+        }
+        static_for<SB - 1>([&](auto jc) {
+          constexpr int j = decltype(jc)::value + 1;
+          constexpr int t = ctz_c(j);
+          constexpr bool leave = (t + 1 < V) ? (((j >> (t + 1)) & 1) != 0) : false;
+          const uint32_t sop = (t == V - 1) ? SX : (leave ? SS[t] : SA[t]);
+          sub_word(z2, g2, SM[t], sop);
+          if (!WIDE) {
+            if (lane == 0) H[j] = make_uint2(z2, g2);
+          }
+          const uint32_t u2 = pair_u2(z2, g2);
+          static_for<K>([&](auto kc) {
+            constexpr int k = decltype(kc)::value;
+            pair_test<((uint32_t)((j << KB) | k) << 16) | 1u>(z1[k], g1[k], z2, u2, rec, one);
+          });
+        });
+        if (__any_sync(FULL, rec != 0)) {
+          if (!WIDE) __syncwarp();
+          const uint32_t cnt = rec & 0xffffu;
+          uint32_t bev = 0, bodd = 0;
+          if (__any_sync(FULL, cnt > 1)) {
+            // exact re-evaluation of every pair of the superblock
+            if (WIDE) {
+              const unsigned long long r = replay_wide<KB>(R, p.n, B << V, SB, lane, p.z0_init, p.z1_init);
+              bev = (uint32_t)r;
+              bodd = (uint32_t)(r >> 32);
+            } else {
+              exact_block(bev, bodd);
+              // switch to the exact mode only when events are really dense
+              // (e.g. all-ones rows: 2/3 of all pairs), not on a stray double hit
+              dense = p.dense_ok != 0 && __any_sync(FULL, bev >= (uint32_t)K / 2);
+            }
+          } else if (cnt == 1) {
+            const uint32_t id = rec >> 16, j = id >> KB, k = id & (K - 1);
+            if (WIDE) {
+              uint32_t zz[2], gg[2];
+              wide_subset_state<KB>(R, p.n, (B << V) + j, (k << 5) | lane, p.z0_init, p.z1_init, zz, gg);
+              if ((zz[0] | zz[1]) == 0) {
+                bev = 1;
+                bodd = (__popc(gg[0]) + __popc(gg[1]) + j + __popc(k) + lanepar) & 1u;
+              }
+            } else {
+              // the hit is exact for n <= 32; its sign word is d ^ g2(step j)
+              uint32_t zk = z1[0], gk = g1[0];
+#pragma unroll
+              for (int q = 1; q < K; ++q)
+                if ((uint32_t)q == k) {
+                  zk = z1[q];
+                  gk = g1[q];
+                }
+              const uint2 h = H[j];
+              uint32_t d;
+              TP_LOP3(d, zk, gk, pair_u2(h.x, h.y), 0x06);
+              bev = 1;
+              bodd = (__popc((d ^ h.y) & colmask) + j + __popc(k) + lanepar) & 1u;
+            }
+          }
+          ev += bev;
+          odd += bodd;
+        }
+      }
+      if (kb + 1 < p.nblk) {
+        const uint32_t u = kb + 1;
+        const int t = __ffs(u) - 1;
+        const RowRec& row = R[FIX + V + t];
+        sub_word(z2, g2, row.m[0], entry_leave(u, t, p, B0) ? row.s[0] : row.a[0]);
+      }
+    }
+    warp_flush(p.pm + 2 * b, ev - odd, odd, lane);
+  }
+  trace_end(p, t_start, n_items, blockIdx.x * WARPS + (threadIdx.x >> 5), lane);
+}
+
+// ---------------------------------------------------------------------------
 // Generic walk: pieces of up to glen high steps (32 reference steps each) of
 // two regions, with lanes masked to the reference step range [lo, hi).
 // Covers small n, and the unaligned heads and tails of step ranges.
@@ -701,7 +928,14 @@ cudaError_t run_alu_peak(int sm_count, uint32_t* scratch, cudaStream_t st, doubl
   X(kWideK2V7W4, k_walk_wide<1, 7, 4>)   \
   X(kWideK4V6W4, k_walk_wide<2, 6, 4>)   \
   X(kWideK8V5W4, k_walk_wide<3, 5, 4>)   \
-  X(kWideK8V6W4, k_walk_wide<3, 6, 4>)
+  X(kWideK8V6W4, k_walk_wide<3, 6, 4>)    \
+  X(kPairK32V4W4, k_walk_pair<5, 4, 4, false>) \
+  X(kPairK16V5W4, k_walk_pair<4, 5, 4, false>) \
+  X(kPairWideK32V4W4, k_walk_pair<5, 4, 4, true>) \
+  X(kPairWideK16V5W4, k_walk_pair<4, 5, 4, true>) \
+  X(kPairK32V3W4, k_walk_pair<5, 3, 4, false>) \
+  X(kPairK16V4W4, k_walk_pair<4, 4, 4, false>) \
+  X(kPairWideK32V3W4, k_walk_pair<5, 3, 4, true>)
 
 const void* walk_fast_symbol(int variant) {
   switch (variant) {

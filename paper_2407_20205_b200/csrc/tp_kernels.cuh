@@ -24,11 +24,25 @@ enum FastVariant {
   kWideK8V5W4 = 4,
   kWideK8V6W4 = 5,
   kLaneV5W4 = 6,
-  kNumFast = 7
+  kPairK32V4W4 = 7,      // pair walk (meet in the middle), n <= 32
+  kPairK16V5W4 = 8,
+  kPairWideK32V4W4 = 9,  // pair walk, n > 32 (primary-column filter)
+  kPairWideK16V5W4 = 10,
+  kPairK32V3W4 = 11,
+  kPairK16V4W4 = 12,
+  kPairWideK32V3W4 = 13,
+  kNumFast = 14
 };
+constexpr bool fast_is_pair(int v) { return v >= kPairK32V4W4 && v <= kPairWideK32V3W4; }
+constexpr bool fast_pair_wide(int v) {
+  return v == kPairWideK32V4W4 || v == kPairWideK16V5W4 || v == kPairWideK32V3W4;
+}
 constexpr bool fast_is_lane(int v) { return v <= kLaneV8W4 || v == kLaneV5W4; }
 constexpr int fast_v(int v) {
-  return v == kLaneV5W4 ? 5
+  return (v == kPairK32V3W4 || v == kPairWideK32V3W4) ? 3
+       : (v == kPairK32V4W4 || v == kPairWideK32V4W4 || v == kPairK16V4W4) ? 4
+       : (v == kPairK16V5W4 || v == kPairWideK16V5W4) ? 5
+       : v == kLaneV5W4 ? 5
        : v == kLaneV7W4 ? 7
        : v == kLaneV8W4 ? 8
        : v == kWideK2V7W4 ? 7
@@ -37,7 +51,9 @@ constexpr int fast_v(int v) {
                           : 6;
 }
 constexpr int fast_kb(int v) {
-  return fast_is_lane(v) ? 0 : v == kWideK2V7W4 ? 1 : v == kWideK4V6W4 ? 2 : 3;
+  return (v == kPairK32V4W4 || v == kPairWideK32V4W4 || v == kPairK32V3W4 || v == kPairWideK32V3W4) ? 5
+       : (v == kPairK16V5W4 || v == kPairWideK16V5W4 || v == kPairK16V4W4) ? 4
+       : fast_is_lane(v) ? 0 : v == kWideK2V7W4 ? 1 : v == kWideK4V6W4 ? 2 : 3;
 }
 constexpr int fast_warps(int) { return 4; }
 
@@ -55,6 +71,7 @@ struct FastParams {
   uint32_t z0_init, z1_init;    // zero-indicator of an empty vector (padding = 0)
   uint32_t one;                 // runtime 1
   unsigned long long* trace;    // optional per-warp trace (smid, t_start, t_end, items); nullptr = off
+  int dense_ok;                 // allow the exact (dense-event) mode
 };
 
 // Generic walk: regions [reg_a0[r], reg_a1[r]) of 32-step high steps, cut

@@ -156,10 +156,13 @@ int choose_variant(int n) {
     const char* e = getenv("TRITPERM_FAST_VARIANT");
     forced = e ? atoi(e) : -1;
   }
-  if (forced >= 0 && forced < tp::kNumFast && tp::fast_is_lane(forced) == (n <= 32)) return forced;
+  if (forced >= 0 && forced < tp::kNumFast) {
+    const bool for_narrow = tp::fast_is_lane(forced) || (tp::fast_is_pair(forced) && !tp::fast_pair_wide(forced));
+    if (for_narrow == (n <= 32)) return forced;
+  }
   // short walks (n <= 21, <= 2^16 high steps) favour parallelism: more, smaller items
-  if (n <= 32) return n >= 22 ? tp::kLaneV8W4 : tp::kLaneV5W4;
-  return tp::kWideK4V6W4;
+  if (n <= 32) return n >= 22 ? tp::kPairK32V3W4 : tp::kLaneV5W4;
+  return tp::kPairWideK32V4W4;
 }
 
 // Optional CTA trace buffer for the fast walks (tp_debug_trace).
@@ -258,6 +261,14 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
     pl.fp.z1_init = z1;
     pl.fp.one = 1u;
     pl.fp.trace = g_trace;
+    {
+      static int dense_ok = -1;
+      if (dense_ok < 0) {
+        const char* e = getenv("TRITPERM_NO_DENSE");
+        dense_ok = (e && atoi(e)) ? 0 : 1;
+      }
+      pl.fp.dense_ok = dense_ok;
+    }
     const int bps = d.fast_blocks_per_sm[pl.variant];
     const unsigned long long ctas = (unsigned long long)d.sm_count * bps;
     const unsigned long long wpc = tp::fast_warps(pl.variant);
@@ -636,6 +647,29 @@ int tp_exact_census(int n, int device, int64_t* zeros, int64_t* plus, int64_t* m
   for (int e = 0; e < n * (n - 1); ++e) q3 *= 3ull;
   *zeros = (int64_t)(p3 * q3 + 2ull * p3 * N0);
   *plus = *minus = (int64_t)(p3 * (q3 - N0));
+  return TP_OK;
+}
+
+int tp_walk_info(int n, char* name, int name_len, double* lop3_per_term) {
+  if (n < 1 || n > TP_MAX_N) return fail(TP_E_INVALID, "need 1 <= n <= %d, got %d", TP_MAX_N, n);
+  const int v = choose_variant(n);
+  const char* kind;
+  double ops;
+  if (n <= tp::kSmallMaxN) {
+    kind = "k_small";  // batch / Monte Carlo path; ranges use the lane walk
+    ops = 3.0;
+  } else if (tp::fast_is_pair(v)) {
+    kind = tp::fast_pair_wide(v) ? "k_walk_pair<wide>" : "k_walk_pair";
+    ops = 2.0;
+  } else if (tp::fast_is_lane(v)) {
+    kind = "k_walk_lane";
+    ops = 3.0;
+  } else {
+    kind = "k_walk_wide";
+    ops = 3.0;
+  }
+  if (name && name_len > 0) snprintf(name, (size_t)name_len, "%s KB=%d V=%d", kind, tp::fast_kb(v), tp::fast_v(v));
+  if (lop3_per_term) *lop3_per_term = ops;
   return TP_OK;
 }
 
