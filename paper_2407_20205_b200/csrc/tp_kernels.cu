@@ -515,13 +515,31 @@ __device__ __forceinline__ uint32_t pair_u2(uint32_t z2, uint32_t g2) {
   return u;
 }
 
+// The B side is kept as (z2, u2) with u2 = ~(z2 ^ g2), the form the pair
+// test consumes; the z-encoded sub of a row (m, s), with c = m ^ s, is then
+//   d = ~z & ~(z ^ u ^ s)   (0x09);  z' = ~d & (z ^ m)   (0x06);
+//   u' = ~(z' ^ d ^ c)      (0x69)   -- still 3 LOP3, and no separate u2 op.
+__device__ __forceinline__ void sub_word_u(uint32_t& z, uint32_t& u, uint32_t m, uint32_t s, uint32_t c) {
+  uint32_t d, zn, un;
+  TP_LOP3(d, z, u, s, 0x09);
+  TP_LOP3(zn, d, z, m, 0x06);
+  TP_LOP3(un, zn, d, c, 0x69);
+  z = zn;
+  u = un;
+}
+__device__ __forceinline__ uint32_t pair_g2(uint32_t z2, uint32_t u2) {  // g2 = ~(u2 ^ z2)
+  uint32_t g;
+  TP_LOP3(g, z2, u2, 0u, 0xC3);
+  return g;
+}
+
 template <int KB, int V, int WARPS, bool WIDE>
 __global__ void __launch_bounds__(32 * WARPS) k_walk_pair(FastParams p) {
   constexpr int K = 1 << KB;
   constexpr int FIX = 5 + KB;
   constexpr int SB = 1 << V;
   __shared__ RowRec Rs[WARPS][64];
-  __shared__ uint2 Hs[WARPS][SB];  // B-side (z2, g2) at every step of the current superblock (n <= 32)
+  __shared__ uint2 Hs[WARPS][SB];  // B-side (z2, u2) at every step of the current superblock (n <= 32)
   const uint32_t lane = threadIdx.x & 31u;
   RowRec* R = Rs[threadIdx.x >> 5];
   uint2* H = Hs[threadIdx.x >> 5];
@@ -567,12 +585,12 @@ __global__ void __launch_bounds__(32 * WARPS) k_walk_pair(FastParams p) {
       });
     }
     // B side: v2 for S2 = gray(A0) on rows >= h (low bits empty)
-    uint32_t z2, g2;
+    uint32_t z2, u2;
     {
       uint32_t zz[2], gg[2];
       wide_subset_state<KB>(R, p.n, A0, 0u, p.z0_init, p.z1_init, zz, gg);
       z2 = zz[0];
-      g2 = gg[0];
+      u2 = pair_u2(zz[0], gg[0]);
     }
     uint32_t ev = 0, odd = 0;
     // Exact evaluation of every pair of the current superblock from the
@@ -581,15 +599,15 @@ __global__ void __launch_bounds__(32 * WARPS) k_walk_pair(FastParams p) {
       bev = bodd = 0;
       for (int j = 0; j < SB; ++j) {
         const uint2 h = H[j];
-        const uint32_t u2 = pair_u2(h.x, h.y);
+        const uint32_t gh = pair_g2(h.x, h.y);
 #pragma unroll
         for (int q = 0; q < K; ++q) {
           uint32_t d, zp;
-          TP_LOP3(d, z1[q], g1[q], u2, 0x06);
+          TP_LOP3(d, z1[q], g1[q], h.y, 0x06);
           TP_LOP3(zp, d, z1[q], h.x, 0x09);
           if (zp == 0) {
             bev += 1;
-            bodd += (__popc((d ^ h.y) & colmask) + (uint32_t)j + (uint32_t)__popc(q) + lanepar) & 1u;
+            bodd += (__popc((d ^ gh) & colmask) + (uint32_t)j + (uint32_t)__popc(q) + lanepar) & 1u;
           }
         }
       }
@@ -598,17 +616,19 @@ __global__ void __launch_bounds__(32 * WARPS) k_walk_pair(FastParams p) {
     for (uint32_t kb = 0; kb < p.nblk; ++kb) {
       const unsigned long long B = B0 + kb;
       const uint32_t SX = (kb & 1u) ? SS[V - 1] : SA[V - 1];
+      const uint32_t CX = (kb & 1u) ? SA[V - 1] : SS[V - 1];
       if (!WIDE && dense) {
         // walk the B side only, recording its states, then evaluate exactly
         __syncwarp();
-        if (lane == 0) H[0] = make_uint2(z2, g2);
+        if (lane == 0) H[0] = make_uint2(z2, u2);
         static_for<SB - 1>([&](auto jc) {
           constexpr int j = decltype(jc)::value + 1;
           constexpr int t = ctz_c(j);
           constexpr bool leave = (t + 1 < V) ? (((j >> (t + 1)) & 1) != 0) : false;
           const uint32_t sop = (t == V - 1) ? SX : (leave ? SS[t] : SA[t]);
-          sub_word(z2, g2, SM[t], sop);
-          if (lane == 0) H[j] = make_uint2(z2, g2);
+          const uint32_t cop = (t == V - 1) ? CX : (leave ? SA[t] : SS[t]);
+          sub_word_u(z2, u2, SM[t], sop, cop);
+          if (lane == 0) H[j] = make_uint2(z2, u2);
         });
         __syncwarp();
         uint32_t bev, bodd;
@@ -620,25 +640,22 @@ __global__ void __launch_bounds__(32 * WARPS) k_walk_pair(FastParams p) {
         uint32_t rec = 0;
         if (!WIDE) {
           __syncwarp();
-          if (lane == 0) H[0] = make_uint2(z2, g2);
+          if (lane == 0) H[0] = make_uint2(z2, u2);
         }
-        {
-          const uint32_t u2 = pair_u2(z2, g2);
-          static_for<K>([&](auto kc) {
-            constexpr int k = decltype(kc)::value;
-            pair_test<(((uint32_t)k) << 16) | 1u>(z1[k], g1[k], z2, u2, rec, one);
-          });
-        }
+        static_for<K>([&](auto kc) {
+          constexpr int k = decltype(kc)::value;
+          pair_test<(((uint32_t)k) << 16) | 1u>(z1[k], g1[k], z2, u2, rec, one);
+        });
         static_for<SB - 1>([&](auto jc) {
           constexpr int j = decltype(jc)::value + 1;
           constexpr int t = ctz_c(j);
           constexpr bool leave = (t + 1 < V) ? (((j >> (t + 1)) & 1) != 0) : false;
           const uint32_t sop = (t == V - 1) ? SX : (leave ? SS[t] : SA[t]);
-          sub_word(z2, g2, SM[t], sop);
+          const uint32_t cop = (t == V - 1) ? CX : (leave ? SA[t] : SS[t]);
+          sub_word_u(z2, u2, SM[t], sop, cop);
           if (!WIDE) {
-            if (lane == 0) H[j] = make_uint2(z2, g2);
+            if (lane == 0) H[j] = make_uint2(z2, u2);
           }
-          const uint32_t u2 = pair_u2(z2, g2);
           static_for<K>([&](auto kc) {
             constexpr int k = decltype(kc)::value;
             pair_test<((uint32_t)((j << KB) | k) << 16) | 1u>(z1[k], g1[k], z2, u2, rec, one);
@@ -680,9 +697,9 @@ __global__ void __launch_bounds__(32 * WARPS) k_walk_pair(FastParams p) {
                 }
               const uint2 h = H[j];
               uint32_t d;
-              TP_LOP3(d, zk, gk, pair_u2(h.x, h.y), 0x06);
+              TP_LOP3(d, zk, gk, h.y, 0x06);
               bev = 1;
-              bodd = (__popc((d ^ h.y) & colmask) + j + __popc(k) + lanepar) & 1u;
+              bodd = (__popc((d ^ pair_g2(h.x, h.y)) & colmask) + j + __popc(k) + lanepar) & 1u;
             }
           }
           ev += bev;
@@ -693,7 +710,8 @@ __global__ void __launch_bounds__(32 * WARPS) k_walk_pair(FastParams p) {
         const uint32_t u = kb + 1;
         const int t = __ffs(u) - 1;
         const RowRec& row = R[FIX + V + t];
-        sub_word(z2, g2, row.m[0], entry_leave(u, t, p, B0) ? row.s[0] : row.a[0]);
+        const bool lv = entry_leave(u, t, p, B0);
+        sub_word_u(z2, u2, row.m[0], lv ? row.s[0] : row.a[0], lv ? row.a[0] : row.s[0]);
       }
     }
     warp_flush(p.pm + 2 * b, ev - odd, odd, lane);
