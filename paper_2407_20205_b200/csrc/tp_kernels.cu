@@ -540,9 +540,11 @@ __global__ void __launch_bounds__(32 * WARPS) k_walk_pair(FastParams p) {
   constexpr int SB = 1 << V;
   __shared__ RowRec Rs[WARPS][64];
   __shared__ uint2 Hs[WARPS][SB];  // B-side (z2, u2) at every step of the current superblock (n <= 32)
+  __shared__ uint2 As[WIDE ? 1 : WARPS][WIDE ? 1 : K][32];  // A-side (z1, g1) per slot and lane, for single hits
   const uint32_t lane = threadIdx.x & 31u;
   RowRec* R = Rs[threadIdx.x >> 5];
   uint2* H = Hs[threadIdx.x >> 5];
+  uint2 (*A)[32] = As[WIDE ? 0 : (threadIdx.x >> 5)];
   const uint32_t lanepar = __popc(lane) & 1u;
   const uint32_t one = p.one;
   const uint32_t colmask = p.z0_init;  // real columns of the primary word
@@ -582,6 +584,7 @@ __global__ void __launch_bounds__(32 * WARPS) k_walk_pair(FastParams p) {
         }
         z1[gray_c(i)] = zc;
         g1[gray_c(i)] = gc;
+        if (!WIDE) A[gray_c(i)][lane] = make_uint2(zc, gc);
       });
     }
     // B side: v2 for S2 = gray(A0) on rows >= h (low bits empty)
@@ -688,16 +691,10 @@ __global__ void __launch_bounds__(32 * WARPS) k_walk_pair(FastParams p) {
               }
             } else {
               // the hit is exact for n <= 32; its sign word is d ^ g2(step j)
-              uint32_t zk = z1[0], gk = g1[0];
-#pragma unroll
-              for (int q = 1; q < K; ++q)
-                if ((uint32_t)q == k) {
-                  zk = z1[q];
-                  gk = g1[q];
-                }
+              const uint2 a1 = A[k][lane];
               const uint2 h = H[j];
               uint32_t d;
-              TP_LOP3(d, zk, gk, h.y, 0x06);
+              TP_LOP3(d, a1.x, a1.y, h.y, 0x06);
               bev = 1;
               bodd = (__popc((d ^ pair_g2(h.x, h.y)) & colmask) + j + __popc(k) + lanepar) & 1u;
             }
