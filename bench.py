@@ -233,7 +233,10 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     os.environ[_kernels.ENV_DEVICE] = str(local)
-    if world > 1:
+    # one process per GPU; TRITPERM_BENCH_DIST=1 forces the NCCL path even for a
+    # single rank (exercises the collective on a 1-GPU box)
+    use_dist = world > 1 or os.environ.get("TRITPERM_BENCH_DIST") == "1"
+    if use_dist:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     wl = args.workload
@@ -271,7 +274,7 @@ def main():
             if timed_walk:
                 e1.record()
             launches += 1 + nl
-            if world > 1:
+            if use_dist:
                 dist.all_reduce(d_pm)
             return e0, e1
         per_rank_terms = span // world
@@ -300,7 +303,7 @@ def main():
                 e1.record()
             _kernels.finalize_async(d_pm.data_ptr(), B, n, d_cls.data_ptr(), d_hist.data_ptr(), s)
             launches += 2 + nl
-            if world > 1:
+            if use_dist:
                 dist.all_reduce(d_hist)
             return e0, e1
         per_rank_terms = B * (1 << n)
@@ -314,7 +317,7 @@ def main():
     # graph of the whole step (pack -> walk -> finalize); the walk kernel's own
     # time for the roofline then comes from a separate evented loop.
     graph = None
-    if args.graph and world == 1:
+    if args.graph and not use_dist:
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
@@ -330,7 +333,7 @@ def main():
 
     # timed region: K steps, L2 flushed (memset of 256 MiB) between steps,
     # each step bracketed by CUDA events on the launching stream
-    if world > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
@@ -348,7 +351,7 @@ def main():
             s1.record()
             evs.append((s0, s1, w))
         torch.cuda.synchronize()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     for s0, s1, (w0, w1) in evs:
         step_ms.append(s0.elapsed_time(s1))
@@ -364,7 +367,7 @@ def main():
         launches = per_step_launches * args.steps
         walk_ms = [a.elapsed_time(b) for a, b in wev]
     total_ms = sum(step_ms)
-    if world > 1:
+    if use_dist:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
@@ -399,7 +402,7 @@ def main():
         for _ in range(reps):
             cls, part, hist = tp.perm_mod3_batch(host)
         e2e_s = (time.perf_counter() - t0) / reps
-        if world > 1:
+        if use_dist:
             t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
@@ -458,7 +461,7 @@ def main():
             "cpu_baseline": cpu,
         }
         print(json.dumps(line))
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
 
 
