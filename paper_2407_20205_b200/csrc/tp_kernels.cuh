@@ -13,48 +13,30 @@ constexpr int kSmallThreads = 128;
 // Fast-walk variants.  Lane walk (n <= 32): one subset per lane, superblock
 // 2^V high steps of 32 reference steps.  Wide walk (n > 32): 2^KB subsets per
 // lane, superblock 2^V high steps of 32 * 2^KB reference steps.
-// Variant = (kind, KB, V, warps per CTA); each warp takes its own items.
-// The unrolled superblock body is (2^V - 1) * 2^KB steps: keep it <= ~20 KB of
-// SASS so it stays resident in the instruction cache.
+// Fast-walk variants: (kind, KB, V); all run 4 warps per CTA and each warp
+// takes its own items.  The unrolled superblock body stays near 20 KB of
+// SASS so it lives in the instruction cache.
+//   lane: one subset per lane, superblock 2^V high steps of 32 steps;
+//   wide: 2^KB subsets per lane (primary-column filter, n > 32);
+//   pair: 2^KB fixed A-side vectors per lane, B side walked (2 LOP3/subset);
+//         pair_wide = primary-column filter for n > 32.
 enum FastVariant {
-  kLaneV7W4 = 0,
-  kLaneV8W4 = 1,
-  kWideK2V7W4 = 2,
-  kWideK4V6W4 = 3,
-  kWideK8V5W4 = 4,
-  kWideK8V6W4 = 5,
-  kLaneV5W4 = 6,
-  kPairK32V4W4 = 7,      // pair walk (meet in the middle), n <= 32
-  kPairK16V5W4 = 8,
-  kPairWideK32V4W4 = 9,  // pair walk, n > 32 (primary-column filter)
-  kPairWideK16V5W4 = 10,
-  kPairK32V3W4 = 11,
-  kPairK16V4W4 = 12,
-  kPairWideK32V3W4 = 13,
-  kNumFast = 14
+  kLaneV5 = 0,
+  kLaneV8 = 1,
+  kWideK4V6 = 2,
+  kPairK32V3 = 3,
+  kPairK32V4 = 4,
+  kPairWideK32V3 = 5,
+  kPairWideK32V4 = 6,
+  kNumFast = 7
 };
-constexpr bool fast_is_pair(int v) { return v >= kPairK32V4W4 && v <= kPairWideK32V3W4; }
-constexpr bool fast_pair_wide(int v) {
-  return v == kPairWideK32V4W4 || v == kPairWideK16V5W4 || v == kPairWideK32V3W4;
-}
-constexpr bool fast_is_lane(int v) { return v <= kLaneV8W4 || v == kLaneV5W4; }
+constexpr bool fast_is_lane(int v) { return v == kLaneV5 || v == kLaneV8; }
+constexpr bool fast_is_pair(int v) { return v >= kPairK32V3 && v <= kPairWideK32V4; }
+constexpr bool fast_pair_wide(int v) { return v == kPairWideK32V3 || v == kPairWideK32V4; }
 constexpr int fast_v(int v) {
-  return (v == kPairK32V3W4 || v == kPairWideK32V3W4) ? 3
-       : (v == kPairK32V4W4 || v == kPairWideK32V4W4 || v == kPairK16V4W4) ? 4
-       : (v == kPairK16V5W4 || v == kPairWideK16V5W4) ? 5
-       : v == kLaneV5W4 ? 5
-       : v == kLaneV7W4 ? 7
-       : v == kLaneV8W4 ? 8
-       : v == kWideK2V7W4 ? 7
-       : v == kWideK4V6W4 ? 6
-       : v == kWideK8V5W4 ? 5
-                          : 6;
+  return v == kLaneV5 ? 5 : v == kLaneV8 ? 8 : v == kWideK4V6 ? 6 : (v == kPairK32V3 || v == kPairWideK32V3) ? 3 : 4;
 }
-constexpr int fast_kb(int v) {
-  return (v == kPairK32V4W4 || v == kPairWideK32V4W4 || v == kPairK32V3W4 || v == kPairWideK32V3W4) ? 5
-       : (v == kPairK16V5W4 || v == kPairWideK16V5W4 || v == kPairK16V4W4) ? 4
-       : fast_is_lane(v) ? 0 : v == kWideK2V7W4 ? 1 : v == kWideK4V6W4 ? 2 : 3;
-}
+constexpr int fast_kb(int v) { return fast_is_lane(v) ? 0 : v == kWideK4V6 ? 2 : 5; }
 constexpr int fast_warps(int) { return 4; }
 
 // Fast walk: items are L-aligned chunks [F0 + c*L, F0 + (c+1)*L) of every

@@ -151,18 +151,15 @@ struct Plan {
 // block (which forces an exact replay); events have probability (2/3)^n.
 // Override with TRITPERM_FAST_VARIANT for measurements.
 int choose_variant(int n) {
-  static int forced = -2;
-  if (forced == -2) {
-    const char* e = getenv("TRITPERM_FAST_VARIANT");
-    forced = e ? atoi(e) : -1;
-  }
+  const char* e = getenv("TRITPERM_FAST_VARIANT");  // read per call: tests switch it at run time
+  const int forced = e ? atoi(e) : -1;
   if (forced >= 0 && forced < tp::kNumFast) {
     const bool for_narrow = tp::fast_is_lane(forced) || (tp::fast_is_pair(forced) && !tp::fast_pair_wide(forced));
     if (for_narrow == (n <= 32)) return forced;
   }
   // short walks (n <= 21, <= 2^16 high steps) favour parallelism: more, smaller items
-  if (n <= 32) return n >= 22 ? tp::kPairK32V3W4 : tp::kLaneV5W4;
-  return tp::kPairWideK32V4W4;
+  if (n <= 32) return n >= 22 ? tp::kPairK32V3 : tp::kLaneV5;
+  return tp::kPairWideK32V4;
 }
 
 // Optional CTA trace buffer for the fast walks (tp_debug_trace).

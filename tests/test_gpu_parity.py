@@ -364,3 +364,27 @@ def test_event_dense_matrices_exact(gpu):
     for b in range(3, 6):
         mags, sgns = o.planes_from_classes(e[b])
         assert part[b] == o.chunk_sum(mags, sgns, 26, 1, 1 << 26)
+
+
+@pytest.mark.parametrize("variant", range(7))
+def test_every_fast_walk_variant(gpu, oracle, variant, monkeypatch):
+    """Each fast-walk kernel (lane V5/V8, wide, pair narrow/wide V3/V4),
+    forced through TRITPERM_FAST_VARIANT, on ranges with heads/tails, a full
+    traversal and an event-dense matrix.  A variant that does not fit an n
+    falls back to the default, which is also fine."""
+    monkeypatch.setenv("TRITPERM_FAST_VARIANT", str(variant))
+    r = random.Random(1000 + variant)
+    for n in (18, 23, 27, 32, 35, 41, 52):
+        a = _rand_matrix(r, n)
+        mags, sgns = oracle.planes_from_classes(a)
+        m = gpu.MatrixF3(centred(a))
+        span = min(1 << 21, 1 << (n - 2))
+        lo = r.randrange(1, (1 << n) - 2 * span)
+        hi = lo + span + r.randrange(0, 999)
+        assert gpu.perm_chunk(m, lo, hi).partial_sum == oracle.chunk_sum(mags, sgns, n, lo, hi), (variant, n)
+    a = _rand_matrix(r, 22)
+    mags, sgns = oracle.planes_from_classes(a)
+    assert gpu.perm_chunk(gpu.MatrixF3(centred(a)), 1, 1 << 22).partial_sum == oracle.chunk_sum(mags, sgns, 22, 1, 1 << 22)
+    for n in (24, 34):
+        m = gpu.MatrixF3([[1] * n for _ in range(n)])
+        assert gpu.perm_chunk(m, 1, 1 << n).partial_sum == _ones_partial(n), (variant, n)
