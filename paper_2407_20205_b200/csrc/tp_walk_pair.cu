@@ -141,9 +141,25 @@ __global__ void __launch_bounds__(32 * WARPS) k_walk_pair(FastParams p) {
         dense = __any_sync(FULL, bev >= (uint32_t)K / 2);
       } else {
         uint32_t rec = 0;
+        // The B states of the whole superblock, one per lane (step j = lane mod
+        // SB): relative to the entry, step j adds the rows FIX + r for the bits r
+        // of gray(j); row FIX+V-1 leaves instead when bit 0 of the superblock
+        // index is set.  V row updates per warp replace SB-1 sequential steps;
+        // each step then broadcasts its state with two shuffles.
+        uint32_t zj = z2, uj = u2;
+        {
+          const uint32_t j = lane & (SB - 1), gj = j ^ (j >> 1);
+#pragma unroll
+          for (int r = 0; r < V; ++r) {
+            if ((gj >> r) & 1u) {
+              const bool lv = (r == V - 1) && (kb & 1u);
+              sub_word_u(zj, uj, SM[r], lv ? SS[r] : SA[r], lv ? SA[r] : SS[r]);
+            }
+          }
+        }
         if (!WIDE) {
           __syncwarp();
-          if (lane == 0) H[0] = make_uint4(z2, u2, 0u, 0u);
+          if (lane < (uint32_t)SB) H[lane] = make_uint4(zj, uj, 0u, 0u);
         }
         static_for<K>([&](auto kc) {
           constexpr int k = decltype(kc)::value;
@@ -151,14 +167,8 @@ __global__ void __launch_bounds__(32 * WARPS) k_walk_pair(FastParams p) {
         });
         static_for<SB - 1>([&](auto jc) {
           constexpr int j = decltype(jc)::value + 1;
-          constexpr int t = ctz_c(j);
-          constexpr bool leave = (t + 1 < V) ? (((j >> (t + 1)) & 1) != 0) : false;
-          const uint32_t sop = (t == V - 1) ? SX : (leave ? SS[t] : SA[t]);
-          const uint32_t cop = (t == V - 1) ? CX : (leave ? SA[t] : SS[t]);
-          sub_word_u(z2, u2, SM[t], sop, cop);
-          if (!WIDE) {
-            if (lane == 0) H[j] = make_uint4(z2, u2, 0u, 0u);
-          }
+          z2 = __shfl_sync(FULL, zj, j);
+          u2 = __shfl_sync(FULL, uj, j);
           static_for<K>([&](auto kc) {
             constexpr int k = decltype(kc)::value;
             pair_test<((uint32_t)((j << KB) | k) << 16) | 1u>(z1[k], g1[k], z2, u2, rec, one);
