@@ -230,6 +230,20 @@ __device__ __forceinline__ void sub_word_u(uint32_t& z, uint32_t& u, uint32_t m,
   z = zn;
   u = un;
 }
+// Exact fold of one pair (n <= 32): if v1 + v2 is full, n += 1 and
+// a += parity(popc(sign word)); predicated, no branches.
+__device__ __forceinline__ void exact_fold(uint32_t z1, uint32_t g1, uint32_t z2, uint32_t u2, uint32_t g2,
+                                           uint32_t cm, uint32_t& n, uint32_t& a, uint32_t one) {
+  uint32_t d, zp, x;
+  TP_LOP3(d, z1, g1, u2, 0x06);
+  TP_LOP3(zp, d, z1, z2, 0x09);
+  TP_LOP3(x, d, g2, cm, 0x28);
+  if (zp == 0) {
+    n += one;
+    a += __popc(x) & 1u;
+  }
+}
+
 __device__ __forceinline__ uint32_t pair_g2(uint32_t z2, uint32_t u2) {  // g2 = ~(u2 ^ z2)
   uint32_t g;
   TP_LOP3(g, z2, u2, 0u, 0xC3);

@@ -76,16 +76,17 @@ __global__ void __launch_bounds__(32 * WARPS) k_walk_pair(FastParams p) {
     // B-side history H: replays (n <= 32) and dense mode (all n).
     auto exact_block = [&](uint32_t& bev, uint32_t& bodd) {
       bev = bodd = 0;
+#pragma unroll 1
       for (int j = 0; j < SB; ++j) {
         const uint4 h = H[j];
         const uint32_t gh = pair_g2(h.x, h.y);
+        if (WIDE) {
 #pragma unroll
-        for (int q = 0; q < K; ++q) {
-          uint32_t d, zp;
-          TP_LOP3(d, z1[q], g1[q], h.y, 0x06);
-          TP_LOP3(zp, d, z1[q], h.x, 0x09);
-          if (zp == 0) {
-            if (WIDE) {  // primary columns all nonzero: test the secondary word
+          for (int q = 0; q < K; ++q) {
+            uint32_t d, zp;
+            TP_LOP3(d, z1[q], g1[q], h.y, 0x06);
+            TP_LOP3(zp, d, z1[q], h.x, 0x09);
+            if (zp == 0) {  // primary columns all nonzero: test the secondary word
               const uint2 a2 = A[q][lane];
               uint32_t d1, zp1;
               TP_LOP3(d1, a2.x, a2.y, h.w, 0x06);
@@ -95,11 +96,22 @@ __global__ void __launch_bounds__(32 * WARPS) k_walk_pair(FastParams p) {
                 bodd += (__popc(d ^ gh) + __popc((d1 ^ pair_g2(h.z, h.w)) & colmask1) + (uint32_t)j +
                          (uint32_t)__popc(q) + lanepar) & 1u;
               }
-            } else {
-              bev += 1;
-              bodd += (__popc((d ^ gh) & colmask) + (uint32_t)j + (uint32_t)__popc(q) + lanepar) & 1u;
             }
           }
+        } else {
+          // Branch-free exact fold: per pair the test (2 LOP3), the sign word
+          // (d ^ g2) & colmask (1 LOP3), and predicated popc / and / two IMAD
+          // counters split by the static parity of popc(q).
+          uint32_t n0 = 0, a0 = 0, n1 = 0, a1 = 0;
+#pragma unroll
+          for (int q = 0; q < K; ++q) {
+            if (__popc(q) & 1) exact_fold(z1[q], g1[q], h.x, h.y, gh, colmask, n1, a1, one);
+            else exact_fold(z1[q], g1[q], h.x, h.y, gh, colmask, n0, a0, one);
+          }
+          // term is odd iff popc(sgn) + j + popc(q) + lane parity is odd
+          const uint32_t pj = ((uint32_t)j ^ lanepar) & 1u;
+          bev += n0 + n1;
+          bodd += pj ? (n0 - a0) + a1 : a0 + (n1 - a1);
         }
       }
     };
