@@ -45,7 +45,9 @@ constexpr int fast_warps(int) { return 4; }
 struct FastParams {
   const RowRec* rows;           // [B][64]
   unsigned long long* pm;       // [B][2] (plus, minus) accumulators
-  unsigned long long* queue;    // dynamic work counter (zeroed before launch)
+  // Work queue {next item, warps done}; the last warp out resets both to 0,
+  // so the counter needs no memset between launches.
+  unsigned long long* queue;
   unsigned long long F0, L, chunks, items;
   uint32_t nblk;                // superblocks per item
   int lognblk;
@@ -54,6 +56,7 @@ struct FastParams {
   uint32_t one;                 // runtime 1
   unsigned long long* trace;    // optional per-warp trace (smid, t_start, t_end, items); nullptr = off
   int dense_ok;                 // allow the exact (dense-event) mode
+  int static_items;             // items <= warps of the grid: warp w takes item w, no queue
 };
 
 // Generic walk: regions [reg_a0[r], reg_a1[r]) of 32-step high steps, cut

@@ -92,7 +92,8 @@ int ensure_device(int dev, Device** out) {
       if (d.generic_blocks_per_sm[nw] < 1) return fail(TP_E_CUDA, "walk kernels cannot be resident on device %d", dev);
     }
     TP_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
-    TP_CUDA(cudaMalloc(&d.queues, Device::kQueues * sizeof(unsigned long long)));
+    TP_CUDA(cudaMalloc(&d.queues, 2 * Device::kQueues * sizeof(unsigned long long)));
+    TP_CUDA(cudaMemset(d.queues, 0, 2 * Device::kQueues * sizeof(unsigned long long)));
     d.ready = true;
   }
   *out = &d;
@@ -166,7 +167,7 @@ int choose_variant(int n) {
 unsigned long long* g_trace = nullptr;
 
 unsigned long long* take_queue(Device& d) {
-  unsigned long long* q = d.queues + d.next_queue;
+  unsigned long long* q = d.queues + 2 * d.next_queue;
   d.next_queue = (d.next_queue + 1) % Device::kQueues;
   return q;
 }
@@ -270,6 +271,7 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
     const unsigned long long ctas = (unsigned long long)d.sm_count * bps;
     const unsigned long long wpc = tp::fast_warps(pl.variant);
     pl.fast_grid = (int)std::max<unsigned long long>(1, std::min(ctas, (pl.fp.items + wpc - 1) / wpc));
+    pl.fp.static_items = pl.fp.items <= (unsigned long long)pl.fast_grid * wpc ? 1 : 0;
   }
   auto pieces = [&](unsigned long long x0, unsigned long long x1) {
     return x1 > x0 ? (x1 - x0 + kGenericPiece - 1) / kGenericPiece : 0ull;
@@ -292,7 +294,6 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
 int run_plan(const Plan& pl, cudaStream_t st, int* launches) {
   int nl = 0;
   if (pl.fast) {
-    TP_CUDA(cudaMemsetAsync(pl.fp.queue, 0, sizeof(unsigned long long), st));
     TP_CUDA(tp::launch_walk_fast(pl.variant, pl.fast_grid, pl.fp, st));
     nl++;
   }

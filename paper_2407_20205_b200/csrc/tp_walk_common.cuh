@@ -71,9 +71,11 @@ __device__ __forceinline__ void load_rows(RowRec* R, const RowRec* src, uint32_t
 
 // Broadcast through REDUX (__reduce_or_sync), whose result lands in a
 // uniform register, so everything derived from the item stays uniform.
-__device__ __forceinline__ unsigned long long next_item(unsigned long long* queue, uint32_t lane) {
+__device__ __forceinline__ unsigned long long next_item(const FastParams& p, uint32_t lane,
+                                                        unsigned long long taken, uint32_t warp_global) {
+  if (p.static_items) return taken ? ~0ull : (unsigned long long)warp_global;
   unsigned long long item = 0;
-  if (lane == 0) item = atomicAdd(queue, 1ull);
+  if (lane == 0) item = atomicAdd(p.queue, 1ull);
   const uint32_t lo = __reduce_or_sync(FULL, (uint32_t)item);
   const uint32_t hi = __reduce_or_sync(FULL, (uint32_t)(item >> 32));
   return ((unsigned long long)hi << 32) | lo;
@@ -84,6 +86,17 @@ __device__ __forceinline__ unsigned long long next_item(unsigned long long* queu
 // the row leaves iff bit tz(kb)+1 of B0 + kb is set.
 __device__ __forceinline__ bool entry_leave(uint32_t kb, int t, const FastParams& p, unsigned long long B0) {
   return (t + 1 < p.lognblk) ? (((kb >> (t + 1)) & 1u) != 0) : (((B0 >> p.lognblk) & 1ull) != 0);
+}
+
+// Called by every warp after its last next_item: the last warp of the grid
+// resets the queue for the next launch (all fetches are done by then).
+__device__ __forceinline__ void queue_done(const FastParams& p, uint32_t lane) {
+  if (p.static_items || lane != 0) return;
+  const unsigned long long total = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+  if (atomicAdd(p.queue + 1, 1ull) == total - 1) {
+    atomicExch(p.queue, 0ull);
+    atomicExch(p.queue + 1, 0ull);
+  }
 }
 
 __device__ __forceinline__ void trace_end(const FastParams& p, unsigned long long t_start, unsigned long long n_items,

@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(32 * WARPS) k_walk_lane(FastParams p) {
   unsigned long long n_items = 0;
 
   for (;;) {
-    const unsigned long long item = next_item(p.queue, lane);
+    const unsigned long long item = next_item(p, lane, n_items, blockIdx.x * WARPS + (threadIdx.x >> 5));
     if (item >= p.items) break;
     ++n_items;
     const unsigned long long b = item / p.chunks;
@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(32 * WARPS) k_walk_lane(FastParams p) {
     }
     warp_flush(p.pm + 2 * b, ev - odd, odd, lane);
   }
+  queue_done(p, lane);
   trace_end(p, t_start, n_items, blockIdx.x * WARPS + (threadIdx.x >> 5), lane);
 }
 

@@ -388,3 +388,45 @@ def test_every_fast_walk_variant(gpu, oracle, variant, monkeypatch):
     for n in (24, 34):
         m = gpu.MatrixF3([[1] * n for _ in range(n)])
         assert gpu.perm_chunk(m, 1, 1 << n).partial_sum == _ones_partial(n), (variant, n)
+
+
+def test_work_queue_resets_between_launches(gpu, oracle):
+    """The fast walk's work queue resets itself (last warp out): repeated
+    launches on the same stream, a static-assignment plan (few items) and
+    CUDA-graph replays all return the same counts."""
+    import torch
+
+    from paper_2407_20205_b200 import _kernels, fixtures
+
+    st = torch.cuda.current_stream()
+    for n, B in ((20, 1), (24, 300)):  # static items / dynamic queue
+        e = fixtures.uniform_batch(n, 7, 0, B)
+        d_e = torch.from_numpy(e).cuda()
+        d_rows = torch.empty((B, _kernels.ROWREC_BYTES), dtype=torch.uint8, device="cuda")
+        d_pm = torch.zeros((B, 2), dtype=torch.int64, device="cuda")
+        _kernels.pack_async(d_e.data_ptr(), B, n, d_rows.data_ptr(), st.cuda_stream)
+        results = []
+        for _ in range(4):
+            d_pm.zero_()
+            _kernels.walk_async(d_rows.data_ptr(), B, n, d_pm.data_ptr(), st.cuda_stream)
+            torch.cuda.synchronize()
+            results.append(d_pm.cpu().numpy().copy())
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(st)
+        with torch.cuda.stream(side):
+            _kernels.walk_async(d_rows.data_ptr(), B, n, d_pm.data_ptr(), side.cuda_stream)
+        st.wait_stream(side)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            _kernels.walk_async(d_rows.data_ptr(), B, n, d_pm.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        for _ in range(3):
+            d_pm.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            results.append(d_pm.cpu().numpy().copy())
+        for r in results[1:]:
+            assert np.array_equal(r, results[0]), n
+        for b in (0, B - 1):
+            mags, sgns = oracle.planes_from_classes(e[b])
+            assert int(results[0][b, 0]) - int(results[0][b, 1]) == oracle.chunk_sum(mags, sgns, n, 1, 1 << n)
