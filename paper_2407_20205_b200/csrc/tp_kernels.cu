@@ -250,10 +250,13 @@ cudaError_t launch_wide(int KB, int V, int grid, const FastParams& p, cudaStream
 const void* wide_symbol(int KB, int V);
 cudaError_t launch_pair(int KB, int V, bool wide, int grid, const FastParams& p, cudaStream_t st);
 const void* pair_symbol(int KB, int V, bool wide);
+cudaError_t launch_packed(int V, int grid, const FastParams& p, cudaStream_t st);
+const void* packed_symbol(int V);
 
 const void* walk_fast_symbol(int v) {
   if (fast_is_lane(v)) return lane_symbol(fast_v(v));
   if (fast_is_pair(v)) return pair_symbol(fast_kb(v), fast_v(v), fast_pair_wide(v));
+  if (fast_is_packed(v)) return packed_symbol(v == kPackedK32V3 ? 0 : 1);
   return wide_symbol(fast_kb(v), fast_v(v));
 }
 
@@ -265,6 +268,7 @@ const void* walk_generic_symbol(int nw) {
 cudaError_t launch_walk_fast(int v, int grid, const FastParams& p, cudaStream_t st) {
   if (fast_is_lane(v)) return launch_lane(fast_v(v), grid, p, st);
   if (fast_is_pair(v)) return launch_pair(fast_kb(v), fast_v(v), fast_pair_wide(v), grid, p, st);
+  if (fast_is_packed(v)) return launch_packed(v == kPackedK32V3 ? 0 : 1, grid, p, st);
   return launch_wide(fast_kb(v), fast_v(v), grid, p, st);
 }
 

@@ -28,13 +28,17 @@ enum FastVariant {
   kPairK32V4 = 4,
   kPairWideK32V3 = 5,
   kPairWideK32V4 = 6,
-  kNumFast = 7
+  kPackedK32V3 = 7,
+  kPackedK32V4 = 8,
+  kNumFast = 9
 };
 constexpr bool fast_is_lane(int v) { return v == kLaneV5 || v == kLaneV8; }
 constexpr bool fast_is_pair(int v) { return v >= kPairK32V3 && v <= kPairWideK32V4; }
 constexpr bool fast_pair_wide(int v) { return v == kPairWideK32V3 || v == kPairWideK32V4; }
+constexpr bool fast_is_packed(int v) { return v == kPackedK32V3 || v == kPackedK32V4; }
 constexpr int fast_v(int v) {
-  return v == kLaneV5 ? 5 : v == kLaneV8 ? 8 : v == kWideK4V6 ? 6 : (v == kPairK32V3 || v == kPairWideK32V3) ? 3 : 4;
+  return v == kLaneV5 ? 5 : v == kLaneV8 ? 8 : v == kWideK4V6 ? 6
+       : (v == kPairK32V3 || v == kPairWideK32V3 || v == kPackedK32V3) ? 3 : 4;
 }
 constexpr int fast_kb(int v) { return fast_is_lane(v) ? 0 : v == kWideK4V6 ? 2 : 5; }
 constexpr int fast_warps(int) { return 4; }

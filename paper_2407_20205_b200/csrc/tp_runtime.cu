@@ -155,11 +155,12 @@ int choose_variant(int n) {
   const char* e = getenv("TRITPERM_FAST_VARIANT");  // read per call: tests switch it at run time
   const int forced = e ? atoi(e) : -1;
   if (forced >= 0 && forced < tp::kNumFast) {
-    const bool for_narrow = tp::fast_is_lane(forced) || (tp::fast_is_pair(forced) && !tp::fast_pair_wide(forced));
+    const bool for_narrow = tp::fast_is_lane(forced) || tp::fast_is_packed(forced) ||
+                            (tp::fast_is_pair(forced) && !tp::fast_pair_wide(forced));
     if (for_narrow == (n <= 32)) return forced;
   }
   // short walks (n <= 21, <= 2^16 high steps) favour parallelism: more, smaller items
-  if (n <= 32) return n >= 22 ? tp::kPairK32V3 : tp::kLaneV5;
+  if (n <= 32) return n >= 22 ? tp::kPackedK32V4 : tp::kLaneV5;
   return tp::kPairWideK32V4;
 }
 
@@ -659,6 +660,9 @@ int tp_walk_info(int n, char* name, int name_len, double* lop3_per_term) {
   } else if (tp::fast_is_pair(v)) {
     kind = tp::fast_pair_wide(v) ? "k_walk_pair<wide>" : "k_walk_pair";
     ops = 2.0;
+  } else if (tp::fast_is_packed(v)) {
+    kind = "k_walk_packed";  // 3 LOP3 per packed word of two pairs
+    ops = 1.5;
   } else if (tp::fast_is_lane(v)) {
     kind = "k_walk_lane";
     ops = 3.0;

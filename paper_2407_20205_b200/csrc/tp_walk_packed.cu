@@ -1,0 +1,327 @@
+// tp_walk_packed.cu -- the pair walk with a packed 16-column filter (n <= 32).
+//
+// Same meet-in-the-middle split as tp_walk_pair.cu (A side = rows 0..9 fixed
+// per lane in K = 32 slots, B side walked), but the filter tests two pairs per
+// 32-bit word: the low 16 columns of slot w sit in the low half of packed word
+// w and those of slot w + 16 in the high half, and the B state's low 16
+// columns are duplicated into both halves.  Per word:
+//
+//   d  = ~z1 & (g1 ^ u2)              lop3 0x06
+//   zp = ~d & ~(z1 ^ z2)              lop3 0x09   (zero columns of the sums)
+//   t  = zp - 0x00010001              imad (FMA pipe)
+//   P  = (t & ~zp & 0x80008000) != 0  lop3 -> predicate: a half without zero columns
+//   @P m += bit(j, w)                 imad (FMA pipe)
+//
+// i.e. 1.5 LOP3 per pair instead of 2, and 2.5 instructions per pair.  A
+// pass (probability (2/3)^16 per pair on uniform inputs) is verified exactly
+// on all 32 columns at the end of each verify batch (one superblock for
+// V = 4, two for V = 3): the lanes park their pass masks in shared memory,
+// an exclusive warp scan turns every nonzero mask into one list entry, and
+// lane e walks the pass bits of entry e against the full A words and the
+// group's B states (both in shared memory).  Terms are evaluated only there,
+// so the counts are exact.  Event-dense matrices switch to an exact mode as
+// in the pair walk.  V = 4 (512 pairs per lane and superblock) is the
+// default for 22 <= n <= 32: 7-16 % above the unpacked pair walk.
+#include "tp_walk_common.cuh"
+
+namespace tp {
+
+template <uint32_t BIT>
+__device__ __forceinline__ void packed_test(uint32_t z1, uint32_t g1, uint32_t z2, uint32_t u2, uint32_t& m,
+                                            uint32_t one, uint32_t cneg) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 d, zp, t, h;\n\t"
+      "lop3.b32 d, %1, %2, %4, 0x06;\n\t"
+      "lop3.b32 zp, d, %1, %3, 0x09;\n\t"
+      "mad.lo.u32 t, zp, %5, %6;\n\t"
+      "lop3.b32 h, t, 0x80008000, zp, 0x40;\n\t"
+      "setp.ne.u32 p, h, 0;\n\t"
+      "@p mad.lo.u32 %0, %5, %7, %0;\n\t}"
+      : "+r"(m)
+      : "r"(z1), "r"(g1), "r"(z2), "r"(u2), "r"(one), "r"(cneg), "n"(BIT));
+}
+
+template <int V, int WARPS, int MINB>
+__global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) {
+  constexpr int KB = 5;
+  constexpr int K = 1 << KB;
+  constexpr int NW = K / 2;  // packed words
+  constexpr int FIX = 5 + KB;
+  constexpr int SB = 1 << V;
+  constexpr int LG = 5 - V;  // a group of G superblocks fills the warp's lanes
+  constexpr int G = 1 << LG;
+  constexpr int MQ = SB / 2;  // pass masks per superblock (2 steps x 16 words each)
+  constexpr uint32_t BATCH = V >= 4 ? 1 : 2;  // superblocks per verify batch
+  static_assert(V >= 1 && V <= 5, "superblock");
+  __shared__ RowRec Rs[WARPS][32];         // n <= 32 rows
+  __shared__ uint2 Hs[WARPS][32];             // B states (z2, u2) of the group, lane = (c << V) | j
+  __shared__ uint4 As[WARPS][NW][32];         // full A words: slot w and slot w + 16
+  __shared__ uint32_t Mss[WARPS][BATCH * MQ][32];  // pass masks of the verify batch
+  __shared__ uint16_t Ls[WARPS][BATCH * MQ * 32];  // verify list: (lane << 4) | mask index
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t wid = threadIdx.x >> 5;
+  RowRec* R = Rs[wid];
+  uint2* H = Hs[wid];
+  uint4 (*A)[32] = As[wid];
+  uint16_t* Lst = Ls[wid];
+  uint32_t (*Ms)[32] = Mss[wid];
+  const uint32_t one = p.one;
+  const uint32_t cneg = 0xfffeffffu * one;  // -0x00010001, runtime so ptxas keeps the IMAD
+  const uint32_t colmask = p.z0_init;
+  const unsigned long long t_start = p.trace ? clock64() : 0;
+  unsigned long long n_items = 0;
+
+  for (;;) {
+    const unsigned long long item = next_item(p, lane, n_items, blockIdx.x * WARPS + wid);
+    if (item >= p.items) break;
+    ++n_items;
+    const unsigned long long b = item / p.chunks;
+    const unsigned long long A0 = p.F0 + (item - b * p.chunks) * p.L;
+    const unsigned long long B0 = A0 >> V;
+    __syncwarp();
+    load_rows(R, p.rows + b * 64, lane, p.n);
+    __syncwarp();
+
+    uint32_t SM[V], SS[V], SA[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      SM[v] = R[FIX + v].m[0];
+      SS[v] = R[FIX + v].s[0];
+      SA[v] = R[FIX + v].a[0];
+    }
+    // A side: v1 for S1 = (k << 5) | lane, k in Gray order; packed low halves
+    uint32_t Zp[NW], Gp[NW];
+    {
+      uint32_t z1[K], g1[K];
+      uint32_t zz[2], gg[2];
+      wide_subset_state<KB>(R, p.n, 0ull, lane, p.z0_init, p.z1_init, zz, gg);
+      uint32_t zc = zz[0], gc = gg[0];
+      static_for<K>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        if constexpr (i > 0) {
+          constexpr int t = ctz_c(i);
+          constexpr bool leave = ((gray_c(i - 1) >> t) & 1) != 0;
+          sub_word(zc, gc, R[5 + t].m[0], leave ? R[5 + t].s[0] : R[5 + t].a[0]);
+        }
+        z1[gray_c(i)] = zc;
+        g1[gray_c(i)] = gc;
+      });
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        Zp[w] = __byte_perm(z1[w], z1[w + NW], 0x5410);
+        Gp[w] = __byte_perm(g1[w], g1[w + NW], 0x5410);
+        A[w][lane] = make_uint4(z1[w], g1[w], z1[w + NW], g1[w + NW]);
+      }
+    }
+    // B side: v2 for S2 = gray(A0) on rows >= FIX (low bits empty)
+    uint32_t z2, u2;
+    {
+      uint32_t zz[2], gg[2];
+      wide_subset_state<KB>(R, p.n, A0, 0u, p.z0_init, p.z1_init, zz, gg);
+      z2 = zz[0];
+      u2 = pair_u2(zz[0], gg[0]);
+    }
+    __syncwarp();
+    uint32_t ev = 0, odd = 0;
+
+    // exact fold of superblock states Hb[0..SB) against all 32 slots
+    auto exact_block = [&](const uint2* Hb, uint32_t& bev, uint32_t& bodd) {
+      bev = bodd = 0;
+#pragma unroll 1
+      for (int j = 0; j < SB; ++j) {
+        const uint2 h = Hb[j];
+        const uint32_t gh = pair_g2(h.x, h.y);
+        uint32_t n0 = 0, a0 = 0, n1 = 0, a1 = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          const uint4 a = A[w][lane];
+          if (__popc(w) & 1) exact_fold(a.x, a.y, h.x, h.y, gh, colmask, n1, a1, one);
+          else exact_fold(a.x, a.y, h.x, h.y, gh, colmask, n0, a0, one);
+          if (__popc(w + NW) & 1) exact_fold(a.z, a.w, h.x, h.y, gh, colmask, n1, a1, one);
+          else exact_fold(a.z, a.w, h.x, h.y, gh, colmask, n0, a0, one);
+        }
+        const uint32_t pj = ((uint32_t)j ^ __popc(lane)) & 1u;
+        bev += n0 + n1;
+        bodd += pj ? (n0 - a0) + a1 : a0 + (n1 - a1);
+      }
+    };
+
+    bool dense = false;   // warp-uniform: exact mode on event-dense matrices
+    bool have = false;    // lanes hold the packed B states of the current group
+    uint32_t hoff = 0;    // superblocks since those states were computed
+    uint32_t nb = 0;      // superblocks in the pending verify batch
+    uint32_t nzq = 0;     // nonzero pass masks of the batch, bit (nb * MQ + q)
+    uint32_t zpk = 0, upk = 0;
+    for (uint32_t kb = 0; kb < p.nblk; ++kb) {
+      const unsigned long long B = B0 + kb;
+      if (dense) {
+        const uint32_t SX = (kb & 1u) ? SS[V - 1] : SA[V - 1];
+        const uint32_t CX = (kb & 1u) ? SA[V - 1] : SS[V - 1];
+        __syncwarp();
+        if (lane == 0) H[0] = make_uint2(z2, u2);
+        static_for<SB - 1>([&](auto jc) {
+          constexpr int j = decltype(jc)::value + 1;
+          constexpr int t = ctz_c(j);
+          constexpr bool leave = (t + 1 < V) ? (((j >> (t + 1)) & 1) != 0) : false;
+          const uint32_t sop = (t == V - 1) ? SX : (leave ? SS[t] : SA[t]);
+          const uint32_t cop = (t == V - 1) ? CX : (leave ? SA[t] : SS[t]);
+          sub_word_u(z2, u2, SM[t], sop, cop);
+          if (lane == 0) H[j] = make_uint2(z2, u2);
+        });
+        __syncwarp();
+        uint32_t bev, bodd;
+        exact_block(H, bev, bodd);
+        ev += bev;
+        odd += bodd;
+        dense = __any_sync(FULL, bev >= (uint32_t)K / 2);
+        have = false;
+      } else {
+        if (!have) {
+          // B states of the rest of this superblock's aligned group, one per
+          // lane (see tp_walk_pair.cu): lane (c << V) | j holds Gray index
+          // y = ((B + c) << V) | j, reached from the entry of B by the rows
+          // FIX + r for the bits r of gray(y) ^ gray(B << V).
+          uint32_t zj = z2, uj = u2;
+          const unsigned long long yB = B << V, y = ((B + (lane >> V)) << V) | (lane & (SB - 1));
+          const uint32_t gB = (uint32_t)(yB ^ (yB >> 1)), D = ((uint32_t)(y ^ (y >> 1)) ^ gB) & 31u;
+#pragma unroll
+          for (int r = 0; r < V + LG; ++r) {
+            if ((D >> r) & 1u) {
+              const bool lv = ((gB >> r) & 1u) != 0;
+              if (r < V) {
+                sub_word_u(zj, uj, SM[r], lv ? SS[r] : SA[r], lv ? SA[r] : SS[r]);
+              } else {
+                const RowRec& row = R[FIX + r];
+                sub_word_u(zj, uj, row.m[0], lv ? row.s[0] : row.a[0], lv ? row.a[0] : row.s[0]);
+              }
+            }
+          }
+          __syncwarp();
+          H[lane] = make_uint2(zj, uj);
+          zpk = __byte_perm(zj, zj, 0x1010);
+          upk = __byte_perm(uj, uj, 0x1010);
+          have = true;
+          hoff = 0;
+        }
+        // opaque zeros: ptxas would turn the first record of each mask into
+        // a SEL on the ALU pipe; keep every record an IMAD (FMA pipe)
+        uint32_t Mc[MQ];
+#pragma unroll
+        for (int q = 0; q < MQ; ++q) asm volatile("mov.u32 %0, 0;" : "=r"(Mc[q]));
+        static_for<SB>([&](auto jc) {
+          constexpr int j = decltype(jc)::value;
+          const uint32_t z2p = __shfl_sync(FULL, zpk, j), u2p = __shfl_sync(FULL, upk, j);
+          static_for<NW>([&](auto wc) {
+            constexpr int w = decltype(wc)::value;
+            packed_test<(1u << ((j & 1) * 16 + w))>(Zp[w], Gp[w], z2p, u2p, Mc[j >> 1], one, cneg);
+          });
+        });
+        // park the masks in shared memory: pass mask q of batch superblock nb
+        // at Ms[nb * MQ + q][lane]; nzq marks the nonzero ones
+#pragma unroll
+        for (int q = 0; q < MQ; ++q) {
+          Ms[nb * MQ + q][lane] = Mc[q];
+          nzq |= (Mc[q] != 0u ? 1u : 0u) << (nb * MQ + q);
+        }
+        ++nb;
+        const bool gend = ((B + 1) & (G - 1)) == 0;
+        if (nb == BATCH || gend || kb + 1 == p.nblk) {
+          // verify the batch: every nonzero mask becomes one list entry
+          // (exclusive scan of the per-lane counts), and lane e walks the
+          // pass bits of entry e
+          const uint32_t cnt = __popc(nzq);
+          uint32_t pre = cnt;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t v = __shfl_up_sync(FULL, pre, d);
+            if (lane >= (uint32_t)d) pre += v;
+          }
+          const uint32_t tot = __shfl_sync(FULL, pre, 31);
+          if (tot) {
+            uint32_t idx = pre - cnt, nzm = nzq;
+            while (nzm) {
+              const uint32_t c = __ffs(nzm) - 1;
+              nzm &= nzm - 1;
+              Lst[idx++] = (uint16_t)((lane << 4) | c);
+            }
+            __syncwarp();
+            uint32_t bev = 0, bodd = 0;
+            const uint32_t hfirst = hoff + 1 - nb;  // H block of the batch's first superblock
+            for (uint32_t e = lane; e < tot; e += 32) {
+              const uint32_t ent = Lst[e], src = ent >> 4, c = ent & 15u;
+              const uint32_t srcpar = __popc(src) & 1u;
+              const uint32_t hblk = hfirst + c / MQ, jb = 2 * (c % MQ);
+              uint32_t mm = Ms[c][src];
+              while (mm) {
+                const uint32_t bit = __ffs(mm) - 1;
+                mm &= mm - 1;
+                const uint32_t j = jb + (bit >> 4), w = bit & 15u;
+                const uint4 av = A[w][src];
+                const uint2 h = H[(hblk << V) + j];
+                const uint32_t gh = pair_g2(h.x, h.y);
+                uint32_t d, zp;
+                TP_LOP3(d, av.x, av.y, h.y, 0x06);
+                TP_LOP3(zp, d, av.x, h.x, 0x09);
+                if (zp == 0) {
+                  bev += 1;
+                  bodd += (__popc((d ^ gh) & colmask) + j + __popc(w) + srcpar) & 1u;
+                }
+                TP_LOP3(d, av.z, av.w, h.y, 0x06);
+                TP_LOP3(zp, d, av.z, h.x, 0x09);
+                if (zp == 0) {
+                  bev += 1;
+                  bodd += (__popc((d ^ gh) & colmask) + j + __popc(w + NW) + srcpar) & 1u;
+                }
+              }
+            }
+            ev += bev;
+            odd += bodd;
+            // switch to the exact mode when events are dense (e.g. all-ones rows)
+            dense = p.dense_ok != 0 && __reduce_add_sync(FULL, bev) >= (uint32_t)(32 * K * SB) / 8u;
+            __syncwarp();
+          }
+          nb = 0;
+          nzq = 0;
+        }
+        if (dense || gend) {
+          have = false;
+          // (z2, u2) = state of step SB-1 of this superblock, for the entry step
+          const uint2 h = H[(hoff << V) + SB - 1];
+          z2 = h.x;
+          u2 = h.y;
+        } else {
+          zpk = __shfl_down_sync(FULL, zpk, SB);
+          upk = __shfl_down_sync(FULL, upk, SB);
+          ++hoff;
+        }
+      }
+      // enter superblock kb+1 when the next superblock needs (z2, u2)
+      if (!have && kb + 1 < p.nblk) {
+        const uint32_t u = kb + 1;
+        const int t = __ffs(u) - 1;
+        const RowRec& row = R[FIX + V + t];
+        const bool lv = entry_leave(u, t, p, B0);
+        sub_word_u(z2, u2, row.m[0], lv ? row.s[0] : row.a[0], lv ? row.a[0] : row.s[0]);
+      }
+    }
+    warp_flush(p.pm + 2 * b, ev - odd, odd, lane);
+  }
+  queue_done(p, lane);
+  trace_end(p, t_start, n_items, blockIdx.x * WARPS + wid, lane);
+}
+
+// variant 0: V = 3; variant 1: V = 4 (4 CTAs/SM, 128 registers)
+cudaError_t launch_packed(int which, int grid, const FastParams& p, cudaStream_t st) {
+  if (which == 0) k_walk_packed<3, 4, 4><<<grid, 128, 0, st>>>(p);
+  else if (which == 1) k_walk_packed<4, 4, 4><<<grid, 128, 0, st>>>(p);
+  else return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
+const void* packed_symbol(int which) {
+  if (which == 0) return reinterpret_cast<const void*>(&k_walk_packed<3, 4, 4>);
+  if (which == 1) return reinterpret_cast<const void*>(&k_walk_packed<4, 4, 4>);
+  return nullptr;
+}
+
+}  // namespace tp
