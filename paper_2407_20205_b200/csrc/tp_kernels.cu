@@ -256,7 +256,7 @@ const void* packed_symbol(int V);
 const void* walk_fast_symbol(int v) {
   if (fast_is_lane(v)) return lane_symbol(fast_v(v));
   if (fast_is_pair(v)) return pair_symbol(fast_kb(v), fast_v(v), fast_pair_wide(v));
-  if (fast_is_packed(v)) return packed_symbol(v == kPackedK32V3 ? 0 : 1);
+  if (fast_is_packed(v)) return packed_symbol(packed_which(v));
   return wide_symbol(fast_kb(v), fast_v(v));
 }
 
@@ -268,7 +268,7 @@ const void* walk_generic_symbol(int nw) {
 cudaError_t launch_walk_fast(int v, int grid, const FastParams& p, cudaStream_t st) {
   if (fast_is_lane(v)) return launch_lane(fast_v(v), grid, p, st);
   if (fast_is_pair(v)) return launch_pair(fast_kb(v), fast_v(v), fast_pair_wide(v), grid, p, st);
-  if (fast_is_packed(v)) return launch_packed(v == kPackedK32V3 ? 0 : 1, grid, p, st);
+  if (fast_is_packed(v)) return launch_packed(packed_which(v), grid, p, st);
   return launch_wide(fast_kb(v), fast_v(v), grid, p, st);
 }
 

@@ -30,12 +30,14 @@ enum FastVariant {
   kPairWideK32V4 = 6,
   kPackedK32V3 = 7,
   kPackedK32V4 = 8,
-  kNumFast = 9
+  kPackedWideK32V4 = 9,
+  kNumFast = 10
 };
 constexpr bool fast_is_lane(int v) { return v == kLaneV5 || v == kLaneV8; }
 constexpr bool fast_is_pair(int v) { return v >= kPairK32V3 && v <= kPairWideK32V4; }
 constexpr bool fast_pair_wide(int v) { return v == kPairWideK32V3 || v == kPairWideK32V4; }
-constexpr bool fast_is_packed(int v) { return v == kPackedK32V3 || v == kPackedK32V4; }
+constexpr bool fast_is_packed(int v) { return v == kPackedK32V3 || v == kPackedK32V4 || v == kPackedWideK32V4; }
+constexpr int packed_which(int v) { return v == kPackedK32V3 ? 0 : v == kPackedK32V4 ? 1 : 2; }
 constexpr int fast_v(int v) {
   return v == kLaneV5 ? 5 : v == kLaneV8 ? 8 : v == kWideK4V6 ? 6
        : (v == kPairK32V3 || v == kPairWideK32V3 || v == kPackedK32V3) ? 3 : 4;

@@ -155,7 +155,7 @@ int choose_variant(int n) {
   const char* e = getenv("TRITPERM_FAST_VARIANT");  // read per call: tests switch it at run time
   const int forced = e ? atoi(e) : -1;
   if (forced >= 0 && forced < tp::kNumFast) {
-    const bool for_narrow = tp::fast_is_lane(forced) || tp::fast_is_packed(forced) ||
+    const bool for_narrow = tp::fast_is_lane(forced) || forced == tp::kPackedK32V3 || forced == tp::kPackedK32V4 ||
                             (tp::fast_is_pair(forced) && !tp::fast_pair_wide(forced));
     if (for_narrow == (n <= 32)) return forced;
   }

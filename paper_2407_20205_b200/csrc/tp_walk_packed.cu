@@ -41,7 +41,10 @@ __device__ __forceinline__ void packed_test(uint32_t z1, uint32_t g1, uint32_t z
       : "r"(z1), "r"(g1), "r"(z2), "r"(u2), "r"(one), "r"(cneg), "n"(BIT));
 }
 
-template <int V, int WARPS, int MINB>
+// WIDE (n > 32): the filter and the verify cover the 32 primary columns; a
+// verified primary hit (probability (2/3)^32) is evaluated over all n columns
+// from scratch, as in the wide pair walk.
+template <int V, int WARPS, int MINB, bool WIDE>
 __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) {
   constexpr int KB = 5;
   constexpr int K = 1 << KB;
@@ -53,7 +56,7 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) 
   constexpr int MQ = SB / 2;  // pass masks per superblock (2 steps x 16 words each)
   constexpr uint32_t BATCH = V >= 4 ? 1 : 2;  // superblocks per verify batch
   static_assert(V >= 1 && V <= 5, "superblock");
-  __shared__ RowRec Rs[WARPS][32];         // n <= 32 rows
+  __shared__ RowRec Rs[WARPS][WIDE ? 64 : 32];
   __shared__ uint2 Hs[WARPS][32];             // B states (z2, u2) of the group, lane = (c << V) | j
   __shared__ uint4 As[WARPS][NW][32];         // full A words: slot w and slot w + 16
   __shared__ uint32_t Mss[WARPS][BATCH * MQ][32];  // pass masks of the verify batch
@@ -146,6 +149,22 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) 
       }
     };
 
+    // a verified pass with a full primary word: exact for n <= 32; for n > 32
+    // the subset's n-column vector is recomputed and tested
+    auto hit = [&](uint32_t d, uint32_t gh, uint32_t j, uint32_t k, uint32_t src, uint32_t srcpar,
+                   unsigned long long sb, uint32_t& bev, uint32_t& bodd) {
+      if (!WIDE) {
+        bev += 1;
+        bodd += (__popc((d ^ gh) & colmask) + j + __popc(k) + srcpar) & 1u;
+      } else {
+        uint32_t zz[2], gg[2];
+        wide_subset_state<KB>(R, p.n, (sb << V) + j, (k << 5) | src, p.z0_init, p.z1_init, zz, gg);
+        if ((zz[0] | zz[1]) == 0) {
+          bev += 1;
+          bodd += (__popc(gg[0]) + __popc(gg[1]) + j + __popc(k) + srcpar) & 1u;
+        }
+      }
+    };
     bool dense = false;   // warp-uniform: exact mode on event-dense matrices
     bool have = false;    // lanes hold the packed B states of the current group
     uint32_t hoff = 0;    // superblocks since those states were computed
@@ -170,7 +189,13 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) 
         });
         __syncwarp();
         uint32_t bev, bodd;
-        exact_block(H, bev, bodd);
+        if (WIDE) {
+          const unsigned long long r = replay_wide<KB>(R, p.n, B << V, SB, lane, p.z0_init, p.z1_init);
+          bev = (uint32_t)r;
+          bodd = (uint32_t)(r >> 32);
+        } else {
+          exact_block(H, bev, bodd);
+        }
         ev += bev;
         odd += bodd;
         dense = __any_sync(FULL, bev >= (uint32_t)K / 2);
@@ -251,6 +276,7 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) 
               const uint32_t ent = Lst[e], src = ent >> 4, c = ent & 15u;
               const uint32_t srcpar = __popc(src) & 1u;
               const uint32_t hblk = hfirst + c / MQ, jb = 2 * (c % MQ);
+              const unsigned long long sb = B + 1 - nb + c / MQ;  // the entry's superblock
               uint32_t mm = Ms[c][src];
               while (mm) {
                 const uint32_t bit = __ffs(mm) - 1;
@@ -262,16 +288,10 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) 
                 uint32_t d, zp;
                 TP_LOP3(d, av.x, av.y, h.y, 0x06);
                 TP_LOP3(zp, d, av.x, h.x, 0x09);
-                if (zp == 0) {
-                  bev += 1;
-                  bodd += (__popc((d ^ gh) & colmask) + j + __popc(w) + srcpar) & 1u;
-                }
+                if (zp == 0) hit(d, gh, j, w, src, srcpar, sb, bev, bodd);
                 TP_LOP3(d, av.z, av.w, h.y, 0x06);
                 TP_LOP3(zp, d, av.z, h.x, 0x09);
-                if (zp == 0) {
-                  bev += 1;
-                  bodd += (__popc((d ^ gh) & colmask) + j + __popc(w + NW) + srcpar) & 1u;
-                }
+                if (zp == 0) hit(d, gh, j, w + NW, src, srcpar, sb, bev, bodd);
               }
             }
             ev += bev;
@@ -310,17 +330,19 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) 
   trace_end(p, t_start, n_items, blockIdx.x * WARPS + wid, lane);
 }
 
-// variant 0: V = 3; variant 1: V = 4 (4 CTAs/SM, 128 registers)
+// which: 0 = V 3, 1 = V 4 (n <= 32); 2 = V 4 wide (n > 32).  4 CTAs/SM.
 cudaError_t launch_packed(int which, int grid, const FastParams& p, cudaStream_t st) {
-  if (which == 0) k_walk_packed<3, 4, 4><<<grid, 128, 0, st>>>(p);
-  else if (which == 1) k_walk_packed<4, 4, 4><<<grid, 128, 0, st>>>(p);
+  if (which == 0) k_walk_packed<3, 4, 4, false><<<grid, 128, 0, st>>>(p);
+  else if (which == 1) k_walk_packed<4, 4, 4, false><<<grid, 128, 0, st>>>(p);
+  else if (which == 2) k_walk_packed<4, 4, 4, true><<<grid, 128, 0, st>>>(p);
   else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 
 const void* packed_symbol(int which) {
-  if (which == 0) return reinterpret_cast<const void*>(&k_walk_packed<3, 4, 4>);
-  if (which == 1) return reinterpret_cast<const void*>(&k_walk_packed<4, 4, 4>);
+  if (which == 0) return reinterpret_cast<const void*>(&k_walk_packed<3, 4, 4, false>);
+  if (which == 1) return reinterpret_cast<const void*>(&k_walk_packed<4, 4, 4, false>);
+  if (which == 2) return reinterpret_cast<const void*>(&k_walk_packed<4, 4, 4, true>);
   return nullptr;
 }
 

@@ -366,7 +366,7 @@ def test_event_dense_matrices_exact(gpu):
         assert part[b] == o.chunk_sum(mags, sgns, 26, 1, 1 << 26)
 
 
-@pytest.mark.parametrize("variant", range(9))
+@pytest.mark.parametrize("variant", range(10))
 def test_every_fast_walk_variant(gpu, oracle, variant, monkeypatch):
     """Each fast-walk kernel (lane V5/V8, wide, pair narrow/wide V3/V4),
     forced through TRITPERM_FAST_VARIANT, on ranges with heads/tails, a full
