@@ -54,23 +54,23 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) 
   constexpr int LG = 5 - V;  // a group of G superblocks fills the warp's lanes
   constexpr int G = 1 << LG;
   constexpr int MQ = SB / 2;  // pass masks per superblock (2 steps x 16 words each)
-  constexpr uint32_t BATCH = V >= 4 ? 1 : 2;  // superblocks per verify batch
   static_assert(V >= 1 && V <= 5, "superblock");
   __shared__ RowRec Rs[WARPS][WIDE ? 64 : 32];
   __shared__ uint2 Hs[WARPS][32];             // B states (z2, u2) of the group, lane = (c << V) | j
   __shared__ uint4 As[WARPS][NW][32];         // full A words: slot w and slot w + 16
-  __shared__ uint32_t Mss[WARPS][BATCH * MQ][32];  // pass masks of the verify batch
-  __shared__ uint16_t Ls[WARPS][BATCH * MQ * 32];  // verify list: (lane << 4) | mask index
+  constexpr uint32_t LCAP = 128;                // verify list capacity (uniform inputs: ~23 entries)
+  __shared__ uint2 Ls[WARPS][LCAP];              // verify list: ((lane << 4) | mask index, mask)
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t wid = threadIdx.x >> 5;
   RowRec* R = Rs[wid];
   uint2* H = Hs[wid];
   uint4 (*A)[32] = As[wid];
-  uint16_t* Lst = Ls[wid];
-  uint32_t (*Ms)[32] = Mss[wid];
+  uint2* Lst = Ls[wid];
   const uint32_t one = p.one;
   const uint32_t cneg = 0xfffeffffu * one;  // -0x00010001, runtime so ptxas keeps the IMAD
   const uint32_t colmask = p.z0_init;
+  const uint32_t zero = one - 1u;  // runtime 0: keeps the first record of a mask an IMAD
+  const uint32_t lanemask_lt = (1u << lane) - 1u;
   const unsigned long long t_start = p.trace ? clock64() : 0;
   unsigned long long n_items = 0;
 
@@ -168,8 +168,6 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) 
     bool dense = false;   // warp-uniform: exact mode on event-dense matrices
     bool have = false;    // lanes hold the packed B states of the current group
     uint32_t hoff = 0;    // superblocks since those states were computed
-    uint32_t nb = 0;      // superblocks in the pending verify batch
-    uint32_t nzq = 0;     // nonzero pass masks of the batch, bit (nb * MQ + q)
     uint32_t zpk = 0, upk = 0;
     for (uint32_t kb = 0; kb < p.nblk; ++kb) {
       const unsigned long long B = B0 + kb;
@@ -228,11 +226,9 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) 
           have = true;
           hoff = 0;
         }
-        // opaque zeros: ptxas would turn the first record of each mask into
-        // a SEL on the ALU pipe; keep every record an IMAD (FMA pipe)
         uint32_t Mc[MQ];
 #pragma unroll
-        for (int q = 0; q < MQ; ++q) asm volatile("mov.u32 %0, 0;" : "=r"(Mc[q]));
+        for (int q = 0; q < MQ; ++q) Mc[q] = zero;
         static_for<SB>([&](auto jc) {
           constexpr int j = decltype(jc)::value;
           const uint32_t z2p = __shfl_sync(FULL, zpk, j), u2p = __shfl_sync(FULL, upk, j);
@@ -241,67 +237,65 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) 
             packed_test<(1u << ((j & 1) * 16 + w))>(Zp[w], Gp[w], z2p, u2p, Mc[j >> 1], one, cneg);
           });
         });
-        // park the masks in shared memory: pass mask q of batch superblock nb
-        // at Ms[nb * MQ + q][lane]; nzq marks the nonzero ones
+        const bool gend = ((B + 1) & (G - 1)) == 0;
+        // verify this superblock's passes: every nonzero mask becomes one list
+        // entry (ballot compaction), and lane e walks the bits of entry e
+        uint32_t bq[MQ], tot = 0;
 #pragma unroll
         for (int q = 0; q < MQ; ++q) {
-          Ms[nb * MQ + q][lane] = Mc[q];
-          nzq |= (Mc[q] != 0u ? 1u : 0u) << (nb * MQ + q);
+          bq[q] = __ballot_sync(FULL, Mc[q] != 0u);
+          tot += __popc(bq[q]);
         }
-        ++nb;
-        const bool gend = ((B + 1) & (G - 1)) == 0;
-        if (nb == BATCH || gend || kb + 1 == p.nblk) {
-          // verify the batch: every nonzero mask becomes one list entry
-          // (exclusive scan of the per-lane counts), and lane e walks the
-          // pass bits of entry e
-          const uint32_t cnt = __popc(nzq);
-          uint32_t pre = cnt;
+        if (tot > LCAP) {
+          // too many passes for the list (event-dense matrix): evaluate the
+          // superblock exactly and let the dense test decide the next mode
+          uint32_t bev, bodd;
+          if (WIDE) {
+            const unsigned long long r = replay_wide<KB>(R, p.n, B << V, SB, lane, p.z0_init, p.z1_init);
+            bev = (uint32_t)r;
+            bodd = (uint32_t)(r >> 32);
+          } else {
+            exact_block(H + (hoff << V), bev, bodd);
+          }
+          ev += bev;
+          odd += bodd;
+          dense = p.dense_ok != 0 && __any_sync(FULL, bev >= (uint32_t)K / 2);
+        } else if (tot) {
+          uint32_t base = 0;
 #pragma unroll
-          for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t v = __shfl_up_sync(FULL, pre, d);
-            if (lane >= (uint32_t)d) pre += v;
+          for (int q = 0; q < MQ; ++q) {
+            if (Mc[q]) Lst[base + __popc(bq[q] & lanemask_lt)] = make_uint2((lane << 4) | (uint32_t)q, Mc[q]);
+            base += __popc(bq[q]);
           }
-          const uint32_t tot = __shfl_sync(FULL, pre, 31);
-          if (tot) {
-            uint32_t idx = pre - cnt, nzm = nzq;
-            while (nzm) {
-              const uint32_t c = __ffs(nzm) - 1;
-              nzm &= nzm - 1;
-              Lst[idx++] = (uint16_t)((lane << 4) | c);
+          __syncwarp();
+          uint32_t bev = 0, bodd = 0;
+          const uint32_t hblk = hoff << V;
+          for (uint32_t e = lane; e < tot; e += 32) {
+            const uint2 ent = Lst[e];
+            const uint32_t src = ent.x >> 4, jb = 2 * (ent.x & 15u);
+            const uint32_t srcpar = __popc(src) & 1u;
+            uint32_t mm = ent.y;
+            while (mm) {
+              const uint32_t bit = __ffs(mm) - 1;
+              mm &= mm - 1;
+              const uint32_t j = jb + (bit >> 4), w = bit & 15u;
+              const uint4 av = A[w][src];
+              const uint2 h = H[hblk + j];
+              const uint32_t gh = pair_g2(h.x, h.y);
+              uint32_t d, zp;
+              TP_LOP3(d, av.x, av.y, h.y, 0x06);
+              TP_LOP3(zp, d, av.x, h.x, 0x09);
+              if (zp == 0) hit(d, gh, j, w, src, srcpar, B, bev, bodd);
+              TP_LOP3(d, av.z, av.w, h.y, 0x06);
+              TP_LOP3(zp, d, av.z, h.x, 0x09);
+              if (zp == 0) hit(d, gh, j, w + NW, src, srcpar, B, bev, bodd);
             }
-            __syncwarp();
-            uint32_t bev = 0, bodd = 0;
-            const uint32_t hfirst = hoff + 1 - nb;  // H block of the batch's first superblock
-            for (uint32_t e = lane; e < tot; e += 32) {
-              const uint32_t ent = Lst[e], src = ent >> 4, c = ent & 15u;
-              const uint32_t srcpar = __popc(src) & 1u;
-              const uint32_t hblk = hfirst + c / MQ, jb = 2 * (c % MQ);
-              const unsigned long long sb = B + 1 - nb + c / MQ;  // the entry's superblock
-              uint32_t mm = Ms[c][src];
-              while (mm) {
-                const uint32_t bit = __ffs(mm) - 1;
-                mm &= mm - 1;
-                const uint32_t j = jb + (bit >> 4), w = bit & 15u;
-                const uint4 av = A[w][src];
-                const uint2 h = H[(hblk << V) + j];
-                const uint32_t gh = pair_g2(h.x, h.y);
-                uint32_t d, zp;
-                TP_LOP3(d, av.x, av.y, h.y, 0x06);
-                TP_LOP3(zp, d, av.x, h.x, 0x09);
-                if (zp == 0) hit(d, gh, j, w, src, srcpar, sb, bev, bodd);
-                TP_LOP3(d, av.z, av.w, h.y, 0x06);
-                TP_LOP3(zp, d, av.z, h.x, 0x09);
-                if (zp == 0) hit(d, gh, j, w + NW, src, srcpar, sb, bev, bodd);
-              }
-            }
-            ev += bev;
-            odd += bodd;
-            // switch to the exact mode when events are dense (e.g. all-ones rows)
-            dense = p.dense_ok != 0 && __reduce_add_sync(FULL, bev) >= (uint32_t)(32 * K * SB) / 8u;
-            __syncwarp();
           }
-          nb = 0;
-          nzq = 0;
+          ev += bev;
+          odd += bodd;
+          // switch to the exact mode when events are dense (e.g. all-ones rows)
+          dense = p.dense_ok != 0 && __reduce_add_sync(FULL, bev) >= (uint32_t)(32 * K * SB) / 8u;
+          __syncwarp();
         }
         if (dense || gend) {
           have = false;
