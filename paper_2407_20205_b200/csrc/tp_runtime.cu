@@ -161,7 +161,7 @@ int choose_variant(int n) {
   }
   // short walks (n <= 21, <= 2^16 high steps) favour parallelism: more, smaller items
   if (n <= 32) return n >= 22 ? tp::kPackedK32V4 : tp::kLaneV5;
-  return tp::kPairWideK32V4;
+  return tp::kPackedWideK32V4;
 }
 
 // Optional CTA trace buffer for the fast walks (tp_debug_trace).
@@ -661,7 +661,7 @@ int tp_walk_info(int n, char* name, int name_len, double* lop3_per_term) {
     kind = tp::fast_pair_wide(v) ? "k_walk_pair<wide>" : "k_walk_pair";
     ops = 2.0;
   } else if (tp::fast_is_packed(v)) {
-    kind = "k_walk_packed";  // 3 LOP3 per packed word of two pairs
+    kind = v == tp::kPackedWideK32V4 ? "k_walk_packed<wide>" : "k_walk_packed";  // 3 LOP3 per word of two pairs
     ops = 1.5;
   } else if (tp::fast_is_lane(v)) {
     kind = "k_walk_lane";
