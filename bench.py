@@ -449,7 +449,10 @@ def main():
                        "terms_per_step": job_terms},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "LOP3 ops/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": kernel_name + " (csrc/tp_kernels.cu)",
+                         "kernel": kernel_name + " (csrc/" + ("tp_walk_packed.cu" if "packed" in kernel_name
+                                                              else "tp_walk_pair.cu" if "pair" in kernel_name
+                                                              else "tp_walk_lane.cu" if "lane" in kernel_name
+                                                              else "tp_walk_wide.cu") + ")",
                          "ops_per_term": ops_per_term,
                          "peak_source": "LOP3 chain probe (tp_alu_peak) on this GPU in this run; "
                                         "nominal 148 SM x 64 lanes x clock",
