@@ -244,7 +244,9 @@ __device__ __forceinline__ void sub_word_u(uint32_t& z, uint32_t& u, uint32_t m,
   u = un;
 }
 // Exact fold of one pair (n <= 32): if v1 + v2 is full, n += 1 and
-// a += parity(popc(sign word)); predicated, no branches.
+// a += parity(popc(sign word)).  4 LOP3 per pair on the ALU pipe; the
+// popcount goes to the (quarter-rate) XU pipe and the two accumulations to the
+// FMA pipe (a runtime `one` keeps ptxas from turning them into ALU adds).
 __device__ __forceinline__ void exact_fold(uint32_t z1, uint32_t g1, uint32_t z2, uint32_t u2, uint32_t g2,
                                            uint32_t cm, uint32_t& n, uint32_t& a, uint32_t one) {
   uint32_t d, zp, x;
@@ -252,8 +254,10 @@ __device__ __forceinline__ void exact_fold(uint32_t z1, uint32_t g1, uint32_t z2
   TP_LOP3(zp, d, z1, z2, 0x09);
   TP_LOP3(x, d, g2, cm, 0x28);
   if (zp == 0) {
-    n += one;
-    a += __popc(x) & 1u;
+    uint32_t t;
+    asm("and.b32 %0, %1, 1;" : "=r"(t) : "r"(__popc(x)));  // opaque to the front end: stays an IMAD below
+    n = one * one + n;
+    a = t * one + a;
   }
 }
 

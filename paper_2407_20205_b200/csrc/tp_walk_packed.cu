@@ -44,6 +44,35 @@ __device__ __forceinline__ void packed_test(uint32_t z1, uint32_t g1, uint32_t z
 // WIDE (n > 32): the filter and the verify cover the 32 primary columns; a
 // verified primary hit (probability (2/3)^32) is evaluated over all n columns
 // from scratch, as in the wide pair walk.
+// Exact fold of the B states Hb[0..SB) against the lane's 32 slots (full A
+// words in shared memory): the dense mode.  Not inlined, so that its
+// registers do not constrain the filter loop's allocation.
+template <int SB>
+static __device__ __noinline__ unsigned long long packed_exact_block(const uint4 (*A)[32], const uint2* Hb,
+                                                                     uint32_t lane, uint32_t colmask, uint32_t one) {
+  constexpr int NW = 16;
+  uint32_t bev = 0, bodd = 0;
+#pragma unroll 1
+  for (int j = 0; j < SB; ++j) {
+    const uint2 h = Hb[j];
+    const uint32_t gh = pair_g2(h.x, h.y);
+    uint32_t n0 = 0, a0 = 0, n1 = 0, a1 = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const uint4 a = A[w][lane];
+      if (__popc(w) & 1) exact_fold(a.x, a.y, h.x, h.y, gh, colmask, n1, a1, one);
+      else exact_fold(a.x, a.y, h.x, h.y, gh, colmask, n0, a0, one);
+      if (__popc(w + NW) & 1) exact_fold(a.z, a.w, h.x, h.y, gh, colmask, n1, a1, one);
+      else exact_fold(a.z, a.w, h.x, h.y, gh, colmask, n0, a0, one);
+    }
+    // term parity: popc(sign word) + j + popc(slot) + lane parity
+    const uint32_t pj = ((uint32_t)j ^ __popc(lane)) & 1u;
+    bev += n0 + n1;
+    bodd += pj ? (n0 - a0) + a1 : a0 + (n1 - a1);
+  }
+  return (unsigned long long)bev | ((unsigned long long)bodd << 32);
+}
+
 template <int V, int WARPS, int MINB, bool WIDE>
 __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) {
   constexpr int KB = 5;
@@ -127,28 +156,6 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) 
     __syncwarp();
     uint32_t ev = 0, odd = 0;
 
-    // exact fold of superblock states Hb[0..SB) against all 32 slots
-    auto exact_block = [&](const uint2* Hb, uint32_t& bev, uint32_t& bodd) {
-      bev = bodd = 0;
-#pragma unroll 1
-      for (int j = 0; j < SB; ++j) {
-        const uint2 h = Hb[j];
-        const uint32_t gh = pair_g2(h.x, h.y);
-        uint32_t n0 = 0, a0 = 0, n1 = 0, a1 = 0;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-          const uint4 a = A[w][lane];
-          if (__popc(w) & 1) exact_fold(a.x, a.y, h.x, h.y, gh, colmask, n1, a1, one);
-          else exact_fold(a.x, a.y, h.x, h.y, gh, colmask, n0, a0, one);
-          if (__popc(w + NW) & 1) exact_fold(a.z, a.w, h.x, h.y, gh, colmask, n1, a1, one);
-          else exact_fold(a.z, a.w, h.x, h.y, gh, colmask, n0, a0, one);
-        }
-        const uint32_t pj = ((uint32_t)j ^ __popc(lane)) & 1u;
-        bev += n0 + n1;
-        bodd += pj ? (n0 - a0) + a1 : a0 + (n1 - a1);
-      }
-    };
-
     // a verified pass with a full primary word: exact for n <= 32; for n > 32
     // the subset's n-column vector is recomputed and tested
     auto hit = [&](uint32_t d, uint32_t gh, uint32_t j, uint32_t k, uint32_t src, uint32_t srcpar,
@@ -192,7 +199,9 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) 
           bev = (uint32_t)r;
           bodd = (uint32_t)(r >> 32);
         } else {
-          exact_block(H, bev, bodd);
+          const unsigned long long r = packed_exact_block<SB>(A, H, lane, colmask, one);
+          bev = (uint32_t)r;
+          bodd = (uint32_t)(r >> 32);
         }
         ev += bev;
         odd += bodd;
@@ -255,7 +264,9 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) 
             bev = (uint32_t)r;
             bodd = (uint32_t)(r >> 32);
           } else {
-            exact_block(H + (hoff << V), bev, bodd);
+            const unsigned long long r = packed_exact_block<SB>(A, H + (hoff << V), lane, colmask, one);
+            bev = (uint32_t)r;
+            bodd = (uint32_t)(r >> 32);
           }
           ev += bev;
           odd += bodd;
