@@ -87,14 +87,16 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) 
   __shared__ RowRec Rs[WARPS][WIDE ? 64 : 32];
   __shared__ uint2 Hs[WARPS][32];             // B states (z2, u2) of the group, lane = (c << V) | j
   __shared__ uint4 As[WARPS][NW][32];         // full A words: slot w and slot w + 16
-  constexpr uint32_t LCAP = 128;                // verify list capacity (uniform inputs: ~23 entries)
-  __shared__ uint2 Ls[WARPS][LCAP];              // verify list: ((lane << 4) | mask index, mask)
+  constexpr uint32_t LCAP = 64;                 // verify list capacity (uniform inputs: ~22 entries)
+  __shared__ uint4 Ls[WARPS][LCAP];              // verify list: ((lane << 4) | mask pair, mask, mask, -)
+  __shared__ uint2 HPs[WARPS][32];               // packed (low 16 columns doubled) B states of the group
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t wid = threadIdx.x >> 5;
   RowRec* R = Rs[wid];
   uint2* H = Hs[wid];
   uint4 (*A)[32] = As[wid];
-  uint2* Lst = Ls[wid];
+  uint4* Lst = Ls[wid];
+  uint2* HP = HPs[wid];
   const uint32_t one = p.one;
   const uint32_t cneg = 0xfffeffffu * one;  // -0x00010001, runtime so ptxas keeps the IMAD
   const uint32_t colmask = p.z0_init;
@@ -175,7 +177,6 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) 
     bool dense = false;   // warp-uniform: exact mode on event-dense matrices
     bool have = false;    // lanes hold the packed B states of the current group
     uint32_t hoff = 0;    // superblocks since those states were computed
-    uint32_t zpk = 0, upk = 0;
     for (uint32_t kb = 0; kb < p.nblk; ++kb) {
       const unsigned long long B = B0 + kb;
       if (dense) {
@@ -230,29 +231,36 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) 
           }
           __syncwarp();
           H[lane] = make_uint2(zj, uj);
-          zpk = __byte_perm(zj, zj, 0x1010);
-          upk = __byte_perm(uj, uj, 0x1010);
+          HP[lane] = make_uint2(__byte_perm(zj, zj, 0x1010), __byte_perm(uj, uj, 0x1010));
+          __syncwarp();
           have = true;
           hoff = 0;
         }
         uint32_t Mc[MQ];
 #pragma unroll
         for (int q = 0; q < MQ; ++q) Mc[q] = zero;
-        static_for<SB>([&](auto jc) {
-          constexpr int j = decltype(jc)::value;
-          const uint32_t z2p = __shfl_sync(FULL, zpk, j), u2p = __shfl_sync(FULL, upk, j);
+        // the packed B states of steps j, j+1 in one uniform 16-byte load
+        const uint4* HP4 = reinterpret_cast<const uint4*>(HP + (hoff << V));
+        static_for<SB / 2>([&](auto ic) {
+          constexpr int i = decltype(ic)::value;
+          const uint4 hp = HP4[i];
           static_for<NW>([&](auto wc) {
             constexpr int w = decltype(wc)::value;
-            packed_test<(1u << ((j & 1) * 16 + w))>(Zp[w], Gp[w], z2p, u2p, Mc[j >> 1], one, cneg);
+            packed_test<(1u << w)>(Zp[w], Gp[w], hp.x, hp.y, Mc[i], one, cneg);
+          });
+          static_for<NW>([&](auto wc) {
+            constexpr int w = decltype(wc)::value;
+            packed_test<(1u << (16 + w))>(Zp[w], Gp[w], hp.z, hp.w, Mc[i], one, cneg);
           });
         });
         const bool gend = ((B + 1) & (G - 1)) == 0;
         // verify this superblock's passes: every nonzero mask becomes one list
         // entry (ballot compaction), and lane e walks the bits of entry e
-        uint32_t bq[MQ], tot = 0;
+        constexpr int MP = MQ / 2;  // mask pairs
+        uint32_t bq[MP], tot = 0;
 #pragma unroll
-        for (int q = 0; q < MQ; ++q) {
-          bq[q] = __ballot_sync(FULL, Mc[q] != 0u);
+        for (int q = 0; q < MP; ++q) {
+          bq[q] = __ballot_sync(FULL, (Mc[2 * q] | Mc[2 * q + 1]) != 0u);
           tot += __popc(bq[q]);
         }
         if (tot > LCAP) {
@@ -274,22 +282,26 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) 
         } else if (tot) {
           uint32_t base = 0;
 #pragma unroll
-          for (int q = 0; q < MQ; ++q) {
-            if (Mc[q]) Lst[base + __popc(bq[q] & lanemask_lt)] = make_uint2((lane << 4) | (uint32_t)q, Mc[q]);
+          for (int q = 0; q < MP; ++q) {
+            if (Mc[2 * q] | Mc[2 * q + 1])
+              Lst[base + __popc(bq[q] & lanemask_lt)] = make_uint4((lane << 4) | (uint32_t)q, Mc[2 * q], Mc[2 * q + 1], 0u);
             base += __popc(bq[q]);
           }
           __syncwarp();
           uint32_t bev = 0, bodd = 0;
           const uint32_t hblk = hoff << V;
           for (uint32_t e = lane; e < tot; e += 32) {
-            const uint2 ent = Lst[e];
-            const uint32_t src = ent.x >> 4, jb = 2 * (ent.x & 15u);
+            const uint4 ent = Lst[e];
+            const uint32_t src = ent.x >> 4, jb = 4 * (ent.x & 15u);
             const uint32_t srcpar = __popc(src) & 1u;
-            uint32_t mm = ent.y;
-            while (mm) {
+            uint32_t m0 = ent.y, m1 = ent.z;
+            while (m0 | m1) {
+              // bit b of mask 2q + h: step 4q + 2h + (b >> 4), word b & 15
+              const uint32_t hsel = m0 ? 0u : 1u;
+              const uint32_t mm = m0 ? m0 : m1;
               const uint32_t bit = __ffs(mm) - 1;
-              mm &= mm - 1;
-              const uint32_t j = jb + (bit >> 4), w = bit & 15u;
+              if (hsel) m1 &= m1 - 1; else m0 &= m0 - 1;
+              const uint32_t j = jb + 2 * hsel + (bit >> 4), w = bit & 15u;
               const uint4 av = A[w][src];
               const uint2 h = H[hblk + j];
               const uint32_t gh = pair_g2(h.x, h.y);
@@ -315,8 +327,6 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) 
           z2 = h.x;
           u2 = h.y;
         } else {
-          zpk = __shfl_down_sync(FULL, zpk, SB);
-          upk = __shfl_down_sync(FULL, upk, SB);
           ++hoff;
         }
       }
