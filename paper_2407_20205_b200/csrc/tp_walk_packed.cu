@@ -73,6 +73,18 @@ static __device__ __noinline__ unsigned long long packed_exact_block(const uint4
   return (unsigned long long)bev | ((unsigned long long)bodd << 32);
 }
 
+// Term of one subset for n > 32, from scratch: bit 0 = all n columns
+// nonzero, bits 2.. = popc of the sign words (0 when not full).  Not inlined
+// (a primary hit has probability (2/3)^32; keeps the hot code small).
+template <int KB>
+static __device__ __noinline__ uint32_t wide_hit_term(const RowRec* R, int n, unsigned long long a, uint32_t low,
+                                                      uint32_t z0i, uint32_t z1i) {
+  uint32_t zz[2], gg[2];
+  wide_subset_state<KB>(R, n, a, low, z0i, z1i, zz, gg);
+  if ((zz[0] | zz[1]) != 0) return 0u;
+  return 1u | ((uint32_t)(__popc(gg[0]) + __popc(gg[1])) << 2);
+}
+
 template <int V, int WARPS, int MINB, bool WIDE>
 __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) {
   constexpr int KB = 5;
@@ -166,12 +178,9 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) 
         bev += 1;
         bodd += (__popc((d ^ gh) & colmask) + j + __popc(k) + srcpar) & 1u;
       } else {
-        uint32_t zz[2], gg[2];
-        wide_subset_state<KB>(R, p.n, (sb << V) + j, (k << 5) | src, p.z0_init, p.z1_init, zz, gg);
-        if ((zz[0] | zz[1]) == 0) {
-          bev += 1;
-          bodd += (__popc(gg[0]) + __popc(gg[1]) + j + __popc(k) + srcpar) & 1u;
-        }
+        const uint32_t r = wide_hit_term<KB>(R, p.n, (sb << V) + j, (k << 5) | src, p.z0_init, p.z1_init);
+        bev += r & 1u;
+        bodd += (r & 1u) & ((r >> 2) + j + __popc(k) + srcpar);
       }
     };
     bool dense = false;   // warp-uniform: exact mode on event-dense matrices
