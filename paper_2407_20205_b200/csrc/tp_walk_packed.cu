@@ -59,7 +59,12 @@ static __device__ __noinline__ unsigned long long packed_exact_block(const uint4
     uint32_t n0 = 0, a0 = 0, n1 = 0, a1 = 0;
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
-      const uint4 a = A[w][lane];
+      // re-read per step (volatile): hoisting all 16 loads out of the j loop
+      // would leave the fold one temporary register and serialise it
+      uint4 a;
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w)
+                   : "r"((uint32_t)__cvta_generic_to_shared(&A[w][lane])));
       if (__popc(w) & 1) exact_fold(a.x, a.y, h.x, h.y, gh, colmask, n1, a1, one);
       else exact_fold(a.x, a.y, h.x, h.y, gh, colmask, n0, a0, one);
       if (__popc(w + NW) & 1) exact_fold(a.z, a.w, h.x, h.y, gh, colmask, n1, a1, one);
