@@ -378,7 +378,7 @@ def main():
     # ALU roofline of the walk kernel: LOP3 per subset term of the kernel that
     # served this n (2 for the pair walk, 3 for the lane/wide walks; n > 32
     # tests only the 32 primary columns -- see DESIGN.md)
-    kernel_name, ops_per_term = _kernels.walk_info(n)
+    kernel_name, ops_per_term = _kernels.walk_info(n, B)
     walk_avg = sum(walk_ms) / len(walk_ms)
     achieved = per_rank_terms * ops_per_term / (walk_avg * 1e-3)
     peak, _ = _kernels.alu_peak(local)

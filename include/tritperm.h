@@ -132,9 +132,11 @@ int tp_finalize_async(const uint64_t *d_pm, int64_t B, int n, int device,
  * it to 3^((n-2) n) rank computations over F3 (see csrc/tp_census.cu). */
 int tp_exact_census(int n, int device, int64_t *zeros, int64_t *plus, int64_t *minus);
 
-/* Which walk kernel serves full traversals of size n, and its LOP3 count
- * per subset term (3 for the lane/wide walks, 2 for the pair walk). */
-int tp_walk_info(int n, char *name, int name_len, double *lop3_per_term);
+/* Which walk kernel serves full traversals of `batch` matrices of size n
+ * (batch = 1: a single matrix or a range), and its LOP3 count per subset
+ * term (3 for the lane/wide walks, 2 for the pair walks, 1.5 for the packed
+ * walks). */
+int tp_walk_info(int n, long long batch, char *name, int name_len, double *lop3_per_term);
 
 /* Diagnostics: measured LOP3 throughput of `device` (ops/s, the ALU-pipe
  * roofline denominator) from a register-resident lop3 chain kernel timed

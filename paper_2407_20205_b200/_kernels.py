@@ -72,7 +72,8 @@ SIGNATURES = {
     "tp_finalize_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "tp_debug_trace": (ctypes.c_int, [ctypes.c_void_p]),
-    "tp_walk_info": (ctypes.c_int, [ctypes.c_int, ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
+    "tp_walk_info": (ctypes.c_int, [ctypes.c_int, ctypes.c_longlong, ctypes.c_char_p, ctypes.c_int,
+                                    ctypes.POINTER(ctypes.c_double)]),
     "tp_exact_census": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _i64p, _i64p, _i64p]),
     "tp_alu_peak": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
 }
@@ -239,11 +240,12 @@ def finalize_async(d_pm_ptr: int, B: int, n: int, d_class_ptr: int, d_hist_ptr: 
                                    ctypes.c_void_p(d_hist_ptr), ctypes.c_void_p(stream_ptr)))
 
 
-def walk_info(n: int) -> Tuple[str, float]:
-    """(kernel description, LOP3 per subset term) for full traversals of size n."""
+def walk_info(n: int, batch: int = 1) -> Tuple[str, float]:
+    """(kernel description, LOP3 per subset term) for full traversals of
+    `batch` matrices of size n."""
     buf = ctypes.create_string_buffer(128)
     ops = ctypes.c_double()
-    _check(lib().tp_walk_info(n, buf, 128, ctypes.byref(ops)))
+    _check(lib().tp_walk_info(n, batch, buf, 128, ctypes.byref(ops)))
     return buf.value.decode(), float(ops.value)
 
 

@@ -151,7 +151,7 @@ struct Plan {
 // raise the chance that one lane sees two events of the same step parity in a
 // block (which forces an exact replay); events have probability (2/3)^n.
 // Override with TRITPERM_FAST_VARIANT for measurements.
-int choose_variant(int n) {
+int choose_variant(int n, unsigned long long B) {
   const char* e = getenv("TRITPERM_FAST_VARIANT");  // read per call: tests switch it at run time
   const int forced = e ? atoi(e) : -1;
   if (forced >= 0 && forced < tp::kNumFast) {
@@ -159,8 +159,14 @@ int choose_variant(int n) {
                             (tp::fast_is_pair(forced) && !tp::fast_pair_wide(forced));
     if (for_narrow == (n <= 32)) return forced;
   }
-  // short walks (n <= 21, <= 2^16 high steps) favour parallelism: more, smaller items
-  if (n <= 32) return n >= 22 ? tp::kPackedK32V4 : tp::kLaneV5;
+  // The packed walk needs enough work to fill the GPU with its items (at
+  // least 32 fast units = 2^15 subsets each): B * 2^(n-15) >= 2048.  Smaller
+  // jobs (one matrix up to n = 25, small batches) run the lane walk, whose
+  // items are 32x shorter.
+  if (n <= 32) {
+    const bool packed = n >= 16 && (B << (n - 15)) >= 2048ull;
+    return packed ? tp::kPackedK32V4 : tp::kLaneV5;
+  }
   return tp::kPackedWideK32V4;
 }
 
@@ -186,7 +192,7 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
                const RowRec* rows, unsigned long long* pm, Plan& pl) {
   pl = Plan();
   pl.nw = n <= 32 ? 1 : 2;
-  pl.variant = choose_variant(n);
+  pl.variant = choose_variant(n, B);
   const int V = tp::fast_v(pl.variant);
   const int U = tp::fast_kb(pl.variant);  // log2(fast unit / 32 reference steps)
   const uint32_t z0 = zmask(std::min(n, 32)), z1 = zmask(n - 32);
@@ -649,9 +655,10 @@ int tp_exact_census(int n, int device, int64_t* zeros, int64_t* plus, int64_t* m
   return TP_OK;
 }
 
-int tp_walk_info(int n, char* name, int name_len, double* lop3_per_term) {
+int tp_walk_info(int n, long long batch, char* name, int name_len, double* lop3_per_term) {
   if (n < 1 || n > TP_MAX_N) return fail(TP_E_INVALID, "need 1 <= n <= %d, got %d", TP_MAX_N, n);
-  const int v = choose_variant(n);
+  if (batch < 1) return fail(TP_E_INVALID, "need batch >= 1, got %lld", batch);
+  const int v = choose_variant(n, (unsigned long long)batch);
   const char* kind;
   double ops;
   if (n <= tp::kSmallMaxN) {
