@@ -430,3 +430,25 @@ def test_work_queue_resets_between_launches(gpu, oracle):
         for b in (0, B - 1):
             mags, sgns = oracle.planes_from_classes(e[b])
             assert int(results[0][b, 0]) - int(results[0][b, 1]) == oracle.chunk_sum(mags, sgns, n, 1, 1 << n)
+
+
+def test_filter_pass_heavy_matrices(gpu, oracle):
+    """The packed walks filter on 16 columns.  Matrices whose last 16 columns
+    are all ones pass that filter for 2/3 of all pairs while real events stay
+    rare: the per-superblock verify list overflows and every superblock takes
+    the exact fallback without entering dense mode.  Ranges and a batch must
+    stay exact (narrow n = 24, 30; wide n = 40)."""
+    r = random.Random(4242)
+    for n in (24, 30, 40):
+        a = _rand_matrix(r, n)
+        a[:, n - 16:] = 1
+        mags, sgns = oracle.planes_from_classes(a)
+        m = gpu.MatrixF3(centred(a))
+        for lo, span in ((1 << 22, 1 << 22), (3 << 21, (1 << 22) + 977), (12345, 1 << 21)):
+            assert gpu.perm_chunk(m, lo, lo + span).partial_sum == oracle.chunk_sum(mags, sgns, n, lo, lo + span), n
+    e = np.stack([_rand_matrix(r, 22) for _ in range(64)])
+    e[:, :, 6:] = 1
+    _, part, _ = gpu.perm_mod3_batch(e)
+    for b in (0, 17, 63):
+        mags, sgns = oracle.planes_from_classes(e[b])
+        assert part[b] == oracle.chunk_sum(mags, sgns, 22, 1, 1 << 22)
