@@ -237,6 +237,9 @@ def main():
     # single rank (exercises the collective on a 1-GPU box)
     use_dist = world > 1 or os.environ.get("TRITPERM_BENCH_DIST") == "1"
     if use_dist:
+        if "RANK" not in os.environ:  # single process outside torchrun
+            os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
+                              MASTER_PORT=os.environ.get("MASTER_PORT", "29533"))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     wl = args.workload
