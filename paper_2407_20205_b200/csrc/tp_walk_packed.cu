@@ -14,14 +14,18 @@
 //
 // i.e. 1.5 LOP3 per pair instead of 2, and 2.5 instructions per pair.  A
 // pass (probability (2/3)^16 per pair on uniform inputs) is verified exactly
-// on all 32 columns at the end of each verify batch (one superblock for
-// V = 4, two for V = 3): the lanes park their pass masks in shared memory,
-// an exclusive warp scan turns every nonzero mask into one list entry, and
-// lane e walks the pass bits of entry e against the full A words and the
-// group's B states (both in shared memory).  Terms are evaluated only there,
-// so the counts are exact.  Event-dense matrices switch to an exact mode as
-// in the pair walk.  V = 4 (512 pairs per lane and superblock) is the
-// default for 22 <= n <= 32: 7-16 % above the unpacked pair walk.
+// on all 32 columns after each superblock: one ballot per pair of pass masks
+// compacts the nonzero ones into a per-warp list, and lane e walks the pass
+// bits of entry e against the full A words and the group's B states (both in
+// shared memory).  Terms are evaluated only there, so the counts are exact.
+// Event-dense matrices switch to an exact mode as in the pair walk; the cold
+// paths (dense fold, n > 32 primary hits) are out of line so that they do not
+// take registers from the filter loop.  V = 4 (512 pairs per lane and
+// superblock) is the default for n >= 16 when the job fills the GPU.
+//
+// WIDE (n > 32): the filter and the verify cover the 32 primary columns; a
+// verified primary hit (probability (2/3)^32) is evaluated over all n columns
+// from scratch, as in the wide pair walk.
 #include "tp_walk_common.cuh"
 
 namespace tp {
@@ -41,9 +45,6 @@ __device__ __forceinline__ void packed_test(uint32_t z1, uint32_t g1, uint32_t z
       : "r"(z1), "r"(g1), "r"(z2), "r"(u2), "r"(one), "r"(cneg), "n"(BIT));
 }
 
-// WIDE (n > 32): the filter and the verify cover the 32 primary columns; a
-// verified primary hit (probability (2/3)^32) is evaluated over all n columns
-// from scratch, as in the wide pair walk.
 // Exact fold of the B states Hb[0..SB) against the lane's 32 slots (full A
 // words in shared memory): the dense mode.  Not inlined, so that its
 // registers do not constrain the filter loop's allocation.
