@@ -138,7 +138,7 @@ def test_montecarlo_matches_reference_tallies(gpu):
 
 
 def test_montecarlo_hist_matches_oracle_classes(gpu, oracle):
-    for n, trials, seed in ((3, 500, 2), (7, 300, 8), (13, 200, 1), (21, 64, 4)):
+    for n, trials, seed in ((3, 500, 2), (7, 300, 8), (13, 200, 1), (16, 400, 3), (18, 200, 5), (21, 64, 4)):
         h = gpu.montecarlo_hist(n, trials, seed)
         cls, _ = oracle.perm_batch(oracle.sample_batch(n, seed, 0, trials), threads=8)
         assert [h.zeros, h.plus_ones, h.minus_ones] == np.bincount(cls, minlength=3).tolist()
