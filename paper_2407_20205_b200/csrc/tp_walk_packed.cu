@@ -91,6 +91,12 @@ static __device__ __noinline__ uint32_t wide_hit_term(const RowRec* R, int n, un
   return 1u | ((uint32_t)(__popc(gg[0]) + __popc(gg[1])) << 2);
 }
 
+__device__ __forceinline__ uint32_t lanemask_lt() {  // %lanemask_lt: read where needed, holds no register
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
 template <int V, int WARPS, int MINB, bool WIDE>
 __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) {
   constexpr int KB = 5;
@@ -119,7 +125,6 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) 
   const uint32_t cneg = 0xfffeffffu * one;  // -0x00010001, runtime so ptxas keeps the IMAD
   const uint32_t colmask = p.z0_init;
   const uint32_t zero = one - 1u;  // runtime 0: keeps the first record of a mask an IMAD
-  const uint32_t lanemask_lt = (1u << lane) - 1u;
   const unsigned long long t_start = p.trace ? clock64() : 0;
   unsigned long long n_items = 0;
 
@@ -299,7 +304,7 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) 
 #pragma unroll
           for (int q = 0; q < MP; ++q) {
             if (Mc[2 * q] | Mc[2 * q + 1])
-              Lst[base + __popc(bq[q] & lanemask_lt)] = make_uint4((lane << 4) | (uint32_t)q, Mc[2 * q], Mc[2 * q + 1], 0u);
+              Lst[base + __popc(bq[q] & lanemask_lt())] = make_uint4((lane << 4) | (uint32_t)q, Mc[2 * q], Mc[2 * q + 1], 0u);
             base += __popc(bq[q]);
           }
           __syncwarp();
