@@ -83,24 +83,29 @@ __device__ __forceinline__ void store_row(RowRec* dst, unsigned long long mag, u
   *dst = r;
 }
 
+// One warp per matrix, one lane per row (rows lane and lane + 32): each lane
+// reads its row's n bytes (independent loads, so a single matrix -- C1 -- is
+// packed in one load latency rather than 64 dependent ones) and writes its
+// RowRec; rows >= n are zero.
 __global__ void k_pack(const uint8_t* __restrict__ entries, long long B, int n, RowRec* __restrict__ rows) {
   const uint32_t lane = threadIdx.x & 31u;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
   for (long long b = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); b < B; b += warps) {
     const uint8_t* E = entries + b * (long long)n * n;
-    for (int t = 0; t < 64; ++t) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int t = (int)lane + 32 * h;
       unsigned long long mag = 0, sgn = 0;
       if (t < n) {
-        uint32_t v0 = lane < (uint32_t)n ? (uint32_t)E[t * n + lane] % 3u : 0u;
-        uint32_t v1 = lane + 32 < (uint32_t)n ? (uint32_t)E[t * n + lane + 32] % 3u : 0u;
-        const unsigned long long m = (unsigned long long)__ballot_sync(FULL, v0 != 0) |
-                                     ((unsigned long long)__ballot_sync(FULL, v1 != 0) << 32);
-        const unsigned long long s = (unsigned long long)__ballot_sync(FULL, v0 == 2) |
-                                     ((unsigned long long)__ballot_sync(FULL, v1 == 2) << 32);
-        mag = __brevll(m) >> (64 - n);
-        sgn = __brevll(s) >> (64 - n);
+        const uint8_t* row = E + (long long)t * n;
+        for (int k = 0; k < n; ++k) {
+          const uint32_t v = (uint32_t)__ldg(row + k) % 3u;
+          const unsigned long long bit = 1ull << (n - 1 - k);  // column k -> bit n-1-k (src/core_f3.py:14-16)
+          if (v) mag |= bit;
+          if (v == 2u) sgn |= bit;
+        }
       }
-      if (lane == 0) store_row(rows + b * 64 + t, mag, sgn);
+      store_row(rows + b * 64 + t, mag, sgn);
     }
   }
 }
