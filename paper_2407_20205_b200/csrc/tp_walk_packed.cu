@@ -97,6 +97,16 @@ __device__ __forceinline__ uint32_t lanemask_lt() {  // %lanemask_lt: read where
   return m;
 }
 
+// (z2, u2) of the primary word at B-side index a (low bits empty), from
+// scratch; out of line (dense superblocks of the wide walk).
+template <int KB>
+static __device__ __noinline__ uint2 wide_b_entry(const RowRec* R, int n, unsigned long long a, uint32_t z0i,
+                                                  uint32_t z1i) {
+  uint32_t zz[2], gg[2];
+  wide_subset_state<KB>(R, n, a, 0u, z0i, z1i, zz, gg);
+  return make_uint2(zz[0], pair_u2(zz[0], gg[0]));
+}
+
 template <int V, int WARPS, int MINB, bool WIDE>
 __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) {
   constexpr int KB = 5;
@@ -199,6 +209,21 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_walk_packed(FastParams p) 
     uint32_t hoff = 0;    // superblocks since those states were computed
     for (uint32_t kb = 0; kb < p.nblk; ++kb) {
       const unsigned long long B = B0 + kb;
+      if (WIDE && dense) {
+        // exact replay of the superblock; the next superblock's entry state
+        // from scratch (both out of line: keeps the hot code small)
+        const unsigned long long r = replay_wide<KB>(R, p.n, B << V, SB, lane, p.z0_init, p.z1_init);
+        ev += (uint32_t)r;
+        odd += (uint32_t)(r >> 32);
+        dense = __any_sync(FULL, (uint32_t)r >= (uint32_t)K / 2);
+        have = false;
+        if (kb + 1 < p.nblk) {
+          const uint2 st = wide_b_entry<KB>(R, p.n, (B + 1) << V, p.z0_init, p.z1_init);
+          z2 = st.x;
+          u2 = st.y;
+        }
+        continue;
+      }
       if (dense) {
         const uint32_t SX = (kb & 1u) ? SS[V - 1] : SA[V - 1];
         const uint32_t CX = (kb & 1u) ? SA[V - 1] : SS[V - 1];
