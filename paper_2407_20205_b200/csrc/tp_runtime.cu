@@ -237,7 +237,9 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
       const unsigned long long f0 = (A0u + Lc - 1) / Lc * Lc, f1 = A1u / Lc * Lc;
       return f1 > f0 ? (f1 - f0) / Lc : 0ull;
     };
-    L = 2 * SBu;
+    // items of >= 2 superblocks keep B0 even for the pair/packed walks; the
+    // lane walk takes single-superblock items (short jobs: more parallelism)
+    L = (tp::fast_is_lane(pl.variant) ? 1 : 2) * SBu;
     if (aligned_chunks(L) == 0) L = 0;
     while (L && 2 * L <= Lmax && aligned_chunks(2 * L) * B >= want_items) L <<= 1;
     if (L) {

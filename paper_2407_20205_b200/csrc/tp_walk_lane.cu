@@ -49,8 +49,9 @@ __global__ void __launch_bounds__(32 * WARPS) k_walk_lane(FastParams p) {
     bool dense = false;  // warp-uniform: exact accumulation mode for event-dense inputs
     for (uint32_t kb = 0; kb < p.nblk; ++kb) {
       const uint32_t ze = z[0], ge = g[0];
-      // row 5+V-1 flips at j = 2^(V-1); it leaves iff bit 0 of B0+kb (= of kb) is set
-      const uint32_t SX = (kb & 1u) ? SS[V - 1] : SA[V - 1];
+      // row 5+V-1 flips at j = 2^(V-1); it leaves iff bit 0 of B0+kb is set
+      // (B0 may be odd: lane-walk items can be a single superblock)
+      const uint32_t SX = (((uint32_t)B0 + kb) & 1u) ? SS[V - 1] : SA[V - 1];
       if (!dense) {
 #pragma unroll
         for (int j = 1; j < (1 << V); ++j) {
