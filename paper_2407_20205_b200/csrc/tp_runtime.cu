@@ -55,6 +55,11 @@ struct Device {
   static constexpr int kQueues = 64;
   unsigned long long* queues = nullptr;
   int next_queue = 0;
+  // Pinned staging for the synchronous single-range call (tp_range_sum): the
+  // row table and zeroed counters go up in one async copy, the counters come
+  // back in one (guarded by mu).
+  static constexpr size_t kStageBytes = 64 * sizeof(RowRec) + 2 * sizeof(unsigned long long);
+  void* stage = nullptr;
   std::mutex mu;
 };
 
@@ -94,6 +99,7 @@ int ensure_device(int dev, Device** out) {
     TP_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
     TP_CUDA(cudaMalloc(&d.queues, 2 * Device::kQueues * sizeof(unsigned long long)));
     TP_CUDA(cudaMemset(d.queues, 0, 2 * Device::kQueues * sizeof(unsigned long long)));
+    TP_CUDA(cudaMallocHost(&d.stage, Device::kStageBytes));
     d.ready = true;
   }
   *out = &d;
@@ -418,23 +424,22 @@ int tp_range_sum(const uint64_t* mags, const uint64_t* sgns, int n, uint64_t lo,
   if ((rc = ensure_device(device, &d))) return rc;
   std::lock_guard<std::mutex> lk(d->mu);
   TP_CUDA(cudaSetDevice(device));
-  Carve cv;
-  cv.take<RowRec>(nullptr, 64);
-  cv.take<unsigned long long>(nullptr, 1);
-  cv.take<unsigned long long>(nullptr, 2);
-  if ((rc = ensure_ws(*d, cv.off))) return rc;
-  char* base = static_cast<char*>(d->ws);
-  Carve c2;
-  c2.take<RowRec>(base, 64);
-  c2.take<unsigned long long>(base, 1);
-  unsigned long long* pm = c2.take<unsigned long long>(base, 2);
-  TP_CUDA(cudaMemsetAsync(pm, 0, 2 * sizeof(unsigned long long), d->stream));
-  if ((rc = enqueue_range(*d, mags, sgns, n, lo, hi, pm, d->stream))) return rc;
-  unsigned long long h[2];
-  TP_CUDA(cudaMemcpyAsync(h, pm, sizeof h, cudaMemcpyDeviceToHost, d->stream));
+  // device layout = staging layout: 64 RowRec, then the (plus, minus) counters
+  if ((rc = ensure_ws(*d, Device::kStageBytes))) return rc;
+  RowRec* hrows = static_cast<RowRec*>(d->stage);
+  unsigned long long* hpm = reinterpret_cast<unsigned long long*>(hrows + 64);
+  planes_to_rows(mags, sgns, n, hrows);
+  hpm[0] = hpm[1] = 0;
+  RowRec* rows = static_cast<RowRec*>(d->ws);
+  unsigned long long* pm = reinterpret_cast<unsigned long long*>(rows + 64);
+  TP_CUDA(cudaMemcpyAsync(rows, hrows, Device::kStageBytes, cudaMemcpyHostToDevice, d->stream));
+  Plan pl;
+  make_plan(*d, n, 1, lo, hi, false, rows, pm, pl);
+  if ((rc = run_plan(pl, d->stream, nullptr))) return rc;
+  TP_CUDA(cudaMemcpyAsync(hpm, pm, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, d->stream));
   TP_CUDA(cudaStreamSynchronize(d->stream));
-  *plus = h[0];
-  *minus = h[1];
+  *plus = hpm[0];
+  *minus = hpm[1];
   return TP_OK;
 }
 
