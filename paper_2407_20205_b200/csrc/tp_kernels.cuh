@@ -79,6 +79,21 @@ struct GenericParams {
   uint32_t z0_init, z1_init;
 };
 
+// Tensor-core pair test (tp_walk_tc.cu): full traversals and chunk-aligned
+// ranges, n >= 18.  Item i = (matrix i / chunks, chunk c0 + i % chunks); a
+// chunk is 2^(15+t) subsets = 2^t tiles of 256 A vectors x 128 B vectors.
+struct TcParams {
+  const RowRec* rows;           // [B][64]
+  unsigned long long* pm;       // [B][2] (plus, minus) accumulators
+  unsigned long long* err;      // count of tensor hits the exact check rejected (must stay 0)
+  unsigned long long items, chunks, c0;
+  int n, t;                     // tiles per item = 2^t
+  int R, ks;                    // K layout (tc_layout)
+};
+void tc_layout(int n, int* R, int* ks);
+size_t tc_smem_bytes(int n, int ks);
+cudaError_t launch_walk_tc(int grid, const TcParams& p, cudaStream_t st);
+
 const void* walk_fast_symbol(int variant);
 const void* walk_generic_symbol(int nw);
 cudaError_t launch_walk_fast(int variant, int grid, const FastParams& p, cudaStream_t st);

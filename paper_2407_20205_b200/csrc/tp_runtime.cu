@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "../../include/tritperm.h"
@@ -55,6 +56,7 @@ struct Device {
   static constexpr int kQueues = 64;
   unsigned long long* queues = nullptr;
   int next_queue = 0;
+  unsigned long long* tc_err = nullptr;  // tensor-path self-check counter (must stay 0)
   // Pinned staging for the synchronous single-range call (tp_range_sum): the
   // row table and zeroed counters go up in one async copy, the counters come
   // back in one (guarded by mu).
@@ -99,6 +101,8 @@ int ensure_device(int dev, Device** out) {
     TP_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
     TP_CUDA(cudaMalloc(&d.queues, 2 * Device::kQueues * sizeof(unsigned long long)));
     TP_CUDA(cudaMemset(d.queues, 0, 2 * Device::kQueues * sizeof(unsigned long long)));
+    TP_CUDA(cudaMalloc(&d.tc_err, sizeof(unsigned long long)));
+    TP_CUDA(cudaMemset(d.tc_err, 0, sizeof(unsigned long long)));
     TP_CUDA(cudaMallocHost(&d.stage, Device::kStageBytes));
     d.ready = true;
   }
@@ -151,7 +155,19 @@ struct Plan {
   tp::FastParams fp{};
   tp::GenericParams gp{};
   int fast_grid = 0, generic_grid = 0;
+  bool tc = false;  // tensor-core pair test covers the whole plan
+  tp::TcParams tcp{};
+  int tc_grid = 0;
 };
+
+// Tensor-core pair test (tp_walk_tc.cu) for full traversals, opt-in with
+// TRITPERM_TC=1: exact, but slower than the packed LOP3 walk on B200 (its
+// 128 x 128 x 64 sub-tiles turn TMEM over faster than the MMA/epilogue
+// handshake allows).
+int tc_mode() {
+  const char* e = getenv("TRITPERM_TC");  // read per call: tests switch it at run time
+  return e ? atoi(e) : 0;
+}
 
 // Superblock size per n: longer superblocks amortise the per-block work, but
 // raise the chance that one lane sees two events of the same step parity in a
@@ -198,6 +214,26 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
                const RowRec* rows, unsigned long long* pm, Plan& pl) {
   pl = Plan();
   pl.nw = n <= 32 ? 1 : 2;
+  // Full traversals of n >= 18 (at least 8 tiles per matrix) go to the tensor
+  // cores.  Tiles per item 2^t: as long as the grid still gets >= 8 items per CTA.
+  if (full && n >= 18 && B > 0 && tc_mode() != 0) {
+    const int tmax = n - 15;
+    const unsigned long long want = 8ull * (unsigned long long)d.sm_count;
+    int t = tmax;
+    while (t > 3 && (B << (tmax - t)) < want) --t;
+    pl.tc = true;
+    pl.tcp.rows = rows;
+    pl.tcp.pm = pm;
+    pl.tcp.err = d.tc_err;
+    pl.tcp.n = n;
+    pl.tcp.t = t;
+    pl.tcp.chunks = 1ull << (tmax - t);
+    pl.tcp.items = B * pl.tcp.chunks;
+    pl.tcp.c0 = 0;
+    tp::tc_layout(n, &pl.tcp.R, &pl.tcp.ks);
+    pl.tc_grid = (int)std::min<unsigned long long>(pl.tcp.items, (unsigned long long)d.sm_count);
+    return;
+  }
   pl.variant = choose_variant(n, B);
   const int V = tp::fast_v(pl.variant);
   const int U = tp::fast_kb(pl.variant);  // log2(fast unit / 32 reference steps)
@@ -308,6 +344,11 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
 // Enqueue the walk of plan `pl`; returns launches in *launches.
 int run_plan(const Plan& pl, cudaStream_t st, int* launches) {
   int nl = 0;
+  if (pl.tc) {
+    TP_CUDA(tp::launch_walk_tc(pl.tc_grid, pl.tcp, st));
+    if (launches) *launches += 1;
+    return TP_OK;
+  }
   if (pl.fast) {
     TP_CUDA(tp::launch_walk_fast(pl.variant, pl.fast_grid, pl.fp, st));
     nl++;
@@ -752,8 +793,14 @@ int tp_perm_batch(const uint8_t* entries, int64_t B, int n, int device, int8_t* 
   if (out_class) TP_CUDA(cudaMemcpyAsync(out_class, dcls, (size_t)B, cudaMemcpyDeviceToHost, st));
   if (out_partial) TP_CUDA(cudaMemcpyAsync(out_partial, dpart, (size_t)B * 8, cudaMemcpyDeviceToHost, st));
   long long hh[3];
+  unsigned long long tcerr = 0;
   TP_CUDA(cudaMemcpyAsync(hh, dhist, sizeof hh, cudaMemcpyDeviceToHost, st));
+  TP_CUDA(cudaMemcpyAsync(&tcerr, d->tc_err, sizeof tcerr, cudaMemcpyDeviceToHost, st));
   TP_CUDA(cudaStreamSynchronize(st));
+  if (tcerr) {
+    TP_CUDA(cudaMemset(d->tc_err, 0, sizeof(unsigned long long)));
+    return fail(TP_E_CUDA, "tensor path self-check failed on %llu terms", tcerr);
+  }
   if (hist) {
     hist[0] = hh[0];
     hist[1] = hh[1];
@@ -808,8 +855,14 @@ static int mc_run(int n, int64_t t0, int64_t count, uint64_t seed, int device, i
     if (out_class) TP_CUDA(cudaStreamSynchronize(st));
   }
   long long hh[3];
+  unsigned long long tcerr = 0;
   TP_CUDA(cudaMemcpyAsync(hh, dhist, sizeof hh, cudaMemcpyDeviceToHost, st));
+  TP_CUDA(cudaMemcpyAsync(&tcerr, d->tc_err, sizeof tcerr, cudaMemcpyDeviceToHost, st));
   TP_CUDA(cudaStreamSynchronize(st));
+  if (tcerr) {
+    TP_CUDA(cudaMemset(d->tc_err, 0, sizeof(unsigned long long)));
+    return fail(TP_E_CUDA, "tensor path self-check failed on %llu terms", tcerr);
+  }
   if (hist) {
     hist[0] = hh[0];
     hist[1] = hh[1];

@@ -452,3 +452,35 @@ def test_filter_pass_heavy_matrices(gpu, oracle):
     for b in (0, 17, 63):
         mags, sgns = oracle.planes_from_classes(e[b])
         assert part[b] == oracle.chunk_sum(mags, sgns, 22, 1, 1 << 22)
+
+
+def test_tensor_core_pair_test_exact(gpu, oracle, monkeypatch):
+    """The opt-in tcgen05 path (TRITPERM_TC=1, tp_walk_tc.cu): full traversals
+    through the batch ABI, n = 18..36 (one and several k-steps, one and two
+    32-bit plane words), uniform, all-ones and sparse matrices; raw partials
+    equal the oracle's / the default path's bit for bit, and the path's own
+    exact re-check of every tensor hit never fires."""
+    from paper_2407_20205_b200 import fixtures
+
+    monkeypatch.setenv("TRITPERM_TC", "1")
+    r = random.Random(77)
+    for n, B in ((18, 40), (21, 9), (24, 64), (29, 3), (32, 2), (33, 1), (36, 1)):
+        e = fixtures.uniform_batch(n, 5, 0, B)
+        cls, part, hist = gpu.perm_mod3_batch(e)
+        monkeypatch.setenv("TRITPERM_TC", "0")
+        cls0, part0, hist0 = gpu.perm_mod3_batch(e)
+        monkeypatch.setenv("TRITPERM_TC", "1")
+        assert np.array_equal(part, part0) and np.array_equal(cls, cls0), n
+        assert hist.tolist() == hist0.tolist(), n
+        if n <= 24:
+            mags, sgns = oracle.planes_from_classes(e[0])
+            assert part[0] == oracle.chunk_sum(mags, sgns, n, 1, 1 << n), n
+    for n in (20, 24, 31):
+        cls, part, _ = gpu.perm_mod3_batch(np.ones((2, n, n), np.uint8))
+        assert part[0] == part[1] == _ones_partial(n), n
+    sparse = np.array([[[r.choice((0, 0, 0, 0, 1, 2)) for _ in range(22)] for _ in range(22)] for _ in range(8)],
+                      dtype=np.uint8)
+    _, part, _ = gpu.perm_mod3_batch(sparse)
+    for b in range(8):
+        mags, sgns = oracle.planes_from_classes(sparse[b])
+        assert part[b] == oracle.chunk_sum(mags, sgns, 22, 1, 1 << 22), b
