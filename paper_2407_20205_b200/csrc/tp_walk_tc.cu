@@ -581,12 +581,9 @@ void tc_layout(int n, int* R, int* ks) {
 template <int NW>
 static cudaError_t launch_tc_nw(int grid, const TcParams& p, cudaStream_t st) {
   const size_t smem = tc_smem_bytes(p.n, p.ks);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_walk_tc<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  // per launch: the attribute belongs to the current device's context
+  cudaError_t e = cudaFuncSetAttribute(k_walk_tc<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
   k_walk_tc<NW><<<grid, kTcThreads, smem, st>>>(p);
   return cudaGetLastError();
 }
