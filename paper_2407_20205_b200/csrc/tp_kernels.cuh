@@ -94,6 +94,20 @@ void tc_layout(int n, int* R, int* ks);
 size_t tc_smem_bytes(int n, int ks);
 cudaError_t launch_walk_tc(int grid, const TcParams& p, cudaStream_t st);
 
+// Bucketed pair walk (tp_walk_bucket.cu): full traversals, 20 <= n <= 31.
+// Items (matrix, piece, chunk); list/ptab come from launch_bucket_group.
+struct BucketParams {
+  FastParams fp;                // items = B * bucket_pieces() * chunks; L, nblk as in the fast walks
+  const uint16_t* list;         // [B][pieces][1024] A subsets (0xFFFF = dummy slot)
+  const uint32_t* ptab;         // [B][pieces] bucket | valid count << 16 (count 0 = unused)
+};
+int bucket_pieces();
+int bucket_fix();
+cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, uint16_t* list, uint32_t* ptab,
+                                cudaStream_t st);
+cudaError_t launch_walk_bucket(int grid, const BucketParams& bp, cudaStream_t st);
+const void* walk_bucket_symbol();
+
 const void* walk_fast_symbol(int variant);
 const void* walk_generic_symbol(int nw);
 cudaError_t launch_walk_fast(int variant, int grid, const FastParams& p, cudaStream_t st);

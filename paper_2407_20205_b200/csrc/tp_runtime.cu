@@ -57,6 +57,9 @@ struct Device {
   unsigned long long* queues = nullptr;
   int next_queue = 0;
   unsigned long long* tc_err = nullptr;  // tensor-path self-check counter (must stay 0)
+  void* bucket_ws = nullptr;  // bucket lists of the bucketed walk (grow-only)
+  size_t bucket_ws_size = 0;
+  int bucket_blocks_per_sm = 0;
   // Pinned staging for the synchronous single-range call (tp_range_sum): the
   // row table and zeroed counters go up in one async copy, the counters come
   // back in one (guarded by mu).
@@ -102,6 +105,8 @@ int ensure_device(int dev, Device** out) {
     TP_CUDA(cudaMalloc(&d.queues, 2 * Device::kQueues * sizeof(unsigned long long)));
     TP_CUDA(cudaMemset(d.queues, 0, 2 * Device::kQueues * sizeof(unsigned long long)));
     TP_CUDA(cudaMalloc(&d.tc_err, sizeof(unsigned long long)));
+    TP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.bucket_blocks_per_sm, tp::walk_bucket_symbol(), 128, 0));
+    if (d.bucket_blocks_per_sm < 1) return fail(TP_E_CUDA, "bucket walk cannot be resident on device %d", dev);
     TP_CUDA(cudaMemset(d.tc_err, 0, sizeof(unsigned long long)));
     TP_CUDA(cudaMallocHost(&d.stage, Device::kStageBytes));
     d.ready = true;
@@ -155,6 +160,12 @@ struct Plan {
   tp::FastParams fp{};
   tp::GenericParams gp{};
   int fast_grid = 0, generic_grid = 0;
+  bool bucket = false;  // bucketed pair walk covers the whole plan
+  tp::BucketParams bkp{};
+  int bucket_grid = 0;
+  long long bucket_B = 0;
+  uint16_t* bucket_list = nullptr;
+  uint32_t* bucket_ptab = nullptr;
   bool tc = false;  // tensor-core pair test covers the whole plan
   tp::TcParams tcp{};
   int tc_grid = 0;
@@ -164,6 +175,13 @@ struct Plan {
 // TRITPERM_TC=1: exact, but slower than the packed LOP3 walk on B200 (its
 // 128 x 128 x 64 sub-tiles turn TMEM over faster than the MMA/epilogue
 // handshake allows).
+// Bucketed pair walk (tp_walk_bucket.cu) for full traversals of 20 <= n <= 31:
+// TRITPERM_BUCKET=0 turns it off, =1 forces it wherever it applies.
+int bucket_mode() {
+  const char* e = getenv("TRITPERM_BUCKET");  // read per call: tests switch it at run time
+  return e ? atoi(e) : 0;
+}
+
 int tc_mode() {
   const char* e = getenv("TRITPERM_TC");  // read per call: tests switch it at run time
   return e ? atoi(e) : 0;
@@ -214,6 +232,52 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
                const RowRec* rows, unsigned long long* pm, Plan& pl) {
   pl = Plan();
   pl.nw = n <= 32 ? 1 : 2;
+  // Bucketed pair walk: items (matrix, piece, chunk) of L = 2^(n-14) / chunks
+  // B steps (superblocks of 16, at least 2 per item).
+  if (full && n >= 20 && n <= 31 && B > 0 && bucket_mode() > 0) {
+    const int P = tp::bucket_pieces();
+    const unsigned long long bsteps = 1ull << (n - tp::bucket_fix());
+    const unsigned long long want = 4ull * d.sm_count * d.bucket_blocks_per_sm * 4;
+    unsigned long long chunks = 1;
+    while (bsteps / (2 * chunks) >= 32 && B * (unsigned long long)P * chunks < want) chunks *= 2;
+    const size_t need = (size_t)B * P * (1024 * sizeof(uint16_t) + sizeof(uint32_t));
+    if (d.bucket_ws_size < need) {
+      cudaDeviceSynchronize();  // earlier launches may still read the old lists
+      if (d.bucket_ws) cudaFree(d.bucket_ws);
+      d.bucket_ws = nullptr;
+      d.bucket_ws_size = 0;
+      if (cudaMalloc(&d.bucket_ws, need) == cudaSuccess) d.bucket_ws_size = need;
+    }
+    if (d.bucket_ws_size >= need) {
+      pl.bucket = true;
+      pl.bucket_B = (long long)B;
+      pl.bucket_list = static_cast<uint16_t*>(d.bucket_ws);
+      pl.bucket_ptab = reinterpret_cast<uint32_t*>(pl.bucket_list + (size_t)B * P * 1024);
+      tp::FastParams& f = pl.bkp.fp;
+      f.rows = rows;
+      f.pm = pm;
+      f.queue = take_queue(d);
+      f.F0 = 0;
+      f.L = bsteps / chunks;
+      f.chunks = chunks;
+      f.items = B * (unsigned long long)P * chunks;
+      f.nblk = (uint32_t)(f.L >> 4);  // superblocks of 16 B steps
+      f.lognblk = 0;
+      while ((1u << f.lognblk) < f.nblk) f.lognblk++;
+      f.n = n;
+      f.z0_init = zmask(n);
+      f.z1_init = 0;
+      f.one = 1u;
+      f.trace = nullptr;
+      f.dense_ok = 1;
+      f.static_items = 0;
+      pl.bkp.list = pl.bucket_list;
+      pl.bkp.ptab = pl.bucket_ptab;
+      const unsigned long long ctas = (unsigned long long)d.sm_count * d.bucket_blocks_per_sm;
+      pl.bucket_grid = (int)std::max<unsigned long long>(1, std::min(ctas, (f.items + 3) / 4));
+      return;
+    }
+  }
   // Full traversals of n >= 18 (at least 8 tiles per matrix) go to the tensor
   // cores.  Tiles per item 2^t: as long as the grid still gets >= 8 items per CTA.
   if (full && n >= 18 && B > 0 && tc_mode() != 0) {
@@ -344,6 +408,12 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
 // Enqueue the walk of plan `pl`; returns launches in *launches.
 int run_plan(const Plan& pl, cudaStream_t st, int* launches) {
   int nl = 0;
+  if (pl.bucket) {
+    TP_CUDA(tp::launch_bucket_group(pl.bkp.fp.rows, pl.bucket_B, pl.bkp.fp.n, pl.bucket_list, pl.bucket_ptab, st));
+    TP_CUDA(tp::launch_walk_bucket(pl.bucket_grid, pl.bkp, st));
+    if (launches) *launches += 2;
+    return TP_OK;
+  }
   if (pl.tc) {
     TP_CUDA(tp::launch_walk_tc(pl.tc_grid, pl.tcp, st));
     if (launches) *launches += 1;

@@ -1,0 +1,331 @@
+// tp_walk_bucket.cu -- the pair walk with the A side bucketed by two key
+// columns (n <= 31, full traversals).
+//
+// The pair walk (tp_walk_pair.cu) tests every (A vector, B state) pair.  A pair
+// whose sum has a zero in ANY column is a zero term, so pairs can be skipped
+// wholesale by looking at a few "key" columns first:
+//
+//   * the A side is rows 0..13 (16384 A vectors per matrix).  k_bucket_group
+//     sorts them by their trits (x1, x2) on the key columns k1 = n-1,
+//     k2 = n-2 into 9 buckets and cuts each bucket into pieces of 1024
+//     (= 32 lanes x 32 slots, the pair walk's A side per warp; the last piece
+//     of a bucket is padded with dummy slots);
+//   * a warp takes one piece, so all its A vectors share (x1, x2), and walks
+//     the B side (rows 14..n-1) in Gray order as usual;
+//   * a B state y is compatible with the piece iff y1 != -x1 and y2 != -x2;
+//     otherwise every one of the warp's 1024 pairs with it has a zero key
+//     column.  Compatibility is warp-uniform, so the 32 pair tests of an
+//     incompatible step are skipped by a uniform branch.
+//
+// On uniform inputs 4/9 of the steps are compatible, so the pair tests drop
+// to 44 % (plus ~11 % of dummy slots), and the sum is unchanged: only zero
+// terms are skipped, so raw partials equal chunk_sum (src/_kernels.py:90-128)
+// bit for bit.  Dummy slots carry a -1 in padding column 31 (the B side has
+// +1 there), so their sums always have a zero column and never count.
+#include "tp_walk_common.cuh"
+
+namespace tp {
+
+namespace {
+
+constexpr int kBucketFix = 14;                    // A side: rows 0..13
+constexpr int kBucketPieces = (1 << (kBucketFix - 10)) + 9;  // 16 full pieces + one partial per bucket
+constexpr uint16_t kBucketDummy = 0xFFFFu;
+
+// ----------------------------------------------------------------- grouping
+// One CTA per matrix: key trits of all 2^14 A subsets from two 128-entry
+// half tables, a counting sort into the 9 buckets, pieces of 1024.
+__global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n, uint16_t* list, uint32_t* ptab) {
+  __shared__ uint8_t tlo[128], thi[128];  // key pattern 3 * x1 + x2 of the low / high 7 rows' subsets
+  __shared__ uint32_t cnt[9], pos[9];
+  __shared__ uint32_t pstart[9];
+  const RowRec* R = rows + (size_t)blockIdx.x * 64;
+  uint16_t* L = list + (size_t)blockIdx.x * kBucketPieces * 1024;
+  uint32_t* P = ptab + (size_t)blockIdx.x * kBucketPieces;
+  const int k1 = n - 1, k2 = n - 2;
+  auto trit = [&](int r, int k) -> uint32_t {
+    const uint32_t m = (R[r].m[0] >> k) & 1u, s = (R[r].s[0] >> k) & 1u;
+    return m ? (s ? 2u : 1u) : 0u;
+  };
+  if (threadIdx.x < 256) {
+    const uint32_t half = threadIdx.x >> 7, sub = threadIdx.x & 127u;
+    uint32_t x1 = 0, x2 = 0;
+    for (int b = 0; b < 7; ++b)
+      if ((sub >> b) & 1u) {
+        x1 += trit(7 * half + b, k1);
+        x2 += trit(7 * half + b, k2);
+      }
+    const uint8_t v = (uint8_t)(3 * (x1 % 3) + (x2 % 3));
+    if (half) thi[sub] = v;
+    else tlo[sub] = v;
+  }
+  if (threadIdx.x < 9) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  auto pat = [&](uint32_t s) -> uint32_t {
+    const uint32_t a = tlo[s & 127u], b = thi[s >> 7];
+    const uint32_t x1 = (a / 3 + b / 3) % 3, x2 = (a % 3 + b % 3) % 3;
+    return 3 * x1 + x2;
+  };
+  for (uint32_t s = threadIdx.x; s < (1u << kBucketFix); s += blockDim.x) atomicAdd(&cnt[pat(s)], 1u);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t piece = 0;
+    for (int g = 0; g < 9; ++g) {
+      pstart[g] = piece;
+      pos[g] = piece * 1024u;
+      const uint32_t np = (cnt[g] + 1023u) / 1024u;
+      for (uint32_t q = 0; q < np; ++q) {
+        const uint32_t c = min(1024u, cnt[g] - 1024u * q);
+        P[piece + q] = (uint32_t)g | (c << 16);
+      }
+      piece += np;
+    }
+    for (uint32_t q = piece; q < (uint32_t)kBucketPieces; ++q) P[q] = 0;  // unused pieces: count 0
+  }
+  __syncthreads();
+  // padding first (the scatter below overwrites the valid prefix of each piece)
+  for (uint32_t i = threadIdx.x; i < (uint32_t)kBucketPieces * 1024u; i += blockDim.x) L[i] = kBucketDummy;
+  __syncthreads();
+  for (uint32_t s = threadIdx.x; s < (1u << kBucketFix); s += blockDim.x) {
+    const uint32_t g = pat(s);
+    L[atomicAdd(&pos[g], 1u)] = (uint16_t)s;
+  }
+}
+
+}  // namespace
+
+template <int V, int WARPS>
+__global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) {
+  constexpr int KB = 5;
+  constexpr int K = 1 << KB;
+  constexpr int FIX = kBucketFix;
+  constexpr int SB = 1 << V;
+  const FastParams& p = bp.fp;
+  __shared__ RowRec Rs[WARPS][32];
+  __shared__ uint4 Hs[WARPS][SB];
+  __shared__ uint2 As[WARPS][K][32];
+  const uint32_t lane = threadIdx.x & 31u;
+  RowRec* R = Rs[threadIdx.x >> 5];
+  uint4* H = Hs[threadIdx.x >> 5];
+  uint2 (*A)[32] = As[threadIdx.x >> 5];
+  const uint32_t one = p.one;
+  const uint32_t colmask = p.z0_init;  // real columns (n <= 31: bit 31 is padding)
+  const int k1 = p.n - 1, k2 = p.n - 2;
+  unsigned long long n_items = 0;
+
+  for (;;) {
+    const unsigned long long item = next_item(p, lane, n_items, blockIdx.x * WARPS + (threadIdx.x >> 5));
+    if (item >= p.items) break;
+    ++n_items;
+    const unsigned long long per_b = (unsigned long long)kBucketPieces * p.chunks;
+    const unsigned long long b = item / per_b;
+    const unsigned long long rem = item - b * per_b;
+    const uint32_t q = (uint32_t)(rem / p.chunks);
+    const unsigned long long A0 = (rem - (unsigned long long)q * p.chunks) * p.L;
+    const uint32_t pt = bp.ptab[b * kBucketPieces + q];
+    if ((pt >> 16) == 0) continue;  // unused piece
+    const uint32_t grp = pt & 0xFFFFu;
+    const unsigned long long B0 = A0 >> V;
+    __syncwarp();
+    load_rows(R, p.rows + b * 64, lane, p.n);
+    __syncwarp();
+
+    // A side: slot k of this lane is the A subset list[piece][32 k + lane]
+    uint32_t z1[K], g1[K];
+    uint32_t spm = 0;  // bit k: parity of slot k's subset
+    {
+      const uint16_t* Lp = bp.list + (b * kBucketPieces + q) * 1024;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const uint32_t s = Lp[32 * k + lane];
+        uint32_t z = colmask, g = 0;
+        if (s == kBucketDummy) {
+          g = 0x80000000u;  // -1 in padding column 31 (B side: +1): never a full sum
+        } else {
+#pragma unroll 1
+          for (uint32_t x = s; x; x &= x - 1) {
+            const int t = __ffs(x) - 1;
+            sub_word(z, g, R[t].m[0], R[t].a[0]);
+          }
+          spm |= (uint32_t)(__popc(s) & 1) << k;
+        }
+        z1[k] = z;
+        g1[k] = g;
+        A[k][lane] = make_uint2(z, g);
+      }
+    }
+    // forbidden key trits of this piece: f = -x (mod 3)
+    const uint32_t x1 = grp / 3, x2 = grp % 3;
+    const uint32_t f1 = (3 - x1) % 3, f2 = (3 - x2) % 3;
+    const uint32_t F0 = (f1 == 0 ? 1u << k1 : 0u) | (f2 == 0 ? 1u << k2 : 0u);
+    const uint32_t F1 = (f1 == 1 ? 1u << k1 : 0u) | (f2 == 1 ? 1u << k2 : 0u);
+    const uint32_t F2 = (f1 == 2 ? 1u << k1 : 0u) | (f2 == 2 ? 1u << k2 : 0u);
+    // B side: v2 for S2 = gray(A0) on rows >= FIX (low bits empty)
+    uint32_t z2, u2;
+    {
+      uint32_t z = colmask, g = 0;
+      const unsigned long long hs = A0 ^ (A0 >> 1);
+      for (int r = FIX; r < p.n; ++r)
+        if ((hs >> (r - FIX)) & 1ull) sub_word(z, g, R[r].m[0], R[r].a[0]);
+      z2 = z;
+      u2 = pair_u2(z, g);
+    }
+    uint32_t ev = 0, odd = 0;
+    // exact evaluation of every pair of the superblock from H (replays, dense mode)
+    auto exact_block = [&](uint32_t& bev, uint32_t& bodd) {
+      bev = bodd = 0;
+#pragma unroll 1
+      for (int j = 0; j < SB; ++j) {
+        const uint4 h = H[j];
+        const uint32_t gh = pair_g2(h.x, h.y);
+        uint32_t n0 = 0, a0 = 0, n1 = 0, a1 = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          if ((spm >> k) & 1u) exact_fold(z1[k], g1[k], h.x, h.y, gh, colmask, n1, a1, one);
+          else exact_fold(z1[k], g1[k], h.x, h.y, gh, colmask, n0, a0, one);
+        }
+        // term is odd iff popc(sgn) + j + parity(A subset) is odd
+        bev += n0 + n1;
+        bodd += (j & 1) ? (n0 - a0) + a1 : a0 + (n1 - a1);
+      }
+    };
+    bool dense = false;
+    for (uint32_t kb = 0; kb < p.nblk; ++kb) {
+      // the B states of the superblock, one per lane (step j = lane mod SB),
+      // as in the pair walk
+      uint32_t zj = z2, uj = u2;
+      {
+        const uint32_t j = lane & (SB - 1), gj = j ^ (j >> 1);
+#pragma unroll
+        for (int r = 0; r < V; ++r) {
+          if ((gj >> r) & 1u) {
+            const bool lv = (r == V - 1) && (kb & 1u);
+            const RowRec& row = R[FIX + r];
+            sub_word_u(zj, uj, row.m[0], lv ? row.s[0] : row.a[0], lv ? row.a[0] : row.s[0]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane < (uint32_t)SB) H[lane] = make_uint4(zj, uj, 0u, 0u);
+      // compatible steps: no key column of y equals the forbidden trit
+      // (y = 0 <=> z; y = 2 <=> ~z & ~u; y = 1 <=> ~z & u)
+      const uint32_t match = (zj & F0) | (~zj & ~uj & F2) | (~zj & uj & F1);
+      const uint32_t cmask = __ballot_sync(FULL, match == 0u) & (SB == 32 ? 0xffffffffu : ((1u << SB) - 1u));
+      if (dense) {
+        __syncwarp();
+        uint32_t bev, bodd;
+        exact_block(bev, bodd);
+        ev += bev;
+        odd += bodd;
+        dense = __any_sync(FULL, bev >= (uint32_t)K / 2);
+      } else {
+        // the compatible steps only: a rolled loop over the set bits of
+        // cmask, the next step's B state loaded (uniform shared-memory
+        // broadcast) before the current step's 32 tests
+        __syncwarp();
+        // hit records (slot of the last hit) << 16 | hit count, four of them
+        // (slots k mod 4) so that the predicated IMADs do not form one chain
+        uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+        // two compatible steps per iteration (independent tests interleave);
+        // the next two states are loaded before the current tests
+        uint32_t cm = cmask;
+        uint32_t ja = 0, jb = 0, hj = 0;
+        uint4 ha = make_uint4(0, 0, 0, 0), hb = ha;
+        auto pop2 = [&]() {
+          ja = __ffs(cm) - 1;
+          cm &= cm - 1;
+          jb = __ffs(cm) - 1;
+          cm &= cm - 1;
+        };
+        if (__popc(cm) >= 2) {
+          pop2();
+          ha = H[ja];
+          hb = H[jb];
+          for (;;) {
+            const uint4 ca = ha, cb = hb;
+            const uint32_t cja = ja, cjb = jb;
+            const bool more = __popc(cm) >= 2;
+            if (more) {
+              pop2();
+              ha = H[ja];
+              hb = H[jb];
+            }
+            const uint32_t sa = r0 + r1, sb = r2 + r3;
+            static_for<K>([&](auto kc) {
+              constexpr int k = decltype(kc)::value;
+              uint32_t& r = (k & 1) ? r1 : r0;
+              uint32_t& rr = (k & 1) ? r3 : r2;
+              pair_test<((uint32_t)k << 16) | 1u>(z1[k], g1[k], ca.x, ca.y, r, one);
+              pair_test<((uint32_t)k << 16) | 1u>(z1[k], g1[k], cb.x, cb.y, rr, one);
+            });
+            // step of this lane's latest hit (the single-hit path needs it)
+            if (r0 + r1 != sa) hj = cja;
+            if (r2 + r3 != sb) hj = cjb;
+            if (!more) break;
+          }
+        }
+        if (cm) {
+          const uint32_t jc = __ffs(cm) - 1;
+          const uint4 hc = H[jc];
+          const uint32_t sa = r0 + r1;
+          static_for<K>([&](auto kc) {
+            constexpr int k = decltype(kc)::value;
+            uint32_t& r = (k & 1) ? r1 : r0;
+            pair_test<((uint32_t)k << 16) | 1u>(z1[k], g1[k], hc.x, hc.y, r, one);
+          });
+          if (r0 + r1 != sa) hj = jc;
+        }
+        const uint32_t cnt = (r0 & 0xffffu) + (r1 & 0xffffu) + (r2 & 0xffffu) + (r3 & 0xffffu);
+        const uint32_t rec = (r0 & 0xffffu) ? r0 : (r1 & 0xffffu) ? r1 : (r2 & 0xffffu) ? r2 : r3;
+        if (__any_sync(FULL, cnt != 0)) {
+          uint32_t bev = 0, bodd = 0;
+          if (__any_sync(FULL, cnt > 1)) {
+            exact_block(bev, bodd);
+            dense = p.dense_ok != 0 && __any_sync(FULL, bev >= (uint32_t)K / 2);
+          } else if (cnt == 1) {
+            // one hit: slot k from the record, step hj tracked in the loop
+            const uint32_t k = rec >> 16;
+            const uint2 a1 = A[k][lane];
+            const uint4 hh = H[hj];
+            uint32_t d;
+            TP_LOP3(d, a1.x, a1.y, hh.y, 0x06);
+            bev = 1;
+            bodd = (__popc((d ^ pair_g2(hh.x, hh.y)) & colmask) + hj + ((spm >> k) & 1u)) & 1u;
+          }
+          ev += bev;
+          odd += bodd;
+        }
+      }
+      // (z2, u2) = step SB-1 of this superblock, then the entry step of kb + 1
+      z2 = __shfl_sync(FULL, zj, SB - 1);
+      u2 = __shfl_sync(FULL, uj, SB - 1);
+      if (kb + 1 < p.nblk) {
+        const uint32_t u = kb + 1;
+        const int t = __ffs(u) - 1;
+        const RowRec& row = R[FIX + V + t];
+        const bool lv = entry_leave(u, t, p, B0);
+        sub_word_u(z2, u2, row.m[0], lv ? row.s[0] : row.a[0], lv ? row.a[0] : row.s[0]);
+      }
+    }
+    warp_flush(p.pm + 2 * b, ev - odd, odd, lane);
+  }
+  queue_done(p, lane);
+}
+
+int bucket_pieces() { return kBucketPieces; }
+int bucket_fix() { return kBucketFix; }
+
+cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, uint16_t* list, uint32_t* ptab,
+                                cudaStream_t st) {
+  k_bucket_group<<<(unsigned)B, 256, 0, st>>>(rows, n, list, ptab);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_walk_bucket(int grid, const BucketParams& bp, cudaStream_t st) {
+  k_walk_bucket<4, 4><<<grid, 128, 0, st>>>(bp);
+  return cudaGetLastError();
+}
+
+const void* walk_bucket_symbol() { return reinterpret_cast<const void*>(&k_walk_bucket<4, 4>); }
+
+}  // namespace tp
