@@ -484,3 +484,28 @@ def test_tensor_core_pair_test_exact(gpu, oracle, monkeypatch):
     for b in range(8):
         mags, sgns = oracle.planes_from_classes(sparse[b])
         assert part[b] == oracle.chunk_sum(mags, sgns, 22, 1, 1 << 22), b
+
+
+def test_bucketed_pair_walk_exact(gpu, oracle, monkeypatch):
+    """The opt-in bucketed pair walk (TRITPERM_BUCKET=1, tp_walk_bucket.cu):
+    full traversals, 20 <= n <= 31, uniform, sparse and all-ones matrices; raw
+    partials equal the default path and the oracle bit for bit (only zero
+    terms are skipped)."""
+    from paper_2407_20205_b200 import fixtures
+
+    r = np.random.default_rng(31)
+    cases = [fixtures.uniform_batch(n, 13, 0, B) for n, B in ((20, 48), (21, 7), (24, 40), (27, 3), (31, 2))]
+    for n in (20, 26):
+        sp = ((r.random((5, n, n)) < 0.25) * r.integers(1, 3, (5, n, n))).astype(np.uint8)
+        cases.append(np.concatenate([sp, np.ones((2, n, n), np.uint8)]))
+    for e in cases:
+        n = e.shape[1]
+        monkeypatch.setenv("TRITPERM_BUCKET", "1")
+        cls, part, hist = gpu.perm_mod3_batch(e)
+        monkeypatch.setenv("TRITPERM_BUCKET", "0")
+        cls0, part0, hist0 = gpu.perm_mod3_batch(e)
+        assert np.array_equal(part, part0) and np.array_equal(cls, cls0), n
+        assert hist.tolist() == hist0.tolist(), n
+        if n <= 21:
+            mags, sgns = oracle.planes_from_classes(e[0])
+            assert part[0] == oracle.chunk_sum(mags, sgns, n, 1, 1 << n), n
