@@ -172,10 +172,12 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
     }
     uint32_t ev = 0, odd = 0;
     // exact evaluation of every pair of the superblock from H (replays, dense mode)
-    auto exact_block = [&](uint32_t& bev, uint32_t& bodd) {
+    // (only the steps in `mask`: incompatible steps have no full term)
+    auto exact_block = [&](uint32_t& bev, uint32_t& bodd, uint32_t mask) {
       bev = bodd = 0;
 #pragma unroll 1
-      for (int j = 0; j < SB; ++j) {
+      for (; mask; mask &= mask - 1) {
+        const int j = __ffs(mask) - 1;
         const uint4 h = H[j];
         const uint32_t gh = pair_g2(h.x, h.y);
         uint32_t n0 = 0, a0 = 0, n1 = 0, a1 = 0;
@@ -214,7 +216,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
       if (dense) {
         __syncwarp();
         uint32_t bev, bodd;
-        exact_block(bev, bodd);
+        exact_block(bev, bodd, cmask);
         ev += bev;
         odd += bodd;
         dense = __any_sync(FULL, bev >= (uint32_t)K / 2);
@@ -280,7 +282,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
         if (__any_sync(FULL, cnt != 0)) {
           uint32_t bev = 0, bodd = 0;
           if (__any_sync(FULL, cnt > 1)) {
-            exact_block(bev, bodd);
+            exact_block(bev, bodd, cmask);
             dense = p.dense_ok != 0 && __any_sync(FULL, bev >= (uint32_t)K / 2);
           } else if (cnt == 1) {
             // one hit: slot k from the record, step hj tracked in the loop
