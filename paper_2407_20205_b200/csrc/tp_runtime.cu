@@ -241,14 +241,15 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
     unsigned long long chunks = 1;
     while (bsteps / (2 * chunks) >= 32 && B * (unsigned long long)P * chunks < want) chunks *= 2;
     const size_t need = (size_t)B * P * (1024 * sizeof(uint16_t) + sizeof(uint32_t));
-    if (d.bucket_ws_size < need) {
+    const size_t kBucketWsMax = (size_t)4 << 30;  // larger batches take the default walk
+    if (need <= kBucketWsMax && d.bucket_ws_size < need) {
       cudaDeviceSynchronize();  // earlier launches may still read the old lists
       if (d.bucket_ws) cudaFree(d.bucket_ws);
       d.bucket_ws = nullptr;
       d.bucket_ws_size = 0;
       if (cudaMalloc(&d.bucket_ws, need) == cudaSuccess) d.bucket_ws_size = need;
     }
-    if (d.bucket_ws_size >= need) {
+    if (need <= kBucketWsMax && d.bucket_ws_size >= need) {
       pl.bucket = true;
       pl.bucket_B = (long long)B;
       pl.bucket_list = static_cast<uint16_t*>(d.bucket_ws);
