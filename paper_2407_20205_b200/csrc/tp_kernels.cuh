@@ -105,8 +105,8 @@ int bucket_pieces();
 int bucket_fix();
 cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, uint16_t* list, uint32_t* ptab,
                                 cudaStream_t st);
-cudaError_t launch_walk_bucket(int grid, const BucketParams& bp, cudaStream_t st);
-const void* walk_bucket_symbol();
+cudaError_t launch_walk_bucket(int grid, const BucketParams& bp, bool packed, cudaStream_t st);
+const void* walk_bucket_symbol(bool packed);
 
 const void* walk_fast_symbol(int variant);
 const void* walk_generic_symbol(int nw);

@@ -105,7 +105,7 @@ int ensure_device(int dev, Device** out) {
     TP_CUDA(cudaMalloc(&d.queues, 2 * Device::kQueues * sizeof(unsigned long long)));
     TP_CUDA(cudaMemset(d.queues, 0, 2 * Device::kQueues * sizeof(unsigned long long)));
     TP_CUDA(cudaMalloc(&d.tc_err, sizeof(unsigned long long)));
-    TP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.bucket_blocks_per_sm, tp::walk_bucket_symbol(), 128, 0));
+    TP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.bucket_blocks_per_sm, tp::walk_bucket_symbol(true), 128, 0));
     if (d.bucket_blocks_per_sm < 1) return fail(TP_E_CUDA, "bucket walk cannot be resident on device %d", dev);
     TP_CUDA(cudaMemset(d.tc_err, 0, sizeof(unsigned long long)));
     TP_CUDA(cudaMallocHost(&d.stage, Device::kStageBytes));
@@ -164,6 +164,7 @@ struct Plan {
   tp::BucketParams bkp{};
   int bucket_grid = 0;
   long long bucket_B = 0;
+  bool bucket_packed = true;
   uint16_t* bucket_list = nullptr;
   uint32_t* bucket_ptab = nullptr;
   bool tc = false;  // tensor-core pair test covers the whole plan
@@ -251,6 +252,7 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
     }
     if (need <= kBucketWsMax && d.bucket_ws_size >= need) {
       pl.bucket = true;
+      pl.bucket_packed = bucket_mode() != 2;  // 2: the unpacked pair tests
       pl.bucket_B = (long long)B;
       pl.bucket_list = static_cast<uint16_t*>(d.bucket_ws);
       pl.bucket_ptab = reinterpret_cast<uint32_t*>(pl.bucket_list + (size_t)B * P * 1024);
@@ -411,7 +413,7 @@ int run_plan(const Plan& pl, cudaStream_t st, int* launches) {
   int nl = 0;
   if (pl.bucket) {
     TP_CUDA(tp::launch_bucket_group(pl.bkp.fp.rows, pl.bucket_B, pl.bkp.fp.n, pl.bucket_list, pl.bucket_ptab, st));
-    TP_CUDA(tp::launch_walk_bucket(pl.bucket_grid, pl.bkp, st));
+    TP_CUDA(tp::launch_walk_bucket(pl.bucket_grid, pl.bkp, pl.bucket_packed, st));
     if (launches) *launches += 2;
     return TP_OK;
   }

@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n,
 
 }  // namespace
 
-template <int V, int WARPS>
+template <int V, int WARPS, bool PACKED>
 __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) {
   constexpr int KB = 5;
   constexpr int K = 1 << KB;
@@ -104,7 +104,10 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
   __shared__ RowRec Rs[WARPS][32];
   __shared__ uint4 Hs[WARPS][SB];
   __shared__ uint2 As[WARPS][K][32];
+  __shared__ uint2 Es[WARPS][PACKED ? SB / 2 : 1][32];  // per-lane filter passes: (mask, steps)
   const uint32_t lane = threadIdx.x & 31u;
+  uint2 (*E)[32] = Es[threadIdx.x >> 5];
+  const uint32_t cneg = 0xfffeffffu * p.one;  // -0x00010001, runtime so ptxas keeps the IMAD
   RowRec* R = Rs[threadIdx.x >> 5];
   uint4* H = Hs[threadIdx.x >> 5];
   uint2 (*A)[32] = As[threadIdx.x >> 5];
@@ -154,6 +157,15 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
         A[k][lane] = make_uint2(z, g);
       }
     }
+    // packed filter words: low 16 columns of slot w (low half) and w + 16 (high half)
+    uint32_t Zp[K / 2], Gp[K / 2];
+    if (PACKED) {
+#pragma unroll
+      for (int w = 0; w < K / 2; ++w) {
+        Zp[w] = __byte_perm(z1[w], z1[w + K / 2], 0x5410);
+        Gp[w] = __byte_perm(g1[w], g1[w + K / 2], 0x5410);
+      }
+    }
     // forbidden key trits of this piece: f = -x (mod 3)
     const uint32_t x1 = grp / 3, x2 = grp % 3;
     const uint32_t f1 = (3 - x1) % 3, f2 = (3 - x2) % 3;
@@ -183,8 +195,9 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
         uint32_t n0 = 0, a0 = 0, n1 = 0, a1 = 0;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          if ((spm >> k) & 1u) exact_fold(z1[k], g1[k], h.x, h.y, gh, colmask, n1, a1, one);
-          else exact_fold(z1[k], g1[k], h.x, h.y, gh, colmask, n0, a0, one);
+          const uint2 a = PACKED ? A[k][lane] : make_uint2(z1[k], g1[k]);
+          if ((spm >> k) & 1u) exact_fold(a.x, a.y, h.x, h.y, gh, colmask, n1, a1, one);
+          else exact_fold(a.x, a.y, h.x, h.y, gh, colmask, n0, a0, one);
         }
         // term is odd iff popc(sgn) + j + parity(A subset) is odd
         bev += n0 + n1;
@@ -208,7 +221,9 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
         }
       }
       __syncwarp();
-      if (lane < (uint32_t)SB) H[lane] = make_uint4(zj, uj, 0u, 0u);
+      if (lane < (uint32_t)SB)
+        H[lane] = PACKED ? make_uint4(zj, uj, __byte_perm(zj, zj, 0x1010), __byte_perm(uj, uj, 0x1010))
+                         : make_uint4(zj, uj, 0u, 0u);
       // compatible steps: no key column of y equals the forbidden trit
       // (y = 0 <=> z; y = 2 <=> ~z & ~u; y = 1 <=> ~z & u)
       const uint32_t match = (zj & F0) | (~zj & ~uj & F2) | (~zj & uj & F1);
@@ -228,74 +243,130 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
         // hit records (slot of the last hit) << 16 | hit count, four of them
         // (slots k mod 4) so that the predicated IMADs do not form one chain
         uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
-        // two compatible steps per iteration (independent tests interleave);
-        // the next two states are loaded before the current tests
-        uint32_t cm = cmask;
-        uint32_t ja = 0, jb = 0, hj = 0;
-        uint4 ha = make_uint4(0, 0, 0, 0), hb = ha;
-        auto pop2 = [&]() {
-          ja = __ffs(cm) - 1;
-          cm &= cm - 1;
-          jb = __ffs(cm) - 1;
-          cm &= cm - 1;
-        };
-        if (__popc(cm) >= 2) {
-          pop2();
-          ha = H[ja];
-          hb = H[jb];
-          for (;;) {
-            const uint4 ca = ha, cb = hb;
-            const uint32_t cja = ja, cjb = jb;
-            const bool more = __popc(cm) >= 2;
-            if (more) {
-              pop2();
-              ha = H[ja];
-              hb = H[jb];
+        if constexpr (PACKED) {
+          // packed filter over the compatible steps, two per iteration: bit w
+          // (step a) / 16 + w (step b) of M = a pass of word w; nonzero masks
+          // go to this lane's list E for the exact verify after the loop
+          uint32_t cm = cmask, ne = 0;
+          while (cm) {
+            const uint32_t ja = __ffs(cm) - 1;
+            cm &= cm - 1;
+            const uint32_t jb = cm ? (uint32_t)(__ffs(cm) - 1) : 0xFFu;
+            if (cm) cm &= cm - 1;
+            const uint4 ha = H[ja];
+            const uint4 hb = H[jb == 0xFFu ? ja : jb];
+            uint32_t M = 0;
+            static_for<K / 2>([&](auto wc) {
+              constexpr int w = decltype(wc)::value;
+              packed_test<(1u << w)>(Zp[w], Gp[w], ha.z, ha.w, M, one, cneg);
+              packed_test<(1u << (16 + w))>(Zp[w], Gp[w], hb.z, hb.w, M, one, cneg);
+            });
+            if (jb == 0xFFu) M &= 0xFFFFu;
+            if (M) {
+              E[ne][lane] = make_uint2(M, ja | (jb << 8));
+              ++ne;
             }
-            const uint32_t sa = r0 + r1, sb = r2 + r3;
+          }
+          if (__any_sync(FULL, ne != 0)) {
+            uint32_t bev = 0, bodd = 0;
+            for (uint32_t e = 0; e < ne; ++e) {
+              const uint2 ent = E[e][lane];
+              uint32_t M = ent.x;
+              while (M) {
+                const uint32_t bit = __ffs(M) - 1;
+                M &= M - 1;
+                const uint32_t j = (bit < 16) ? (ent.y & 0xFFu) : (ent.y >> 8), w = bit & 15u;
+                const uint4 h = H[j];
+                const uint32_t gh = pair_g2(h.x, h.y);
+  #pragma unroll
+                for (int hf = 0; hf < 2; ++hf) {
+                  const uint32_t k = w + 16 * hf;
+                  const uint2 a = A[k][lane];
+                  uint32_t d, zp;
+                  TP_LOP3(d, a.x, a.y, h.y, 0x06);
+                  TP_LOP3(zp, d, a.x, h.x, 0x09);
+                  if (zp == 0) {
+                    bev += 1;
+                    bodd += (__popc((d ^ gh) & colmask) + j + ((spm >> k) & 1u)) & 1u;
+                  }
+                }
+              }
+            }
+            ev += bev;
+            odd += bodd;
+            // event-dense (e.g. all-ones rows): exact mode for the next superblocks
+            dense = p.dense_ok != 0 && __any_sync(FULL, bev >= (uint32_t)K / 2);
+          }
+        } else {
+          // two compatible steps per iteration (independent tests interleave);
+          // the next two states are loaded before the current tests
+          uint32_t cm = cmask;
+          uint32_t ja = 0, jb = 0, hj = 0;
+          uint4 ha = make_uint4(0, 0, 0, 0), hb = ha;
+          auto pop2 = [&]() {
+            ja = __ffs(cm) - 1;
+            cm &= cm - 1;
+            jb = __ffs(cm) - 1;
+            cm &= cm - 1;
+          };
+          if (__popc(cm) >= 2) {
+            pop2();
+            ha = H[ja];
+            hb = H[jb];
+            for (;;) {
+              const uint4 ca = ha, cb = hb;
+              const uint32_t cja = ja, cjb = jb;
+              const bool more = __popc(cm) >= 2;
+              if (more) {
+                pop2();
+                ha = H[ja];
+                hb = H[jb];
+              }
+              const uint32_t sa = r0 + r1, sb = r2 + r3;
+              static_for<K>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                uint32_t& r = (k & 1) ? r1 : r0;
+                uint32_t& rr = (k & 1) ? r3 : r2;
+                pair_test<((uint32_t)k << 16) | 1u>(z1[k], g1[k], ca.x, ca.y, r, one);
+                pair_test<((uint32_t)k << 16) | 1u>(z1[k], g1[k], cb.x, cb.y, rr, one);
+              });
+              // step of this lane's latest hit (the single-hit path needs it)
+              if (r0 + r1 != sa) hj = cja;
+              if (r2 + r3 != sb) hj = cjb;
+              if (!more) break;
+            }
+          }
+          if (cm) {
+            const uint32_t jc = __ffs(cm) - 1;
+            const uint4 hc = H[jc];
+            const uint32_t sa = r0 + r1;
             static_for<K>([&](auto kc) {
               constexpr int k = decltype(kc)::value;
               uint32_t& r = (k & 1) ? r1 : r0;
-              uint32_t& rr = (k & 1) ? r3 : r2;
-              pair_test<((uint32_t)k << 16) | 1u>(z1[k], g1[k], ca.x, ca.y, r, one);
-              pair_test<((uint32_t)k << 16) | 1u>(z1[k], g1[k], cb.x, cb.y, rr, one);
+              pair_test<((uint32_t)k << 16) | 1u>(z1[k], g1[k], hc.x, hc.y, r, one);
             });
-            // step of this lane's latest hit (the single-hit path needs it)
-            if (r0 + r1 != sa) hj = cja;
-            if (r2 + r3 != sb) hj = cjb;
-            if (!more) break;
+            if (r0 + r1 != sa) hj = jc;
           }
-        }
-        if (cm) {
-          const uint32_t jc = __ffs(cm) - 1;
-          const uint4 hc = H[jc];
-          const uint32_t sa = r0 + r1;
-          static_for<K>([&](auto kc) {
-            constexpr int k = decltype(kc)::value;
-            uint32_t& r = (k & 1) ? r1 : r0;
-            pair_test<((uint32_t)k << 16) | 1u>(z1[k], g1[k], hc.x, hc.y, r, one);
-          });
-          if (r0 + r1 != sa) hj = jc;
-        }
-        const uint32_t cnt = (r0 & 0xffffu) + (r1 & 0xffffu) + (r2 & 0xffffu) + (r3 & 0xffffu);
-        const uint32_t rec = (r0 & 0xffffu) ? r0 : (r1 & 0xffffu) ? r1 : (r2 & 0xffffu) ? r2 : r3;
-        if (__any_sync(FULL, cnt != 0)) {
-          uint32_t bev = 0, bodd = 0;
-          if (__any_sync(FULL, cnt > 1)) {
-            exact_block(bev, bodd, cmask);
-            dense = p.dense_ok != 0 && __any_sync(FULL, bev >= (uint32_t)K / 2);
-          } else if (cnt == 1) {
-            // one hit: slot k from the record, step hj tracked in the loop
-            const uint32_t k = rec >> 16;
-            const uint2 a1 = A[k][lane];
-            const uint4 hh = H[hj];
-            uint32_t d;
-            TP_LOP3(d, a1.x, a1.y, hh.y, 0x06);
-            bev = 1;
-            bodd = (__popc((d ^ pair_g2(hh.x, hh.y)) & colmask) + hj + ((spm >> k) & 1u)) & 1u;
+          const uint32_t cnt = (r0 & 0xffffu) + (r1 & 0xffffu) + (r2 & 0xffffu) + (r3 & 0xffffu);
+          const uint32_t rec = (r0 & 0xffffu) ? r0 : (r1 & 0xffffu) ? r1 : (r2 & 0xffffu) ? r2 : r3;
+          if (__any_sync(FULL, cnt != 0)) {
+            uint32_t bev = 0, bodd = 0;
+            if (__any_sync(FULL, cnt > 1)) {
+              exact_block(bev, bodd, cmask);
+              dense = p.dense_ok != 0 && __any_sync(FULL, bev >= (uint32_t)K / 2);
+            } else if (cnt == 1) {
+              // one hit: slot k from the record, step hj tracked in the loop
+              const uint32_t k = rec >> 16;
+              const uint2 a1 = A[k][lane];
+              const uint4 hh = H[hj];
+              uint32_t d;
+              TP_LOP3(d, a1.x, a1.y, hh.y, 0x06);
+              bev = 1;
+              bodd = (__popc((d ^ pair_g2(hh.x, hh.y)) & colmask) + hj + ((spm >> k) & 1u)) & 1u;
+            }
+            ev += bev;
+            odd += bodd;
           }
-          ev += bev;
-          odd += bodd;
         }
       }
       // (z2, u2) = step SB-1 of this superblock, then the entry step of kb + 1
@@ -323,11 +394,15 @@ cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, uint16_t
   return cudaGetLastError();
 }
 
-cudaError_t launch_walk_bucket(int grid, const BucketParams& bp, cudaStream_t st) {
-  k_walk_bucket<4, 4><<<grid, 128, 0, st>>>(bp);
+cudaError_t launch_walk_bucket(int grid, const BucketParams& bp, bool packed, cudaStream_t st) {
+  if (packed) k_walk_bucket<4, 4, true><<<grid, 128, 0, st>>>(bp);
+  else k_walk_bucket<4, 4, false><<<grid, 128, 0, st>>>(bp);
   return cudaGetLastError();
 }
 
-const void* walk_bucket_symbol() { return reinterpret_cast<const void*>(&k_walk_bucket<4, 4>); }
+const void* walk_bucket_symbol(bool packed) {
+  return packed ? reinterpret_cast<const void*>(&k_walk_bucket<4, 4, true>)
+                : reinterpret_cast<const void*>(&k_walk_bucket<4, 4, false>);
+}
 
 }  // namespace tp

@@ -225,6 +225,23 @@ __device__ __forceinline__ void pair_test(uint32_t z1, uint32_t g1, uint32_t z2,
       : "r"(z1), "r"(g1), "r"(z2), "r"(u2), "r"(one), "n"(IMM));
 }
 
+// Packed pair test (tp_walk_packed.cu): two pairs per 32-bit word on 16
+// columns each; sets BIT of m when either half has no zero column.
+template <uint32_t BIT>
+__device__ __forceinline__ void packed_test(uint32_t z1, uint32_t g1, uint32_t z2, uint32_t u2, uint32_t& m,
+                                            uint32_t one, uint32_t cneg) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 d, zp, t, h;\n\t"
+      "lop3.b32 d, %1, %2, %4, 0x06;\n\t"
+      "lop3.b32 zp, d, %1, %3, 0x09;\n\t"
+      "mad.lo.u32 t, zp, %5, %6;\n\t"
+      "lop3.b32 h, t, 0x80008000, zp, 0x40;\n\t"
+      "setp.ne.u32 p, h, 0;\n\t"
+      "@p mad.lo.u32 %0, %5, %7, %0;\n\t}"
+      : "+r"(m)
+      : "r"(z1), "r"(g1), "r"(z2), "r"(u2), "r"(one), "r"(cneg), "n"(BIT));
+}
+
 __device__ __forceinline__ uint32_t pair_u2(uint32_t z2, uint32_t g2) {
   uint32_t u;
   TP_LOP3(u, z2, g2, 0u, 0xC3);

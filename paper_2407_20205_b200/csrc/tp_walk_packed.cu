@@ -30,21 +30,6 @@
 
 namespace tp {
 
-template <uint32_t BIT>
-__device__ __forceinline__ void packed_test(uint32_t z1, uint32_t g1, uint32_t z2, uint32_t u2, uint32_t& m,
-                                            uint32_t one, uint32_t cneg) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t.reg .b32 d, zp, t, h;\n\t"
-      "lop3.b32 d, %1, %2, %4, 0x06;\n\t"
-      "lop3.b32 zp, d, %1, %3, 0x09;\n\t"
-      "mad.lo.u32 t, zp, %5, %6;\n\t"
-      "lop3.b32 h, t, 0x80008000, zp, 0x40;\n\t"
-      "setp.ne.u32 p, h, 0;\n\t"
-      "@p mad.lo.u32 %0, %5, %7, %0;\n\t}"
-      : "+r"(m)
-      : "r"(z1), "r"(g1), "r"(z2), "r"(u2), "r"(one), "r"(cneg), "n"(BIT));
-}
-
 // Exact fold of the B states Hb[0..SB) against the lane's 32 slots (full A
 // words in shared memory): the dense mode.  Not inlined, so that its
 // registers do not constrain the filter loop's allocation.
