@@ -103,6 +103,7 @@ struct BucketParams {
 };
 int bucket_pieces();
 int bucket_fix();
+int bucket_v(bool packed);
 cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, uint16_t* list, uint32_t* ptab,
                                 cudaStream_t st);
 cudaError_t launch_walk_bucket(int grid, const BucketParams& bp, bool packed, cudaStream_t st);

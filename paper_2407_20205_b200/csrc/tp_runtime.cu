@@ -235,12 +235,14 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
   pl.nw = n <= 32 ? 1 : 2;
   // Bucketed pair walk: items (matrix, piece, chunk) of L = 2^(n-14) / chunks
   // B steps (superblocks of 16, at least 2 per item).
-  if (full && n >= 20 && n <= 31 && B > 0 && bucket_mode() > 0) {
+  if (full && n >= 21 && n <= 31 && B > 0 && bucket_mode() > 0) {
     const int P = tp::bucket_pieces();
+    const bool packed = bucket_mode() != 2;  // 2: the unpacked pair tests
+    const int bv = tp::bucket_v(packed);
     const unsigned long long bsteps = 1ull << (n - tp::bucket_fix());
     const unsigned long long want = 4ull * d.sm_count * d.bucket_blocks_per_sm * 4;
     unsigned long long chunks = 1;
-    while (bsteps / (2 * chunks) >= 32 && B * (unsigned long long)P * chunks < want) chunks *= 2;
+    while (bsteps / (2 * chunks) >= (2ull << bv) && B * (unsigned long long)P * chunks < want) chunks *= 2;
     const size_t need = (size_t)B * P * (1024 * sizeof(uint16_t) + sizeof(uint32_t));
     const size_t kBucketWsMax = (size_t)4 << 30;  // larger batches take the default walk
     if (need <= kBucketWsMax && d.bucket_ws_size < need) {
@@ -252,7 +254,7 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
     }
     if (need <= kBucketWsMax && d.bucket_ws_size >= need) {
       pl.bucket = true;
-      pl.bucket_packed = bucket_mode() != 2;  // 2: the unpacked pair tests
+      pl.bucket_packed = packed;
       pl.bucket_B = (long long)B;
       pl.bucket_list = static_cast<uint16_t*>(d.bucket_ws);
       pl.bucket_ptab = reinterpret_cast<uint32_t*>(pl.bucket_list + (size_t)B * P * 1024);
@@ -264,7 +266,7 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
       f.L = bsteps / chunks;
       f.chunks = chunks;
       f.items = B * (unsigned long long)P * chunks;
-      f.nblk = (uint32_t)(f.L >> 4);  // superblocks of 16 B steps
+      f.nblk = (uint32_t)(f.L >> bv);  // superblocks of 2^bv B steps
       f.lognblk = 0;
       while ((1u << f.lognblk) < f.nblk) f.lognblk++;
       f.n = n;

@@ -104,7 +104,8 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
   __shared__ RowRec Rs[WARPS][32];
   __shared__ uint4 Hs[WARPS][SB];
   __shared__ uint2 As[WARPS][K][32];
-  __shared__ uint2 Es[WARPS][PACKED ? SB / 2 : 1][32];  // per-lane filter passes: (mask, steps)
+  constexpr int ECAP = PACKED ? 6 : 1;  // per-lane pass-list capacity (overflow: exact superblock)
+  __shared__ uint2 Es[WARPS][ECAP][32];   // per-lane filter passes: (mask, steps)
   const uint32_t lane = threadIdx.x & 31u;
   uint2 (*E)[32] = Es[threadIdx.x >> 5];
   const uint32_t cneg = 0xfffeffffu * p.one;  // -0x00010001, runtime so ptxas keeps the IMAD
@@ -263,11 +264,20 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
             });
             if (jb == 0xFFu) M &= 0xFFFFu;
             if (M) {
-              E[ne][lane] = make_uint2(M, ja | (jb << 8));
+              if (ne < (uint32_t)ECAP) E[ne][lane] = make_uint2(M, ja | (jb << 8));
               ++ne;
             }
           }
-          if (__any_sync(FULL, ne != 0)) {
+          if (__any_sync(FULL, ne > (uint32_t)ECAP)) {
+            // a lane's pass list overflowed (event-dense matrix): evaluate the
+            // superblock's compatible steps exactly instead
+            __syncwarp();
+            uint32_t bev, bodd;
+            exact_block(bev, bodd, cmask);
+            ev += bev;
+            odd += bodd;
+            dense = p.dense_ok != 0 && __any_sync(FULL, bev >= (uint32_t)K / 2);
+          } else if (__any_sync(FULL, ne != 0)) {
             uint32_t bev = 0, bodd = 0;
             for (uint32_t e = 0; e < ne; ++e) {
               const uint2 ent = E[e][lane];
@@ -386,6 +396,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
 }
 
 int bucket_pieces() { return kBucketPieces; }
+int bucket_v(bool packed) { return packed ? 5 : 4; }  // log2 superblock length
 int bucket_fix() { return kBucketFix; }
 
 cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, uint16_t* list, uint32_t* ptab,
@@ -395,13 +406,13 @@ cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, uint16_t
 }
 
 cudaError_t launch_walk_bucket(int grid, const BucketParams& bp, bool packed, cudaStream_t st) {
-  if (packed) k_walk_bucket<4, 4, true><<<grid, 128, 0, st>>>(bp);
+  if (packed) k_walk_bucket<5, 4, true><<<grid, 128, 0, st>>>(bp);
   else k_walk_bucket<4, 4, false><<<grid, 128, 0, st>>>(bp);
   return cudaGetLastError();
 }
 
 const void* walk_bucket_symbol(bool packed) {
-  return packed ? reinterpret_cast<const void*>(&k_walk_bucket<4, 4, true>)
+  return packed ? reinterpret_cast<const void*>(&k_walk_bucket<5, 4, true>)
                 : reinterpret_cast<const void*>(&k_walk_bucket<4, 4, false>);
 }
 
