@@ -339,6 +339,7 @@ def main():
     if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
+    _kernels.walk_tested(local)  # reset the bucketed walk's tested-pair counter
     with ClockSampler(local) as clk:
         evs = []
         for _ in range(args.steps):
@@ -354,6 +355,7 @@ def main():
             s1.record()
             evs.append((s0, s1, w))
         torch.cuda.synchronize()
+    tested_pairs = _kernels.walk_tested(local)  # pairs the bucketed walk tested in the K steps
     if use_dist:
         dist.barrier()
     for s0, s1, (w0, w1) in evs:
@@ -382,6 +384,13 @@ def main():
     # served this n (2 for the pair walk, 3 for the lane/wide walks; n > 32
     # tests only the 32 primary columns -- see DESIGN.md)
     kernel_name, ops_per_term = _kernels.walk_info(n, B)
+    tested_frac = None
+    if "bucket" in kernel_name:
+        # the bucketed walk tests only the pairs its key columns do not prove
+        # zero: LOP3 per term = LOP3 per tested pair x the tested fraction,
+        # counted by the kernel itself over the timed steps
+        tested_frac = tested_pairs / (per_rank_terms * args.steps)
+        ops_per_term = ops_per_term * tested_frac
     walk_avg = sum(walk_ms) / len(walk_ms)
     achieved = per_rank_terms * ops_per_term / (walk_avg * 1e-3)
     peak, _ = _kernels.alu_peak(local)
@@ -459,11 +468,13 @@ def main():
                        "terms_per_step": job_terms},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "LOP3 ops/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": kernel_name + " (csrc/" + ("tp_walk_packed.cu" if "packed" in kernel_name
+                         "kernel": kernel_name + " (csrc/" + ("tp_walk_bucket.cu" if "bucket" in kernel_name
+                                                              else "tp_walk_packed.cu" if "packed" in kernel_name
                                                               else "tp_walk_pair.cu" if "pair" in kernel_name
                                                               else "tp_walk_lane.cu" if "lane" in kernel_name
                                                               else "tp_walk_wide.cu") + ")",
                          "ops_per_term": ops_per_term,
+                         "tested_pairs_frac": tested_frac,
                          "peak_source": "LOP3 chain probe (tp_alu_peak) on this GPU in this run; "
                                         "nominal 148 SM x 64 lanes x clock",
                          "walk_ms_avg": walk_avg,

@@ -135,8 +135,14 @@ int tp_exact_census(int n, int device, int64_t *zeros, int64_t *plus, int64_t *m
 /* Which walk kernel serves full traversals of `batch` matrices of size n
  * (batch = 1: a single matrix or a range), and its LOP3 count per subset
  * term (3 for the lane/wide walks, 2 for the pair walks, 1.5 for the packed
- * walks). */
+ * walks).  For the bucketed walk (batches, 21 <= n <= 31) the count is per
+ * TESTED pair: it skips the pairs its key columns prove zero, and
+ * tp_walk_tested reports how many it tested. */
 int tp_walk_info(int n, long long batch, char *name, int name_len, double *lop3_per_term);
+
+/* Pairs tested by the bucketed walk on `device` since the last call (the
+ * counter is read and reset).  Diagnostics for the roofline accounting. */
+int tp_walk_tested(int device, uint64_t *pairs);
 
 /* Diagnostics: measured LOP3 throughput of `device` (ops/s, the ALU-pipe
  * roofline denominator) from a register-resident lop3 chain kernel timed

@@ -76,6 +76,7 @@ SIGNATURES = {
                                     ctypes.POINTER(ctypes.c_double)]),
     "tp_exact_census": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _i64p, _i64p, _i64p]),
     "tp_alu_peak": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
+    "tp_walk_tested": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)]),
 }
 
 ROWREC_BYTES = 2048  # TP_ROWREC_BYTES: packed row records per matrix
@@ -247,6 +248,14 @@ def walk_info(n: int, batch: int = 1) -> Tuple[str, float]:
     ops = ctypes.c_double()
     _check(lib().tp_walk_info(n, batch, buf, 128, ctypes.byref(ops)))
     return buf.value.decode(), float(ops.value)
+
+
+def walk_tested(device: Optional[int] = None) -> int:
+    """Pairs tested by the bucketed walk since the last call (read and reset)."""
+    dev = default_device() if device is None else device
+    v = ctypes.c_uint64(0)
+    _check(lib().tp_walk_tested(dev, ctypes.byref(v)))
+    return int(v.value)
 
 
 def alu_peak(device: Optional[int] = None) -> Tuple[float, float]:

@@ -100,6 +100,7 @@ struct BucketParams {
   FastParams fp;                // items = B * bucket_pieces() * chunks; L, nblk as in the fast walks
   const uint16_t* list;         // [B][pieces][1024] A subsets (0xFFFF = dummy slot)
   const uint32_t* ptab;         // [B][pieces] bucket | valid count << 16 (count 0 = unused)
+  unsigned long long* tested;   // += pairs actually tested (compatible steps x 1024), or nullptr
 };
 int bucket_pieces();
 int bucket_fix();

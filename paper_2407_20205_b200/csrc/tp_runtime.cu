@@ -57,6 +57,7 @@ struct Device {
   unsigned long long* queues = nullptr;
   int next_queue = 0;
   unsigned long long* tc_err = nullptr;  // tensor-path self-check counter (must stay 0)
+  unsigned long long* bucket_tested = nullptr;  // pairs tested by the bucketed walk (tp_walk_tested)
   void* bucket_ws = nullptr;  // bucket lists of the bucketed walk (grow-only)
   size_t bucket_ws_size = 0;
   int bucket_blocks_per_sm = 0;
@@ -108,6 +109,8 @@ int ensure_device(int dev, Device** out) {
     TP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.bucket_blocks_per_sm, tp::walk_bucket_symbol(true), 128, 0));
     if (d.bucket_blocks_per_sm < 1) return fail(TP_E_CUDA, "bucket walk cannot be resident on device %d", dev);
     TP_CUDA(cudaMemset(d.tc_err, 0, sizeof(unsigned long long)));
+    TP_CUDA(cudaMalloc(&d.bucket_tested, sizeof(unsigned long long)));
+    TP_CUDA(cudaMemset(d.bucket_tested, 0, sizeof(unsigned long long)));
     TP_CUDA(cudaMallocHost(&d.stage, Device::kStageBytes));
     d.ready = true;
   }
@@ -176,11 +179,17 @@ struct Plan {
 // TRITPERM_TC=1: exact, but slower than the packed LOP3 walk on B200 (its
 // 128 x 128 x 64 sub-tiles turn TMEM over faster than the MMA/epilogue
 // handshake allows).
-// Bucketed pair walk (tp_walk_bucket.cu) for full traversals of 20 <= n <= 31:
-// TRITPERM_BUCKET=0 turns it off, =1 forces it wherever it applies.
+// Bucketed pair walk (tp_walk_bucket.cu), the default for full traversals of
+// batches with 21 <= n <= 31: TRITPERM_BUCKET=0 selects the packed walk,
+// =2 the bucketed walk with unpacked pair tests.
 int bucket_mode() {
   const char* e = getenv("TRITPERM_BUCKET");  // read per call: tests switch it at run time
-  return e ? atoi(e) : 0;
+  return e ? atoi(e) : 1;
+}
+
+// Same size rule as the packed walk: the job must fill the GPU.
+bool bucket_applies(int n, unsigned long long B) {
+  return n >= 21 && n <= 31 && B > 0 && (B << (n - 15)) >= 2048ull && bucket_mode() > 0;
 }
 
 int tc_mode() {
@@ -235,7 +244,7 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
   pl.nw = n <= 32 ? 1 : 2;
   // Bucketed pair walk: items (matrix, piece, chunk) of L = 2^(n-14) / chunks
   // B steps (superblocks of 16, at least 2 per item).
-  if (full && n >= 21 && n <= 31 && B > 0 && bucket_mode() > 0) {
+  if (full && bucket_applies(n, B)) {
     const int P = tp::bucket_pieces();
     const bool packed = bucket_mode() != 2;  // 2: the unpacked pair tests
     const int bv = tp::bucket_v(packed);
@@ -278,6 +287,7 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
       f.static_items = 0;
       pl.bkp.list = pl.bucket_list;
       pl.bkp.ptab = pl.bucket_ptab;
+      pl.bkp.tested = d.bucket_tested;
       const unsigned long long ctas = (unsigned long long)d.sm_count * d.bucket_blocks_per_sm;
       pl.bucket_grid = (int)std::max<unsigned long long>(1, std::min(ctas, (f.items + 3) / 4));
       return;
@@ -782,6 +792,15 @@ int tp_walk_info(int n, long long batch, char* name, int name_len, double* lop3_
   if (n < 1 || n > TP_MAX_N) return fail(TP_E_INVALID, "need 1 <= n <= %d, got %d", TP_MAX_N, n);
   if (batch < 1) return fail(TP_E_INVALID, "need batch >= 1, got %lld", batch);
   const int v = choose_variant(n, (unsigned long long)batch);
+  if (bucket_applies(n, (unsigned long long)batch)) {
+    // 1.5 LOP3 per TESTED pair: the bucketed walk skips the incompatible
+    // steps, so the tested fraction (tp_walk_tested) scales this per term
+    const bool packed = bucket_mode() != 2;
+    if (name && name_len > 0)
+      snprintf(name, (size_t)name_len, "k_walk_bucket<%s> V=%d", packed ? "packed" : "pair", tp::bucket_v(packed));
+    if (lop3_per_term) *lop3_per_term = packed ? 1.5 : 2.0;
+    return TP_OK;
+  }
   const char* kind;
   double ops;
   if (n <= tp::kSmallMaxN) {
@@ -802,6 +821,20 @@ int tp_walk_info(int n, long long batch, char* name, int name_len, double* lop3_
   }
   if (name && name_len > 0) snprintf(name, (size_t)name_len, "%s KB=%d V=%d", kind, tp::fast_kb(v), tp::fast_v(v));
   if (lop3_per_term) *lop3_per_term = ops;
+  return TP_OK;
+}
+
+int tp_walk_tested(int device, uint64_t* pairs) {
+  if (!pairs) return fail(TP_E_INVALID, "pairs must not be NULL");
+  Device* d;
+  int rc = ensure_device(device, &d);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(d->mu);
+  TP_CUDA(cudaSetDevice(device));
+  unsigned long long v = 0;
+  TP_CUDA(cudaMemcpy(&v, d->bucket_tested, sizeof v, cudaMemcpyDeviceToHost));
+  TP_CUDA(cudaMemset(d->bucket_tested, 0, sizeof v));
+  *pairs = v;
   return TP_OK;
 }
 

@@ -184,6 +184,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
       u2 = pair_u2(z, g);
     }
     uint32_t ev = 0, odd = 0;
+    uint32_t tested_steps = 0;  // compatible steps of this item (x 1024 pairs)
     // exact evaluation of every pair of the superblock from H (replays, dense mode)
     // (only the steps in `mask`: incompatible steps have no full term)
     auto exact_block = [&](uint32_t& bev, uint32_t& bodd, uint32_t mask) {
@@ -229,6 +230,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
       // (y = 0 <=> z; y = 2 <=> ~z & ~u; y = 1 <=> ~z & u)
       const uint32_t match = (zj & F0) | (~zj & ~uj & F2) | (~zj & uj & F1);
       const uint32_t cmask = __ballot_sync(FULL, match == 0u) & (SB == 32 ? 0xffffffffu : ((1u << SB) - 1u));
+      tested_steps += __popc(cmask);
       if (dense) {
         __syncwarp();
         uint32_t bev, bodd;
@@ -391,6 +393,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
       }
     }
     warp_flush(p.pm + 2 * b, ev - odd, odd, lane);
+    if (bp.tested && lane == 0) atomicAdd(bp.tested, 1024ull * tested_steps);
   }
   queue_done(p, lane);
 }

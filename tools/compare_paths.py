@@ -1,8 +1,8 @@
 """Time the C2 workload (16,384 x 24x24, reference trial stream, seed 0)
-through perm_mod3_batch on the default packed walk and on the opt-in exact
-alternatives (TRITPERM_BUCKET=1/2: bucketed pair walk, TRITPERM_TC=1: tcgen05
-pair test), and check that every path returns the same classes and raw
-partials.  Host-timed (H2D, pack, walk, finalize, D2H): the numbers quoted in
+through perm_mod3_batch on every exact path -- the bucketed walk (the
+default, TRITPERM_BUCKET=1; =2 with unpacked pair tests), the packed walk
+(TRITPERM_BUCKET=0) and the tcgen05 pair test (TRITPERM_TC=1) -- and check
+that they return the same classes and raw partials.  Host-timed (H2D, pack, walk, finalize, D2H): the numbers quoted in
 DESIGN.md sections 5b and 5c.
 
     python tools/compare_paths.py [--batch 16384] [--n 24] [--reps 3]
@@ -19,8 +19,8 @@ import paper_2407_20205_b200 as tp  # noqa: E402
 from paper_2407_20205_b200 import fixtures  # noqa: E402
 
 PATHS = {
-    "packed (default)": {"TRITPERM_BUCKET": "0", "TRITPERM_TC": "0"},
-    "bucketed, packed filter": {"TRITPERM_BUCKET": "1", "TRITPERM_TC": "0"},
+    "packed walk": {"TRITPERM_BUCKET": "0", "TRITPERM_TC": "0"},
+    "bucketed (default)": {"TRITPERM_BUCKET": "1", "TRITPERM_TC": "0"},
     "bucketed, pair tests": {"TRITPERM_BUCKET": "2", "TRITPERM_TC": "0"},
     "tcgen05 pair test": {"TRITPERM_BUCKET": "0", "TRITPERM_TC": "1"},
 }
