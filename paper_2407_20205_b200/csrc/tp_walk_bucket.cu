@@ -83,12 +83,14 @@ __global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n,
     for (uint32_t q = piece; q < (uint32_t)kBucketPieces; ++q) P[q] = 0;  // unused pieces: count 0
   }
   __syncthreads();
-  // padding first (the scatter below overwrites the valid prefix of each piece)
-  for (uint32_t i = threadIdx.x; i < (uint32_t)kBucketPieces * 1024u; i += blockDim.x) L[i] = kBucketDummy;
-  __syncthreads();
   for (uint32_t s = threadIdx.x; s < (1u << kBucketFix); s += blockDim.x) {
     const uint32_t g = pat(s);
     L[atomicAdd(&pos[g], 1u)] = (uint16_t)s;
+  }
+  // dummy slots: the tail of each bucket's last piece (unused pieces are never read)
+  for (int g = 0; g < 9; ++g) {
+    const uint32_t end = pstart[g] * 1024u + cnt[g], pend = pstart[g] * 1024u + ((cnt[g] + 1023u) & ~1023u);
+    for (uint32_t i = end + threadIdx.x; i < pend; i += blockDim.x) L[i] = kBucketDummy;
   }
 }
 
