@@ -487,25 +487,27 @@ def test_tensor_core_pair_test_exact(gpu, oracle, monkeypatch):
 
 
 def test_bucketed_pair_walk_exact(gpu, oracle, monkeypatch):
-    """The opt-in bucketed pair walk (TRITPERM_BUCKET=1, tp_walk_bucket.cu):
-    full traversals, 20 <= n <= 31, uniform, sparse and all-ones matrices; raw
-    partials equal the default path and the oracle bit for bit (only zero
-    terms are skipped)."""
+    """The bucketed pair walk (tp_walk_bucket.cu; the default for batches of
+    21 <= n <= 31, TRITPERM_BUCKET=1 packed filter / 2 pair tests) against the
+    packed walk (TRITPERM_BUCKET=0) and the oracle: full traversals, uniform,
+    sparse and all-ones matrices; raw partials bit for bit (only zero terms are
+    skipped)."""
     from paper_2407_20205_b200 import fixtures
 
     r = np.random.default_rng(31)
-    cases = [fixtures.uniform_batch(n, 13, 0, B) for n, B in ((20, 48), (21, 7), (24, 40), (27, 3), (31, 2))]
-    for n in (20, 26):
+    cases = [fixtures.uniform_batch(n, 13, 0, B) for n, B in ((21, 48), (22, 7), (24, 40), (27, 3), (31, 2))]
+    for n in (21, 26):
         sp = ((r.random((5, n, n)) < 0.25) * r.integers(1, 3, (5, n, n))).astype(np.uint8)
         cases.append(np.concatenate([sp, np.ones((2, n, n), np.uint8)]))
     for e in cases:
         n = e.shape[1]
-        monkeypatch.setenv("TRITPERM_BUCKET", "1")
-        cls, part, hist = gpu.perm_mod3_batch(e)
         monkeypatch.setenv("TRITPERM_BUCKET", "0")
         cls0, part0, hist0 = gpu.perm_mod3_batch(e)
-        assert np.array_equal(part, part0) and np.array_equal(cls, cls0), n
-        assert hist.tolist() == hist0.tolist(), n
+        for mode in ("1", "2"):
+            monkeypatch.setenv("TRITPERM_BUCKET", mode)
+            cls, part, hist = gpu.perm_mod3_batch(e)
+            assert np.array_equal(part, part0) and np.array_equal(cls, cls0), (n, mode)
+            assert hist.tolist() == hist0.tolist(), (n, mode)
         if n <= 21:
             mags, sgns = oracle.planes_from_classes(e[0])
             assert part[0] == oracle.chunk_sum(mags, sgns, n, 1, 1 << n), n
