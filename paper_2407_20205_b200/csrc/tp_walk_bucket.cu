@@ -136,15 +136,19 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
     load_rows(R, p.rows + b * 64, lane, p.n);
     __syncwarp();
 
-    // A side: slot k of this lane is the A subset list[piece][32 k + lane]
-    uint32_t z1[K], g1[K];
+    // A side: slot k of this lane is the A subset list[piece][32 k + lane];
+    // full words in shared memory (verify, exact fallback), registers: the
+    // unpacked walk keeps all 32 slots, the packed one only the packed words
+    // (low 16 columns of slot w in the low half, of slot w + 16 in the high)
+    uint32_t z1[PACKED ? 1 : K], g1[PACKED ? 1 : K];
+    uint32_t Zp[PACKED ? K / 2 : 1], Gp[PACKED ? K / 2 : 1];
     uint32_t spm = 0;  // bit k: parity of slot k's subset
     {
       const uint16_t* Lp = bp.list + (b * kBucketPieces + q) * 1024;
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
+      auto slot = [&](int k, uint32_t& z, uint32_t& g) {
         const uint32_t s = Lp[32 * k + lane];
-        uint32_t z = colmask, g = 0;
+        z = colmask;
+        g = 0;
         if (s == kBucketDummy) {
           g = 0x80000000u;  // -1 in padding column 31 (B side: +1): never a full sum
         } else {
@@ -155,18 +159,20 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
           }
           spm |= (uint32_t)(__popc(s) & 1) << k;
         }
-        z1[k] = z;
-        g1[k] = g;
         A[k][lane] = make_uint2(z, g);
-      }
-    }
-    // packed filter words: low 16 columns of slot w (low half) and w + 16 (high half)
-    uint32_t Zp[K / 2], Gp[K / 2];
-    if (PACKED) {
+      };
+      if constexpr (PACKED) {
 #pragma unroll
-      for (int w = 0; w < K / 2; ++w) {
-        Zp[w] = __byte_perm(z1[w], z1[w + K / 2], 0x5410);
-        Gp[w] = __byte_perm(g1[w], g1[w + K / 2], 0x5410);
+        for (int w = 0; w < K / 2; ++w) {
+          uint32_t za, ga, zb, gb;
+          slot(w, za, ga);
+          slot(w + K / 2, zb, gb);
+          Zp[w] = __byte_perm(za, zb, 0x5410);
+          Gp[w] = __byte_perm(ga, gb, 0x5410);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k) slot(k, z1[k], g1[k]);
       }
     }
     // forbidden key trits of this piece: f = -x (mod 3)
@@ -199,7 +205,9 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
         uint32_t n0 = 0, a0 = 0, n1 = 0, a1 = 0;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          const uint2 a = PACKED ? A[k][lane] : make_uint2(z1[k], g1[k]);
+          uint2 a;
+          if constexpr (PACKED) a = A[k][lane];
+          else a = make_uint2(z1[k], g1[k]);
           if ((spm >> k) & 1u) exact_fold(a.x, a.y, h.x, h.y, gh, colmask, n1, a1, one);
           else exact_fold(a.x, a.y, h.x, h.y, gh, colmask, n0, a0, one);
         }
