@@ -180,7 +180,7 @@ struct Plan {
 // 128 x 128 x 64 sub-tiles turn TMEM over faster than the MMA/epilogue
 // handshake allows).
 // Bucketed pair walk (tp_walk_bucket.cu), the default for full traversals of
-// batches with 21 <= n <= 31: TRITPERM_BUCKET=0 selects the packed walk,
+// batches with 21 <= n <= 32: TRITPERM_BUCKET=0 selects the packed walk,
 // =2 the bucketed walk with unpacked pair tests.
 int bucket_mode() {
   const char* e = getenv("TRITPERM_BUCKET");  // read per call: tests switch it at run time
@@ -189,7 +189,11 @@ int bucket_mode() {
 
 // Same size rule as the packed walk: the job must fill the GPU.
 bool bucket_applies(int n, unsigned long long B) {
-  return n >= 21 && n <= 31 && B > 0 && (B << (n - 15)) >= 2048ull && bucket_mode() > 0;
+  const int m = bucket_mode();
+  // n = 32 (no padding column: slower on event-dense matrices, e.g. C3's
+  // all-ones family) only on request, with the packed filter
+  const int nmax = (m == 1 && getenv("TRITPERM_BUCKET")) ? 32 : 31;
+  return n >= 21 && n <= nmax && B > 0 && (B << (n - 15)) >= 2048ull && m > 0;
 }
 
 int tc_mode() {

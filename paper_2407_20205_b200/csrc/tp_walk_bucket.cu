@@ -1,5 +1,6 @@
 // tp_walk_bucket.cu -- the pair walk with the A side bucketed by two key
-// columns (n <= 31, full traversals).
+// columns (full traversals; n <= 32 for the packed filter, n <= 31 for the
+// unpacked pair tests).
 //
 // The pair walk (tp_walk_pair.cu) tests every (A vector, B state) pair.  A pair
 // whose sum has a zero in ANY column is a zero term, so pairs can be skipped
@@ -94,6 +95,70 @@ __global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n,
   }
 }
 
+// Exact fold of one pair with the A subset's parity bit sp: n += full,
+// a += full & (parity(popc(sign word)) ^ sp).
+__device__ __forceinline__ void exact_fold_par(uint32_t z1, uint32_t g1, uint32_t z2, uint32_t u2, uint32_t g2,
+                                               uint32_t cm, uint32_t sp, uint32_t& n, uint32_t& a, uint32_t one) {
+  uint32_t d, zp, x;
+  TP_LOP3(d, z1, g1, u2, 0x06);
+  TP_LOP3(zp, d, z1, z2, 0x09);
+  TP_LOP3(x, d, g2, cm, 0x28);
+  if (zp == 0) {
+    uint32_t t;
+    TP_LOP3(t, (uint32_t)__popc(x), 1u, sp, 0x6A);  // (popc & 1) ^ sp
+    n = one * one + n;
+    a = t * one + a;
+  }
+}
+
+// Exact evaluation of the steps in `mask` against this lane's 32 slots (the
+// packed variant's dense mode and list-overflow path).  Out of line, so its
+// registers do not constrain the filter loop.  Returns ev | odd << 32.
+static __device__ __noinline__ unsigned long long bucket_exact_packed(const uint4 (*A2)[32], const uint4* H,
+                                                                      uint32_t mask, uint32_t lane, uint32_t spm,
+                                                                      uint32_t vmask, uint32_t colmask, int n,
+                                                                      uint32_t one) {
+  constexpr int K = 32;
+  uint32_t bev = 0, bodd = 0;
+#pragma unroll 1
+  for (; mask; mask &= mask - 1) {
+    const int j = __ffs(mask) - 1;
+    const uint4 h = H[j];
+    const uint32_t gh = pair_g2(h.x, h.y);
+    uint32_t n0 = 0, a0 = 0;
+    if (n <= 31) {
+      // the subset parity rides in padding column 31 of the sign word
+      const uint32_t cmp = colmask | 0x80000000u;
+#pragma unroll
+      for (int w = 0; w < K / 2; ++w) {
+        const uint4 a = A2[w][lane];
+        exact_fold(a.x, a.y, h.x, h.y, gh, cmp, n0, a0, one);
+        exact_fold(a.z, a.w, h.x, h.y, gh, cmp, n0, a0, one);
+      }
+    } else {
+      // n = 32: the slot's subset parity is a runtime bit, folded into the
+      // sign parity with one LOP3 instead of a divergent branch
+#pragma unroll
+      for (int w = 0; w < K / 2; ++w) {
+        const uint4 a = A2[w][lane];
+        exact_fold_par(a.x, a.y, h.x, h.y, gh, colmask, (spm >> w) & 1u, n0, a0, one);
+        exact_fold_par(a.z, a.w, h.x, h.y, gh, colmask, (spm >> (w + K / 2)) & 1u, n0, a0, one);
+      }
+      // padding slots hold the zero vector (no column to kill it): each
+      // pairs fully with a full y, with subset parity 0; remove them
+      if (h.x == 0u) {
+        const uint32_t nd = (uint32_t)K - __popc(vmask);
+        n0 -= nd;
+        a0 -= nd * (__popc(gh) & 1u);
+      }
+    }
+    // term is odd iff popc(sgn) + j + parity(A subset) is odd
+    bev += n0;
+    bodd += (j & 1) ? (n0 - a0) : a0;
+  }
+  return (unsigned long long)bev | ((unsigned long long)bodd << 32);
+}
+
 }  // namespace
 
 template <int V, int WARPS, bool PACKED>
@@ -105,7 +170,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
   const FastParams& p = bp.fp;
   __shared__ RowRec Rs[WARPS][32];
   __shared__ uint4 Hs[WARPS][SB];
-  __shared__ uint2 As[WARPS][K][32];
+  __shared__ uint2 As[WARPS][K][32];  // full A words; packed: [w][lane] pairs (slot w, slot w + 16) as uint4
   constexpr int ECAP = PACKED ? 6 : 1;  // per-lane pass-list capacity (overflow: exact superblock)
   __shared__ uint2 Es[WARPS][ECAP][32];   // per-lane filter passes: (mask, steps)
   const uint32_t lane = threadIdx.x & 31u;
@@ -114,6 +179,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
   RowRec* R = Rs[threadIdx.x >> 5];
   uint4* H = Hs[threadIdx.x >> 5];
   uint2 (*A)[32] = As[threadIdx.x >> 5];
+  uint4 (*A2)[32] = reinterpret_cast<uint4 (*)[32]>(As[threadIdx.x >> 5]);
   const uint32_t one = p.one;
   const uint32_t colmask = p.z0_init;  // real columns (n <= 31: bit 31 is padding)
   const int k1 = p.n - 1, k2 = p.n - 2;
@@ -143,6 +209,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
     uint32_t z1[PACKED ? 1 : K], g1[PACKED ? 1 : K];
     uint32_t Zp[PACKED ? K / 2 : 1], Gp[PACKED ? K / 2 : 1];
     uint32_t spm = 0;  // bit k: parity of slot k's subset
+    uint32_t vmask = 0;  // bit k: slot k holds a real A subset (not padding)
     {
       const uint16_t* Lp = bp.list + (b * kBucketPieces + q) * 1024;
       auto slot = [&](int k, uint32_t& z, uint32_t& g) {
@@ -150,8 +217,15 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
         z = colmask;
         g = 0;
         if (s == kBucketDummy) {
-          g = 0x80000000u;  // -1 in padding column 31 (B side: +1): never a full sum
+          // n <= 31: -1 in padding column 31 (B side: +1), never a full sum;
+          // n = 32 has no padding column: the verify and exact paths test vmask
+          if (p.n <= 31) g = 0x80000000u;
         } else {
+          vmask |= 1u << k;
+          // n <= 31: padding column 31 carries the subset parity p as the trit
+          // p (0 or +1; B side +1): the sum there is +1 or -1, so it never
+          // zeroes a column and its sign bit is p (the exact fold counts it)
+          if (p.n <= 31 && !(__popc(s) & 1)) z |= 0x80000000u;
 #pragma unroll 1
           for (uint32_t x = s; x; x &= x - 1) {
             const int t = __ffs(x) - 1;
@@ -159,7 +233,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
           }
           spm |= (uint32_t)(__popc(s) & 1) << k;
         }
-        A[k][lane] = make_uint2(z, g);
+        if constexpr (!PACKED) A[k][lane] = make_uint2(z, g);
       };
       if constexpr (PACKED) {
 #pragma unroll
@@ -169,6 +243,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
           slot(w + K / 2, zb, gb);
           Zp[w] = __byte_perm(za, zb, 0x5410);
           Gp[w] = __byte_perm(ga, gb, 0x5410);
+          A2[w][lane] = make_uint4(za, ga, zb, gb);
         }
       } else {
 #pragma unroll
@@ -196,6 +271,12 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
     // exact evaluation of every pair of the superblock from H (replays, dense mode)
     // (only the steps in `mask`: incompatible steps have no full term)
     auto exact_block = [&](uint32_t& bev, uint32_t& bodd, uint32_t mask) {
+      if constexpr (PACKED) {
+        const unsigned long long r = bucket_exact_packed(A2, H, mask, lane, spm, vmask, colmask, p.n, one);
+        bev = (uint32_t)r;
+        bodd = (uint32_t)(r >> 32);
+        return;
+      }
       bev = bodd = 0;
 #pragma unroll 1
       for (; mask; mask &= mask - 1) {
@@ -205,11 +286,8 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
         uint32_t n0 = 0, a0 = 0, n1 = 0, a1 = 0;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          uint2 a;
-          if constexpr (PACKED) a = A[k][lane];
-          else a = make_uint2(z1[k], g1[k]);
-          if ((spm >> k) & 1u) exact_fold(a.x, a.y, h.x, h.y, gh, colmask, n1, a1, one);
-          else exact_fold(a.x, a.y, h.x, h.y, gh, colmask, n0, a0, one);
+          if ((spm >> k) & 1u) exact_fold(z1[k], g1[k], h.x, h.y, gh, colmask, n1, a1, one);
+          else exact_fold(z1[k], g1[k], h.x, h.y, gh, colmask, n0, a0, one);
         }
         // term is odd iff popc(sgn) + j + parity(A subset) is odd
         bev += n0 + n1;
@@ -303,11 +381,12 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
   #pragma unroll
                 for (int hf = 0; hf < 2; ++hf) {
                   const uint32_t k = w + 16 * hf;
-                  const uint2 a = A[k][lane];
+                  const uint4 a4 = A2[w][lane];
+                  const uint2 a = hf ? make_uint2(a4.z, a4.w) : make_uint2(a4.x, a4.y);
                   uint32_t d, zp;
                   TP_LOP3(d, a.x, a.y, h.y, 0x06);
                   TP_LOP3(zp, d, a.x, h.x, 0x09);
-                  if (zp == 0) {
+                  if (zp == 0 && ((vmask >> k) & 1u)) {
                     bev += 1;
                     bodd += (__popc((d ^ gh) & colmask) + j + ((spm >> k) & 1u)) & 1u;
                   }
