@@ -190,10 +190,9 @@ int bucket_mode() {
 // Same size rule as the packed walk: the job must fill the GPU.
 bool bucket_applies(int n, unsigned long long B) {
   const int m = bucket_mode();
-  // n = 32 (no padding column: slower on event-dense matrices, e.g. C3's
-  // all-ones family) only on request, with the packed filter
-  const int nmax = (m == 1 && getenv("TRITPERM_BUCKET")) ? 32 : 31;
-  return n >= 21 && n <= nmax && B > 0 && (B << (n - 15)) >= 2048ull && m > 0;
+  // n = 32 only with the packed filter (its verify tests the padding-slot
+  // mask: there is no padding column); the unpacked pair tests need n <= 31
+  return n >= 21 && n <= (m == 2 ? 31 : 32) && B > 0 && (B << (n - 15)) >= 2048ull && m > 0;
 }
 
 int tc_mode() {
