@@ -94,18 +94,22 @@ void tc_layout(int n, int* R, int* ks);
 size_t tc_smem_bytes(int n, int ks);
 cudaError_t launch_walk_tc(int grid, const TcParams& p, cudaStream_t st);
 
-// Bucketed pair walk (tp_walk_bucket.cu): full traversals, 20 <= n <= 31.
-// Items (matrix, piece, chunk); list/ptab come from launch_bucket_group.
+// Bucketed pair walk (tp_walk_bucket.cu): 21 <= n <= 64, full traversals and
+// the superblock-aligned middle of ranges.  Items (matrix, piece, chunk);
+// chunk c covers B-side superblocks [F0 + c * nblk, min(F0 + (c + 1) * nblk,
+// s_end)) (superblocks of 2^bucket_v B steps, a B step = 2^14 reference
+// steps); list/ptab come from launch_bucket_group.
 struct BucketParams {
-  FastParams fp;                // items = B * bucket_pieces() * chunks; L, nblk as in the fast walks
+  FastParams fp;                // items = B * bucket_pieces(fix) * chunks; F0, nblk in superblocks
   const uint16_t* list;         // [B][pieces][1024] A subsets (0xFFFF = dummy slot)
   const uint32_t* ptab;         // [B][pieces] bucket | valid count << 16 (count 0 = unused)
   unsigned long long* tested;   // += pairs actually tested (compatible steps x 1024), or nullptr
+  unsigned long long s_end;     // end of the superblock region
 };
-int bucket_pieces();
-int bucket_fix();
+int bucket_pieces(int fix);
+int bucket_fix(int n, bool packed);
 int bucket_v(bool packed);
-cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, uint16_t* list, uint32_t* ptab,
+cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, int fix, uint16_t* list, uint32_t* ptab,
                                 cudaStream_t st);
 cudaError_t launch_walk_bucket(int grid, const BucketParams& bp, bool packed, cudaStream_t st);
 const void* walk_bucket_symbol(bool packed);

@@ -168,6 +168,7 @@ struct Plan {
   int bucket_grid = 0;
   long long bucket_B = 0;
   bool bucket_packed = true;
+  int bucket_fix = 14;
   uint16_t* bucket_list = nullptr;
   uint32_t* bucket_ptab = nullptr;
   bool tc = false;  // tensor-core pair test covers the whole plan
@@ -179,20 +180,22 @@ struct Plan {
 // TRITPERM_TC=1: exact, but slower than the packed LOP3 walk on B200 (its
 // 128 x 128 x 64 sub-tiles turn TMEM over faster than the MMA/epilogue
 // handshake allows).
-// Bucketed pair walk (tp_walk_bucket.cu), the default for full traversals of
-// batches with 21 <= n <= 32: TRITPERM_BUCKET=0 selects the packed walk,
-// =2 the bucketed walk with unpacked pair tests.
+// Bucketed pair walk (tp_walk_bucket.cu), the default for 21 <= n <= 64 (full
+// traversals and the superblock-aligned middle of ranges): TRITPERM_BUCKET=0
+// selects the packed walk, =2 the bucketed walk with unpacked pair tests
+// (n <= 31).
 int bucket_mode() {
   const char* e = getenv("TRITPERM_BUCKET");  // read per call: tests switch it at run time
   return e ? atoi(e) : 1;
 }
 
-// Same size rule as the packed walk: the job must fill the GPU.
+// Same size rule as the packed walk: the job must fill the GPU
+// (B * 2^n >= 2^26; make_plan applies it to the region of a range).
 bool bucket_applies(int n, unsigned long long B) {
   const int m = bucket_mode();
-  // n = 32 only with the packed filter (its verify tests the padding-slot
+  // n >= 32 only with the packed filter (its verify tests the padding-slot
   // mask: there is no padding column); the unpacked pair tests need n <= 31
-  return n >= 21 && n <= (m == 2 ? 31 : 32) && B > 0 && (B << (n - 15)) >= 2048ull && m > 0;
+  return n >= 21 && n <= (m == 2 ? 31 : 64) && B > 0 && (n >= 26 || (B << (n - 15)) >= 2048ull) && m > 0;
 }
 
 int tc_mode() {
@@ -245,45 +248,73 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
                const RowRec* rows, unsigned long long* pm, Plan& pl) {
   pl = Plan();
   pl.nw = n <= 32 ? 1 : 2;
-  // Bucketed pair walk: items (matrix, piece, chunk) of L = 2^(n-14) / chunks
-  // B steps (superblocks of 16, at least 2 per item).
-  if (full && bucket_applies(n, B)) {
-    const int P = tp::bucket_pieces();
-    const bool packed = bucket_mode() != 2;  // 2: the unpacked pair tests
+  // Bucketed pair walk over the superblocks [s0, s1) the step range covers
+  // completely (superblock = 2^(14 + bv) reference steps); range heads and
+  // tails go to the generic walk.  Items (matrix, piece, chunk of nblk
+  // superblocks).
+  bool bucket_mid = false;
+  unsigned long long mid0 = 0, mid1 = 0;  // bucket region in 32-step units (ranges)
+  if (bucket_applies(n, B) && (full || lo < hi)) {
+    const bool packed = n > 31 || bucket_mode() != 2;  // 2: the unpacked pair tests
+    const int fix = tp::bucket_fix(n, packed);  // A side: rows 0..fix-1
+    const int P = tp::bucket_pieces(fix);
     const int bv = tp::bucket_v(packed);
-    const unsigned long long bsteps = 1ull << (n - tp::bucket_fix());
-    const unsigned long long want = 4ull * d.sm_count * d.bucket_blocks_per_sm * 4;
-    unsigned long long chunks = 1;
-    while (bsteps / (2 * chunks) >= (2ull << bv) && B * (unsigned long long)P * chunks < want) chunks *= 2;
+    const int sbl = fix + bv;  // log2 reference steps per superblock
+    unsigned long long s0 = 0, s1 = 0;
+    if (full) {
+      s1 = 1ull << (n - sbl);
+    } else {
+      const unsigned long long lo0 = lo == 1 ? 0 : lo;  // step 0 contributes 0
+      s0 = (lo0 >> sbl) + ((lo0 & ((1ull << sbl) - 1)) ? 1 : 0);
+      s1 = hi >> sbl;
+    }
+    // the region must fill the GPU: B * 2^(sbl) * (s1 - s0) >= 2^26
+    const bool big = s1 > s0 && (s1 - s0 >= (1ull << (26 - sbl)) || B * (s1 - s0) >= (1ull << (26 - sbl)));
+    const unsigned long long total = big ? s1 - s0 : 0;
+    // Items per warp: at least 4 (fill the grid); items longer than 1024
+    // superblocks are split further, up to ~128 per warp, so that uneven items
+    // (event-dense matrices in exact mode run ~4x longer) balance through the
+    // dynamic queue.  Short items (C2: one matrix's whole B side of 64
+    // superblocks) stay whole: their per-item setup is not free.
+    static const unsigned long long per_warp = [] {
+      const char* e = getenv("TRITPERM_BUCKET_ITEMS");  // tuning knob: the ~128 above
+      return (unsigned long long)(e && atoi(e) > 0 ? atoi(e) : 128);
+    }();
+    const unsigned long long warps = (unsigned long long)d.sm_count * d.bucket_blocks_per_sm * 4;
+    unsigned long long nblk = std::min<unsigned long long>(std::max<unsigned long long>(total, 1), 1ull << 16);
+    auto items_of = [&](unsigned long long nb) { return B * (unsigned long long)P * ((total + nb - 1) / nb); };
+    while (nblk > 1 && (items_of(nblk) < 4 * warps || (nblk > 1024 && items_of(nblk) < per_warp * warps)))
+      nblk = (nblk + 1) / 2;
+    const unsigned long long chunks = (total + nblk - 1) / nblk;
     const size_t need = (size_t)B * P * (1024 * sizeof(uint16_t) + sizeof(uint32_t));
     const size_t kBucketWsMax = (size_t)4 << 30;  // larger batches take the default walk
-    if (need <= kBucketWsMax && d.bucket_ws_size < need) {
+    if (big && need <= kBucketWsMax && d.bucket_ws_size < need) {
       cudaDeviceSynchronize();  // earlier launches may still read the old lists
       if (d.bucket_ws) cudaFree(d.bucket_ws);
       d.bucket_ws = nullptr;
       d.bucket_ws_size = 0;
       if (cudaMalloc(&d.bucket_ws, need) == cudaSuccess) d.bucket_ws_size = need;
     }
-    if (need <= kBucketWsMax && d.bucket_ws_size >= need) {
+    if (big && need <= kBucketWsMax && d.bucket_ws_size >= need) {
       pl.bucket = true;
       pl.bucket_packed = packed;
       pl.bucket_B = (long long)B;
+      pl.bucket_fix = fix;
       pl.bucket_list = static_cast<uint16_t*>(d.bucket_ws);
       pl.bucket_ptab = reinterpret_cast<uint32_t*>(pl.bucket_list + (size_t)B * P * 1024);
       tp::FastParams& f = pl.bkp.fp;
       f.rows = rows;
       f.pm = pm;
       f.queue = take_queue(d);
-      f.F0 = 0;
-      f.L = bsteps / chunks;
+      f.F0 = s0;
+      f.L = nblk << bv;
       f.chunks = chunks;
       f.items = B * (unsigned long long)P * chunks;
-      f.nblk = (uint32_t)(f.L >> bv);  // superblocks of 2^bv B steps
+      f.nblk = (uint32_t)nblk;  // superblocks of 2^bv B steps
       f.lognblk = 0;
-      while ((1u << f.lognblk) < f.nblk) f.lognblk++;
       f.n = n;
-      f.z0_init = zmask(n);
-      f.z1_init = 0;
+      f.z0_init = zmask(std::min(n, 32));
+      f.z1_init = zmask(n - 32);
       f.one = 1u;
       f.trace = nullptr;
       f.dense_ok = 1;
@@ -291,14 +322,18 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
       pl.bkp.list = pl.bucket_list;
       pl.bkp.ptab = pl.bucket_ptab;
       pl.bkp.tested = d.bucket_tested;
+      pl.bkp.s_end = s1;
       const unsigned long long ctas = (unsigned long long)d.sm_count * d.bucket_blocks_per_sm;
       pl.bucket_grid = (int)std::max<unsigned long long>(1, std::min(ctas, (f.items + 3) / 4));
-      return;
+      if (full) return;
+      bucket_mid = true;
+      mid0 = s0 << (sbl - 5);
+      mid1 = s1 << (sbl - 5);
     }
   }
   // Full traversals of n >= 18 (at least 8 tiles per matrix) go to the tensor
   // cores.  Tiles per item 2^t: as long as the grid still gets >= 8 items per CTA.
-  if (full && n >= 18 && B > 0 && tc_mode() != 0) {
+  if (!bucket_mid && full && n >= 18 && B > 0 && tc_mode() != 0) {
     const int tmax = n - 15;
     const unsigned long long want = 8ull * (unsigned long long)d.sm_count;
     int t = tmax;
@@ -352,7 +387,7 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
   const unsigned long long A0u = (A0 + (1ull << U) - 1) >> U, A1u = A1 >> U;
   const unsigned long long SBu = 1ull << V;
   unsigned long long F0 = 0, F1 = 0, L = 0;
-  if (n >= 5 + U + V + 1 && A0u < A1u) {
+  if (!bucket_mid && n >= 5 + U + V + 1 && A0u < A1u) {
     const int bps = d.fast_blocks_per_sm[pl.variant];
     const unsigned long long warps = (unsigned long long)d.sm_count * bps * tp::fast_warps(pl.variant);
     const unsigned long long want_items = warps * 32;  // dynamic queue: a few dozen per warp
@@ -372,6 +407,11 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
     }
   }
   unsigned long long g0a = a_lo, g0b = a_hi, g1a = 0, g1b = 0;  // generic regions (32-step units)
+  if (bucket_mid) {  // range head and tail around the bucket region
+    g0b = mid0;
+    g1a = mid1;
+    g1b = a_hi;
+  }
   if (L) {
     g0b = F0 << U;
     g1a = F1 << U;
@@ -426,11 +466,10 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
 // Enqueue the walk of plan `pl`; returns launches in *launches.
 int run_plan(const Plan& pl, cudaStream_t st, int* launches) {
   int nl = 0;
-  if (pl.bucket) {
-    TP_CUDA(tp::launch_bucket_group(pl.bkp.fp.rows, pl.bucket_B, pl.bkp.fp.n, pl.bucket_list, pl.bucket_ptab, st));
+  if (pl.bucket) {  // (ranges: plus the generic head and tail below)
+    TP_CUDA(tp::launch_bucket_group(pl.bkp.fp.rows, pl.bucket_B, pl.bkp.fp.n, pl.bucket_fix, pl.bucket_list, pl.bucket_ptab, st));
     TP_CUDA(tp::launch_walk_bucket(pl.bucket_grid, pl.bkp, pl.bucket_packed, st));
-    if (launches) *launches += 2;
-    return TP_OK;
+    nl += 2;
   }
   if (pl.tc) {
     TP_CUDA(tp::launch_walk_tc(pl.tc_grid, pl.tcp, st));

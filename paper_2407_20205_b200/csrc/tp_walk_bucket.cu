@@ -29,21 +29,24 @@ namespace tp {
 
 namespace {
 
-constexpr int kBucketFix = 14;                    // A side: rows 0..13
-constexpr int kBucketPieces = (1 << (kBucketFix - 10)) + 9;  // 16 full pieces + one partial per bucket
+// A side: rows 0..FIX-1, FIX = 13 or 14 (bucket_fix); pieces per matrix:
+// 2^(FIX-10) full ones plus one partial per bucket
+__host__ __device__ constexpr int pieces_of(int fix) { return (1 << (fix - 10)) + 9; }
 constexpr uint16_t kBucketDummy = 0xFFFFu;
 
 // ----------------------------------------------------------------- grouping
 // One CTA per matrix: key trits of all 2^14 A subsets from two 128-entry
 // half tables, a counting sort into the 9 buckets, pieces of 1024.
-__global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n, uint16_t* list, uint32_t* ptab) {
+__global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n, int fix, uint16_t* list,
+                                                      uint32_t* ptab) {
+  const int kBucketPieces = pieces_of(fix);
   __shared__ uint8_t tlo[128], thi[128];  // key pattern 3 * x1 + x2 of the low / high 7 rows' subsets
   __shared__ uint32_t cnt[9], pos[9];
   __shared__ uint32_t pstart[9];
   const RowRec* R = rows + (size_t)blockIdx.x * 64;
   uint16_t* L = list + (size_t)blockIdx.x * kBucketPieces * 1024;
   uint32_t* P = ptab + (size_t)blockIdx.x * kBucketPieces;
-  const int k1 = n - 1, k2 = n - 2;
+  const int k1 = (n < 32 ? n : 32) - 1, k2 = k1 - 1;  // key columns (primary word for n > 32)
   auto trit = [&](int r, int k) -> uint32_t {
     const uint32_t m = (R[r].m[0] >> k) & 1u, s = (R[r].s[0] >> k) & 1u;
     return m ? (s ? 2u : 1u) : 0u;
@@ -67,7 +70,7 @@ __global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n,
     const uint32_t x1 = (a / 3 + b / 3) % 3, x2 = (a % 3 + b % 3) % 3;
     return 3 * x1 + x2;
   };
-  for (uint32_t s = threadIdx.x; s < (1u << kBucketFix); s += blockDim.x) atomicAdd(&cnt[pat(s)], 1u);
+  for (uint32_t s = threadIdx.x; s < (1u << fix); s += blockDim.x) atomicAdd(&cnt[pat(s)], 1u);
   __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t piece = 0;
@@ -84,7 +87,7 @@ __global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n,
     for (uint32_t q = piece; q < (uint32_t)kBucketPieces; ++q) P[q] = 0;  // unused pieces: count 0
   }
   __syncthreads();
-  for (uint32_t s = threadIdx.x; s < (1u << kBucketFix); s += blockDim.x) {
+  for (uint32_t s = threadIdx.x; s < (1u << fix); s += blockDim.x) {
     const uint32_t g = pat(s);
     L[atomicAdd(&pos[g], 1u)] = (uint16_t)s;
   }
@@ -159,45 +162,117 @@ static __device__ __noinline__ unsigned long long bucket_exact_packed(const uint
   return (unsigned long long)bev | ((unsigned long long)bodd << 32);
 }
 
+// n > 32: the secondary word (columns 32..n-1) of A subset s, from scratch.
+__device__ __forceinline__ void a_word1(const RowRec* R, uint32_t s, uint32_t z1i, uint32_t& z, uint32_t& g) {
+  z = z1i;
+  g = 0;
+#pragma unroll 1
+  for (uint32_t x = s; x; x &= x - 1) {
+    const int t = __ffs(x) - 1;
+    sub_word(z, g, R[t].m[1], R[t].a[1]);
+  }
+}
+
+// n > 32, a pair whose 32 primary columns are all nonzero: 1 | parity of the
+// secondary sign word << 1 if the secondary columns are nonzero too, else 0.
+static __device__ __noinline__ uint32_t bucket_wide_term(const RowRec* R, uint32_t s, uint2 h1, uint32_t z1i) {
+  uint32_t za, ga, d, zp;
+  a_word1(R, s, z1i, za, ga);
+  TP_LOP3(d, za, ga, h1.y, 0x06);
+  TP_LOP3(zp, d, za, h1.x, 0x09);
+  if (zp != 0) return 0u;
+  return 1u | ((__popc((d ^ pair_g2(h1.x, h1.y)) & z1i) & 1u) << 1);
+}
+
+// n > 32: exact evaluation of the steps in `mask` against this lane's real
+// slots, both words (dense mode, list overflow).  Slot-major, so each slot's
+// secondary word is built once.  Returns ev | odd << 32.
+static __device__ __noinline__ unsigned long long bucket_exact_wide(const uint4 (*A2)[32], const uint4* H,
+                                                                    const uint2* H1, const RowRec* R,
+                                                                    const uint16_t* Lp, uint32_t mask, uint32_t lane,
+                                                                    uint32_t spm, uint32_t vmask, uint32_t z1i) {
+  uint32_t ev = 0, odd = 0;
+#pragma unroll 1
+  for (int k = 0; k < 32; ++k) {
+    if (!((vmask >> k) & 1u)) continue;
+    uint32_t za1, ga1;
+    a_word1(R, Lp[32 * k + lane], z1i, za1, ga1);
+    const uint4 a4 = A2[k & 15][lane];
+    const uint32_t za = k < 16 ? a4.x : a4.z, ga = k < 16 ? a4.y : a4.w;
+    const uint32_t kp = (spm >> k) & 1u;
+#pragma unroll 1
+    for (uint32_t m = mask; m; m &= m - 1) {
+      const uint32_t j = __ffs(m) - 1;
+      const uint4 h = H[j];
+      uint32_t d, zp;
+      TP_LOP3(d, za, ga, h.y, 0x06);
+      TP_LOP3(zp, d, za, h.x, 0x09);
+      if (zp == 0) {
+        const uint2 h1 = H1[j];
+        uint32_t d1, zp1;
+        TP_LOP3(d1, za1, ga1, h1.y, 0x06);
+        TP_LOP3(zp1, d1, za1, h1.x, 0x09);
+        if (zp1 == 0) {
+          ev += 1;
+          odd += (__popc(d ^ pair_g2(h.x, h.y)) + __popc((d1 ^ pair_g2(h1.x, h1.y)) & z1i) + j + kp) & 1u;
+        }
+      }
+    }
+  }
+  return (unsigned long long)ev | ((unsigned long long)odd << 32);
+}
+
 }  // namespace
 
-template <int V, int WARPS, bool PACKED>
+template <int V, int WARPS, bool PACKED, bool WIDE, int FIX>
 __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) {
   constexpr int KB = 5;
   constexpr int K = 1 << KB;
-  constexpr int FIX = kBucketFix;
+  constexpr int kBucketPieces = pieces_of(FIX);
   constexpr int SB = 1 << V;
   const FastParams& p = bp.fp;
-  __shared__ RowRec Rs[WARPS][32];
+  static_assert(PACKED || !WIDE, "n > 32 needs the packed filter");
+  __shared__ RowRec Rs[WARPS][WIDE ? 64 : 32];
   __shared__ uint4 Hs[WARPS][SB];
+  __shared__ uint2 H1s[WARPS][WIDE ? SB : 1];  // n > 32: secondary words (z, u) of the superblock's B states
   __shared__ uint2 As[WARPS][K][32];  // full A words; packed: [w][lane] pairs (slot w, slot w + 16) as uint4
-  constexpr int ECAP = PACKED ? 6 : 1;  // per-lane pass-list capacity (overflow: exact superblock)
+  constexpr int ECAP = PACKED ? (WIDE ? 5 : 6) : 1;  // (48 KB of static shared memory)  // per-lane pass-list capacity (overflow: exact superblock)
   __shared__ uint2 Es[WARPS][ECAP][32];   // per-lane filter passes: (mask, steps)
   const uint32_t lane = threadIdx.x & 31u;
   uint2 (*E)[32] = Es[threadIdx.x >> 5];
   const uint32_t cneg = 0xfffeffffu * p.one;  // -0x00010001, runtime so ptxas keeps the IMAD
   RowRec* R = Rs[threadIdx.x >> 5];
   uint4* H = Hs[threadIdx.x >> 5];
+  uint2* H1 = H1s[threadIdx.x >> 5];
   uint2 (*A)[32] = As[threadIdx.x >> 5];
   uint4 (*A2)[32] = reinterpret_cast<uint4 (*)[32]>(As[threadIdx.x >> 5]);
   const uint32_t one = p.one;
   const uint32_t colmask = p.z0_init;  // real columns (n <= 31: bit 31 is padding)
-  const int k1 = p.n - 1, k2 = p.n - 2;
+  const uint32_t colmask1 = p.z1_init;  // n > 32: real columns of the secondary word
+  const int k1 = (WIDE ? 32 : p.n) - 1, k2 = k1 - 1;
   unsigned long long n_items = 0;
 
   for (;;) {
     const unsigned long long item = next_item(p, lane, n_items, blockIdx.x * WARPS + (threadIdx.x >> 5));
     if (item >= p.items) break;
     ++n_items;
-    const unsigned long long per_b = (unsigned long long)kBucketPieces * p.chunks;
-    const unsigned long long b = item / per_b;
-    const unsigned long long rem = item - b * per_b;
-    const uint32_t q = (uint32_t)(rem / p.chunks);
-    const unsigned long long A0 = (rem - (unsigned long long)q * p.chunks) * p.L;
+    // item = (piece * chunks + chunk) * B + matrix: consecutive items go to
+    // different matrices, so the slow items of event-dense matrices spread
+    // over the whole launch instead of forming its tail (and the unused
+    // high pieces come last)
+    const unsigned long long nmat = p.items / ((unsigned long long)kBucketPieces * p.chunks);
+    const unsigned long long rest = item / nmat;
+    const unsigned long long b = item - rest * nmat;
+    const uint32_t q = (uint32_t)(rest / p.chunks);
+    const unsigned long long c = rest - (unsigned long long)q * p.chunks;
+    // superblocks [sb0, sb0 + nsb) of the B side (global indices: the
+    // region [F0, s_end) need not be aligned to the item length)
+    const unsigned long long sb0 = p.F0 + c * p.nblk;
+    const uint32_t nsb = (uint32_t)min((unsigned long long)p.nblk, bp.s_end - sb0);
+    const unsigned long long A0 = sb0 << V;
     const uint32_t pt = bp.ptab[b * kBucketPieces + q];
     if ((pt >> 16) == 0) continue;  // unused piece
     const uint32_t grp = pt & 0xFFFFu;
-    const unsigned long long B0 = A0 >> V;
     __syncwarp();
     load_rows(R, p.rows + b * 64, lane, p.n);
     __syncwarp();
@@ -210,8 +285,8 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
     uint32_t Zp[PACKED ? K / 2 : 1], Gp[PACKED ? K / 2 : 1];
     uint32_t spm = 0;  // bit k: parity of slot k's subset
     uint32_t vmask = 0;  // bit k: slot k holds a real A subset (not padding)
+    const uint16_t* Lp = bp.list + (b * kBucketPieces + q) * 1024;
     {
-      const uint16_t* Lp = bp.list + (b * kBucketPieces + q) * 1024;
       auto slot = [&](int k, uint32_t& z, uint32_t& g) {
         const uint32_t s = Lp[32 * k + lane];
         z = colmask;
@@ -258,20 +333,31 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
     const uint32_t F2 = (f1 == 2 ? 1u << k1 : 0u) | (f2 == 2 ? 1u << k2 : 0u);
     // B side: v2 for S2 = gray(A0) on rows >= FIX (low bits empty)
     uint32_t z2, u2;
+    uint32_t z2w = 0, u2w = 0;  // n > 32: secondary word of the entry state
     {
-      uint32_t z = colmask, g = 0;
+      uint32_t z = colmask, g = 0, zw = colmask1, gw = 0;
       const unsigned long long hs = A0 ^ (A0 >> 1);
       for (int r = FIX; r < p.n; ++r)
-        if ((hs >> (r - FIX)) & 1ull) sub_word(z, g, R[r].m[0], R[r].a[0]);
+        if ((hs >> (r - FIX)) & 1ull) {
+          sub_word(z, g, R[r].m[0], R[r].a[0]);
+          if (WIDE) sub_word(zw, gw, R[r].m[1], R[r].a[1]);
+        }
       z2 = z;
       u2 = pair_u2(z, g);
+      z2w = zw;
+      u2w = pair_u2(zw, gw);
     }
     uint32_t ev = 0, odd = 0;
     uint32_t tested_steps = 0;  // compatible steps of this item (x 1024 pairs)
     // exact evaluation of every pair of the superblock from H (replays, dense mode)
     // (only the steps in `mask`: incompatible steps have no full term)
     auto exact_block = [&](uint32_t& bev, uint32_t& bodd, uint32_t mask) {
-      if constexpr (PACKED) {
+      if constexpr (WIDE) {
+        const unsigned long long r = bucket_exact_wide(A2, H, H1, R, Lp, mask, lane, spm, vmask, colmask1);
+        bev = (uint32_t)r;
+        bodd = (uint32_t)(r >> 32);
+        return;
+      } else if constexpr (PACKED) {
         const unsigned long long r = bucket_exact_packed(A2, H, mask, lane, spm, vmask, colmask, p.n, one);
         bev = (uint32_t)r;
         bodd = (uint32_t)(r >> 32);
@@ -295,25 +381,31 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
       }
     };
     bool dense = false;
-    for (uint32_t kb = 0; kb < p.nblk; ++kb) {
+    for (uint32_t kb = 0; kb < nsb; ++kb) {
       // the B states of the superblock, one per lane (step j = lane mod SB),
-      // as in the pair walk
+      // as in the pair walk; the top row's direction follows the parity of
+      // the global superblock index
+      const bool godd = ((sb0 + kb) & 1ull) != 0;
       uint32_t zj = z2, uj = u2;
+      uint32_t zjw = z2w, ujw = u2w;
       {
         const uint32_t j = lane & (SB - 1), gj = j ^ (j >> 1);
 #pragma unroll
         for (int r = 0; r < V; ++r) {
           if ((gj >> r) & 1u) {
-            const bool lv = (r == V - 1) && (kb & 1u);
+            const bool lv = (r == V - 1) && godd;
             const RowRec& row = R[FIX + r];
             sub_word_u(zj, uj, row.m[0], lv ? row.s[0] : row.a[0], lv ? row.a[0] : row.s[0]);
+            if (WIDE) sub_word_u(zjw, ujw, row.m[1], lv ? row.s[1] : row.a[1], lv ? row.a[1] : row.s[1]);
           }
         }
       }
       __syncwarp();
-      if (lane < (uint32_t)SB)
+      if (lane < (uint32_t)SB) {
         H[lane] = PACKED ? make_uint4(zj, uj, __byte_perm(zj, zj, 0x1010), __byte_perm(uj, uj, 0x1010))
                          : make_uint4(zj, uj, 0u, 0u);
+        if (WIDE) H1[lane] = make_uint2(zjw, ujw);
+      }
       // compatible steps: no key column of y equals the forbidden trit
       // (y = 0 <=> z; y = 2 <=> ~z & ~u; y = 1 <=> ~z & u)
       const uint32_t match = (zj & F0) | (~zj & ~uj & F2) | (~zj & uj & F1);
@@ -387,8 +479,15 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
                   TP_LOP3(d, a.x, a.y, h.y, 0x06);
                   TP_LOP3(zp, d, a.x, h.x, 0x09);
                   if (zp == 0 && ((vmask >> k) & 1u)) {
+                    uint32_t par = 0;
+                    if constexpr (WIDE) {
+                      // the primary columns are nonzero: test the secondary ones
+                      const uint32_t r = bucket_wide_term(R, Lp[32 * k + lane], H1[j], colmask1);
+                      if (!r) continue;
+                      par = r >> 1;
+                    }
                     bev += 1;
-                    bodd += (__popc((d ^ gh) & colmask) + j + ((spm >> k) & 1u)) & 1u;
+                    bodd += (__popc((d ^ gh) & colmask) + par + j + ((spm >> k) & 1u)) & 1u;
                   }
                 }
               }
@@ -473,12 +572,21 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
       // (z2, u2) = step SB-1 of this superblock, then the entry step of kb + 1
       z2 = __shfl_sync(FULL, zj, SB - 1);
       u2 = __shfl_sync(FULL, uj, SB - 1);
-      if (kb + 1 < p.nblk) {
-        const uint32_t u = kb + 1;
-        const int t = __ffs(u) - 1;
+      if (WIDE) {
+        __syncwarp();
+        const uint2 e = H1[SB - 1];
+        z2w = e.x;
+        u2w = e.y;
+      }
+      if (kb + 1 < nsb) {
+        // entry of global superblock G flips row FIX + V + tz(G); it leaves
+        // iff bit tz(G) + 1 of G is set
+        const unsigned long long G = sb0 + kb + 1;
+        const int t = tz64(G);
         const RowRec& row = R[FIX + V + t];
-        const bool lv = entry_leave(u, t, p, B0);
+        const bool lv = ((G >> (t + 1)) & 1ull) != 0;
         sub_word_u(z2, u2, row.m[0], lv ? row.s[0] : row.a[0], lv ? row.a[0] : row.s[0]);
+        if (WIDE) sub_word_u(z2w, u2w, row.m[1], lv ? row.s[1] : row.a[1], lv ? row.a[1] : row.s[1]);
       }
     }
     warp_flush(p.pm + 2 * b, ev - odd, odd, lane);
@@ -487,25 +595,29 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
   queue_done(p, lane);
 }
 
-int bucket_pieces() { return kBucketPieces; }
+int bucket_pieces(int fix) { return pieces_of(fix); }
 int bucket_v(bool packed) { return packed ? 5 : 4; }  // log2 superblock length
-int bucket_fix() { return kBucketFix; }
+// 13 rows when the B side is short (n < 27: items are one matrix's whole B
+// side, and a 13-row A side doubles its length); 14 otherwise
+int bucket_fix(int n, bool packed) { return (packed && n < 27) ? 13 : 14; }
 
-cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, uint16_t* list, uint32_t* ptab,
+cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, int fix, uint16_t* list, uint32_t* ptab,
                                 cudaStream_t st) {
-  k_bucket_group<<<(unsigned)B, 256, 0, st>>>(rows, n, list, ptab);
+  k_bucket_group<<<(unsigned)B, 256, 0, st>>>(rows, n, fix, list, ptab);
   return cudaGetLastError();
 }
 
 cudaError_t launch_walk_bucket(int grid, const BucketParams& bp, bool packed, cudaStream_t st) {
-  if (packed) k_walk_bucket<5, 4, true><<<grid, 128, 0, st>>>(bp);
-  else k_walk_bucket<4, 4, false><<<grid, 128, 0, st>>>(bp);
+  if (bp.fp.n > 32) k_walk_bucket<5, 4, true, true, 14><<<grid, 128, 0, st>>>(bp);
+  else if (!packed) k_walk_bucket<4, 4, false, false, 14><<<grid, 128, 0, st>>>(bp);
+  else if (bucket_fix(bp.fp.n, true) == 13) k_walk_bucket<5, 4, true, false, 13><<<grid, 128, 0, st>>>(bp);
+  else k_walk_bucket<5, 4, true, false, 14><<<grid, 128, 0, st>>>(bp);
   return cudaGetLastError();
 }
 
 const void* walk_bucket_symbol(bool packed) {
-  return packed ? reinterpret_cast<const void*>(&k_walk_bucket<5, 4, true>)
-                : reinterpret_cast<const void*>(&k_walk_bucket<4, 4, false>);
+  return packed ? reinterpret_cast<const void*>(&k_walk_bucket<5, 4, true, false, 14>)
+                : reinterpret_cast<const void*>(&k_walk_bucket<4, 4, false, false, 14>);
 }
 
 }  // namespace tp

@@ -511,3 +511,45 @@ def test_bucketed_pair_walk_exact(gpu, oracle, monkeypatch):
         if n <= 21:
             mags, sgns = oracle.planes_from_classes(e[0])
             assert part[0] == oracle.chunk_sum(mags, sgns, n, 1, 1 << n), n
+
+
+def test_bucketed_walk_ranges_and_wide(gpu, oracle, monkeypatch):
+    """The bucketed walk on single matrices: n > 32 (primary-word filter, the
+    secondary columns checked per pass) and step ranges whose superblock-
+    aligned middle it takes while the generic walk takes the unaligned head
+    and tail.  Uniform, sparse and all-ones matrices against the oracle and
+    the packed walk (TRITPERM_BUCKET=0); the kernel's tested-pair counter
+    proves the bucketed walk served the call."""
+    from paper_2407_20205_b200 import _kernels
+
+    r = random.Random(77)
+    cases = []
+    for n in (28, 33, 36, 41, 50):
+        cases.append((_rand_matrix(r, n), r.randrange(1, 1 << (n - 3))))
+    for n in (34, 39):
+        sp = np.array([[r.choice((1, 2)) if r.random() < 0.3 else 0 for _ in range(n)] for _ in range(n)], np.uint8)
+        cases.append((sp, r.randrange(1, 1 << 30)))
+    cases.append((np.ones((35, 35), np.uint8), 12345))
+    for a, lo in cases:
+        n = a.shape[0]
+        hi = lo + (1 << 27) + r.randrange(0, 1 << 20)
+        mags, sgns = oracle.planes_from_classes(a)
+        want = oracle.chunk_sum_mt(mags, sgns, n, lo, hi, 8)
+        m = gpu.MatrixF3(centred(a))
+        monkeypatch.setenv("TRITPERM_BUCKET", "0")
+        assert gpu.perm_chunk(m, lo, hi).partial_sum == want, (n, lo, "packed")
+        monkeypatch.setenv("TRITPERM_BUCKET", "1")
+        _kernels.walk_tested(0)
+        assert gpu.perm_chunk(m, lo, hi).partial_sum == want, (n, lo, "bucket")
+        assert _kernels.walk_tested(0) > 0, (n, "bucketed walk not used")
+    # aligned full traversal above 32 columns, split at arbitrary edges
+    a = _rand_matrix(r, 34)
+    mags, sgns = oracle.planes_from_classes(a)
+    m = gpu.MatrixF3(centred(a))
+    full = gpu.perm_chunk(m, 1, 1 << 34).partial_sum
+    monkeypatch.setenv("TRITPERM_BUCKET", "0")
+    assert gpu.perm_chunk(m, 1, 1 << 34).partial_sum == full
+    monkeypatch.setenv("TRITPERM_BUCKET", "1")
+    cut = sorted(r.randrange(1, 1 << 34) for _ in range(3))
+    edges = [1] + cut + [1 << 34]
+    assert sum(gpu.perm_chunk(m, x, y).partial_sum for x, y in zip(edges, edges[1:])) == full
