@@ -100,16 +100,22 @@ cudaError_t launch_walk_tc(int grid, const TcParams& p, cudaStream_t st);
 // s_end)) (superblocks of 2^bucket_v B steps, a B step = 2^14 reference
 // steps); list/ptab come from launch_bucket_group.
 struct BucketParams {
-  FastParams fp;                // items = B * bucket_pieces(fix) * chunks; F0, nblk in superblocks
-  const uint16_t* list;         // [B][pieces][1024] A subsets (0xFFFF = dummy slot)
+  FastParams fp;                // items = B * bucket_pieces(cfg) * chunks; F0, nblk in superblocks
+  const void* list;             // [B][pieces][1024] A subsets, uint16 or uint32 (all ones = dummy slot)
   const uint32_t* ptab;         // [B][pieces] bucket | valid count << 16 (count 0 = unused)
   unsigned long long* tested;   // += pairs actually tested (compatible steps x 1024), or nullptr
   unsigned long long s_end;     // end of the superblock region
+  int fix, keys;                // bucket configuration (bucket_cfg)
 };
-int bucket_pieces(int fix);
-int bucket_fix(int n, bool packed);
+struct BucketCfg {
+  int fix;   // A side: rows 0..fix-1
+  int keys;  // key columns: 3^keys buckets
+};
+BucketCfg bucket_cfg(int n, bool packed);
+int bucket_pieces(BucketCfg c);
+size_t bucket_list_elem(BucketCfg c);
 int bucket_v(bool packed);
-cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, int fix, uint16_t* list, uint32_t* ptab,
+cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, BucketCfg c, void* list, uint32_t* ptab,
                                 cudaStream_t st);
 cudaError_t launch_walk_bucket(int grid, const BucketParams& bp, bool packed, cudaStream_t st);
 const void* walk_bucket_symbol(bool packed);

@@ -168,8 +168,8 @@ struct Plan {
   int bucket_grid = 0;
   long long bucket_B = 0;
   bool bucket_packed = true;
-  int bucket_fix = 14;
-  uint16_t* bucket_list = nullptr;
+  tp::BucketCfg bucket_cfg{14, 2};
+  void* bucket_list = nullptr;
   uint32_t* bucket_ptab = nullptr;
   bool tc = false;  // tensor-core pair test covers the whole plan
   tp::TcParams tcp{};
@@ -256,8 +256,9 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
   unsigned long long mid0 = 0, mid1 = 0;  // bucket region in 32-step units (ranges)
   if (bucket_applies(n, B) && (full || lo < hi)) {
     const bool packed = n > 31 || bucket_mode() != 2;  // 2: the unpacked pair tests
-    const int fix = tp::bucket_fix(n, packed);  // A side: rows 0..fix-1
-    const int P = tp::bucket_pieces(fix);
+    const tp::BucketCfg cfg = tp::bucket_cfg(n, packed);
+    const int fix = cfg.fix;  // A side: rows 0..fix-1
+    const int P = tp::bucket_pieces(cfg);
     const int bv = tp::bucket_v(packed);
     const int sbl = fix + bv;  // log2 reference steps per superblock
     unsigned long long s0 = 0, s1 = 0;
@@ -286,7 +287,7 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
     while (nblk > 1 && (items_of(nblk) < 4 * warps || (nblk > 1024 && items_of(nblk) < per_warp * warps)))
       nblk = (nblk + 1) / 2;
     const unsigned long long chunks = (total + nblk - 1) / nblk;
-    const size_t need = (size_t)B * P * (1024 * sizeof(uint16_t) + sizeof(uint32_t));
+    const size_t need = (size_t)B * P * (1024 * tp::bucket_list_elem(cfg) + sizeof(uint32_t));
     const size_t kBucketWsMax = (size_t)4 << 30;  // larger batches take the default walk
     if (big && need <= kBucketWsMax && d.bucket_ws_size < need) {
       cudaDeviceSynchronize();  // earlier launches may still read the old lists
@@ -299,9 +300,10 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
       pl.bucket = true;
       pl.bucket_packed = packed;
       pl.bucket_B = (long long)B;
-      pl.bucket_fix = fix;
-      pl.bucket_list = static_cast<uint16_t*>(d.bucket_ws);
-      pl.bucket_ptab = reinterpret_cast<uint32_t*>(pl.bucket_list + (size_t)B * P * 1024);
+      pl.bucket_cfg = cfg;
+      pl.bucket_list = d.bucket_ws;
+      pl.bucket_ptab = reinterpret_cast<uint32_t*>(static_cast<char*>(d.bucket_ws) +
+                                                   (size_t)B * P * 1024 * tp::bucket_list_elem(cfg));
       tp::FastParams& f = pl.bkp.fp;
       f.rows = rows;
       f.pm = pm;
@@ -320,6 +322,8 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
       f.dense_ok = 1;
       f.static_items = 0;
       pl.bkp.list = pl.bucket_list;
+      pl.bkp.fix = cfg.fix;
+      pl.bkp.keys = cfg.keys;
       pl.bkp.ptab = pl.bucket_ptab;
       pl.bkp.tested = d.bucket_tested;
       pl.bkp.s_end = s1;
@@ -467,7 +471,7 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
 int run_plan(const Plan& pl, cudaStream_t st, int* launches) {
   int nl = 0;
   if (pl.bucket) {  // (ranges: plus the generic head and tail below)
-    TP_CUDA(tp::launch_bucket_group(pl.bkp.fp.rows, pl.bucket_B, pl.bkp.fp.n, pl.bucket_fix, pl.bucket_list, pl.bucket_ptab, st));
+    TP_CUDA(tp::launch_bucket_group(pl.bkp.fp.rows, pl.bucket_B, pl.bkp.fp.n, pl.bucket_cfg, pl.bucket_list, pl.bucket_ptab, st));
     TP_CUDA(tp::launch_walk_bucket(pl.bucket_grid, pl.bkp, pl.bucket_packed, st));
     nl += 2;
   }

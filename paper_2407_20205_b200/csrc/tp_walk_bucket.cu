@@ -23,78 +23,91 @@
 // terms are skipped, so raw partials equal chunk_sum (src/_kernels.py:90-128)
 // bit for bit.  Dummy slots carry a -1 in padding column 31 (the B side has
 // +1 there), so their sums always have a zero column and never count.
+#include <type_traits>
+
 #include "tp_walk_common.cuh"
 
 namespace tp {
 
 namespace {
 
-// A side: rows 0..FIX-1, FIX = 13 or 14 (bucket_fix); pieces per matrix:
-// 2^(FIX-10) full ones plus one partial per bucket
-__host__ __device__ constexpr int pieces_of(int fix) { return (1 << (fix - 10)) + 9; }
-constexpr uint16_t kBucketDummy = 0xFFFFu;
+// Bucket configurations (bucket_cfg): A side = rows 0..FIX-1, sorted by the
+// trits of KEYS key columns into 3^KEYS buckets; pieces per matrix:
+// 2^(FIX-10) full ones plus one partial per bucket.  Lists of FIX > 15 hold
+// uint32 subsets (0xFFFF is a real subset of 16 rows).
+__host__ __device__ constexpr int nbuckets(int keys) { return keys == 2 ? 9 : 27; }
+__host__ __device__ constexpr int pieces_of(int fix, int keys) { return (1 << (fix - 10)) + nbuckets(keys); }
+template <int FIX>
+using list_t = typename std::conditional<(FIX > 15), uint32_t, uint16_t>::type;
 
 // ----------------------------------------------------------------- grouping
-// One CTA per matrix: key trits of all 2^14 A subsets from two 128-entry
-// half tables, a counting sort into the 9 buckets, pieces of 1024.
-__global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n, int fix, uint16_t* list,
-                                                      uint32_t* ptab) {
-  const int kBucketPieces = pieces_of(fix);
-  __shared__ uint8_t tlo[128], thi[128];  // key pattern 3 * x1 + x2 of the low / high 7 rows' subsets
-  __shared__ uint32_t cnt[9], pos[9];
-  __shared__ uint32_t pstart[9];
+// One CTA per matrix: key digits of all 2^FIX A subsets from two half
+// tables (the low / high rows' subsets) and a digit-wise sum table, a
+// counting sort into the buckets (per-warp counters), pieces of 1024.
+template <int FIX, int KEYS>
+__global__ void __launch_bounds__(512) k_bucket_group(const RowRec* rows, int n, list_t<FIX>* list, uint32_t* ptab) {
+  using LT = list_t<FIX>;
+  constexpr int NB = nbuckets(KEYS), P = pieces_of(FIX, KEYS);
+  constexpr int TB = (FIX + 1) / 2, NW = 16;
+  __shared__ uint8_t tab[2][1 << TB];  // bucket digits of the low / high rows' subsets
+  __shared__ uint8_t comb[NB][NB];     // digit-wise sum mod 3
+  __shared__ uint32_t cw[NW][NB];      // per-warp counts, then scatter positions
+  __shared__ uint32_t cnt[NB], pstart[NB], pos[NB];
   const RowRec* R = rows + (size_t)blockIdx.x * 64;
-  uint16_t* L = list + (size_t)blockIdx.x * kBucketPieces * 1024;
-  uint32_t* P = ptab + (size_t)blockIdx.x * kBucketPieces;
-  const int k1 = (n < 32 ? n : 32) - 1, k2 = k1 - 1;  // key columns (primary word for n > 32)
+  LT* L = list + (size_t)blockIdx.x * P * 1024;
+  uint32_t* Pt = ptab + (size_t)blockIdx.x * P;
+  const int k1 = (n < 32 ? n : 32) - 1;  // key columns k1, k1-1 (, k1-2): primary word for n > 32
+  const uint32_t warp = threadIdx.x >> 5;
   auto trit = [&](int r, int k) -> uint32_t {
     const uint32_t m = (R[r].m[0] >> k) & 1u, s = (R[r].s[0] >> k) & 1u;
     return m ? (s ? 2u : 1u) : 0u;
   };
-  if (threadIdx.x < 256) {
-    const uint32_t half = threadIdx.x >> 7, sub = threadIdx.x & 127u;
-    uint32_t x1 = 0, x2 = 0;
-    for (int b = 0; b < 7; ++b)
-      if ((sub >> b) & 1u) {
-        x1 += trit(7 * half + b, k1);
-        x2 += trit(7 * half + b, k2);
-      }
-    const uint8_t v = (uint8_t)(3 * (x1 % 3) + (x2 % 3));
-    if (half) thi[sub] = v;
-    else tlo[sub] = v;
-  }
-  if (threadIdx.x < 9) cnt[threadIdx.x] = 0;
-  __syncthreads();
-  auto pat = [&](uint32_t s) -> uint32_t {
-    const uint32_t a = tlo[s & 127u], b = thi[s >> 7];
-    const uint32_t x1 = (a / 3 + b / 3) % 3, x2 = (a % 3 + b % 3) % 3;
-    return 3 * x1 + x2;
+  auto enc = [](uint32_t d0, uint32_t d1, uint32_t d2) -> uint32_t {
+    return KEYS == 2 ? 3 * (d0 % 3) + d1 % 3 : 9 * (d0 % 3) + 3 * (d1 % 3) + d2 % 3;
   };
-  for (uint32_t s = threadIdx.x; s < (1u << fix); s += blockDim.x) atomicAdd(&cnt[pat(s)], 1u);
+  for (uint32_t e = threadIdx.x; e < (2u << TB); e += blockDim.x) {
+    const uint32_t half = e >> TB, sub = e & ((1u << TB) - 1u);
+    uint32_t x[3] = {0, 0, 0};
+    for (int bt = 0; bt < TB; ++bt) {
+      const int r = TB * (int)half + bt;
+      if (r < FIX && ((sub >> bt) & 1u))
+        for (int i = 0; i < KEYS; ++i) x[i] += trit(r, k1 - i);
+    }
+    tab[half][sub] = (uint8_t)enc(x[0], x[1], x[2]);
+  }
+  for (uint32_t e = threadIdx.x; e < (uint32_t)(NB * NB); e += blockDim.x) {
+    const uint32_t a = e / NB, c = e % NB;
+    comb[a][c] = KEYS == 2 ? (uint8_t)enc(a / 3 + c / 3, a + c, 0)
+                           : (uint8_t)enc(a / 9 + c / 9, a / 3 + c / 3, a + c);
+  }
+  for (uint32_t e = threadIdx.x; e < (uint32_t)(NW * NB); e += blockDim.x) cw[e / NB][e % NB] = 0;
+  __syncthreads();
+  auto pat = [&](uint32_t s) -> uint32_t { return comb[tab[0][s & ((1u << TB) - 1u)]][tab[1][s >> TB]]; };
+  for (uint32_t s = threadIdx.x; s < (1u << FIX); s += blockDim.x) atomicAdd(&cw[warp][pat(s)], 1u);
   __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t piece = 0;
-    for (int g = 0; g < 9; ++g) {
+    for (int g = 0; g < NB; ++g) {
+      uint32_t c = 0;
+      for (int w = 0; w < NW; ++w) c += cw[w][g];
+      cnt[g] = c;
       pstart[g] = piece;
       pos[g] = piece * 1024u;
-      const uint32_t np = (cnt[g] + 1023u) / 1024u;
-      for (uint32_t q = 0; q < np; ++q) {
-        const uint32_t c = min(1024u, cnt[g] - 1024u * q);
-        P[piece + q] = (uint32_t)g | (c << 16);
-      }
+      const uint32_t np = (c + 1023u) / 1024u;
+      for (uint32_t q = 0; q < np; ++q) Pt[piece + q] = (uint32_t)g | (min(1024u, c - 1024u * q) << 16);
       piece += np;
     }
-    for (uint32_t q = piece; q < (uint32_t)kBucketPieces; ++q) P[q] = 0;  // unused pieces: count 0
+    for (uint32_t q = piece; q < (uint32_t)P; ++q) Pt[q] = 0;  // unused pieces: count 0
   }
   __syncthreads();
-  for (uint32_t s = threadIdx.x; s < (1u << fix); s += blockDim.x) {
-    const uint32_t g = pat(s);
-    L[atomicAdd(&pos[g], 1u)] = (uint16_t)s;
-  }
+  // scatter in arrival order (one counter per bucket): a lane's slots are
+  // then spread over the whole subset range, which keeps filter passes from
+  // clustering in one lane (per-warp ranges measured 4 % slower on C2)
+  for (uint32_t s = threadIdx.x; s < (1u << FIX); s += blockDim.x) L[atomicAdd(&pos[pat(s)], 1u)] = (LT)s;
   // dummy slots: the tail of each bucket's last piece (unused pieces are never read)
-  for (int g = 0; g < 9; ++g) {
+  for (int g = 0; g < NB; ++g) {
     const uint32_t end = pstart[g] * 1024u + cnt[g], pend = pstart[g] * 1024u + ((cnt[g] + 1023u) & ~1023u);
-    for (uint32_t i = end + threadIdx.x; i < pend; i += blockDim.x) L[i] = kBucketDummy;
+    for (uint32_t i = end + threadIdx.x; i < pend; i += blockDim.x) L[i] = (LT)~0u;
   }
 }
 
@@ -187,9 +200,10 @@ static __device__ __noinline__ uint32_t bucket_wide_term(const RowRec* R, uint32
 // n > 32: exact evaluation of the steps in `mask` against this lane's real
 // slots, both words (dense mode, list overflow).  Slot-major, so each slot's
 // secondary word is built once.  Returns ev | odd << 32.
+template <class LT>
 static __device__ __noinline__ unsigned long long bucket_exact_wide(const uint4 (*A2)[32], const uint4* H,
                                                                     const uint2* H1, const RowRec* R,
-                                                                    const uint16_t* Lp, uint32_t mask, uint32_t lane,
+                                                                    const LT* Lp, uint32_t mask, uint32_t lane,
                                                                     uint32_t spm, uint32_t vmask, uint32_t z1i) {
   uint32_t ev = 0, odd = 0;
 #pragma unroll 1
@@ -224,11 +238,12 @@ static __device__ __noinline__ unsigned long long bucket_exact_wide(const uint4 
 
 }  // namespace
 
-template <int V, int WARPS, bool PACKED, bool WIDE, int FIX>
+template <int V, int WARPS, bool PACKED, bool WIDE, int FIX, int KEYS>
 __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) {
   constexpr int KB = 5;
   constexpr int K = 1 << KB;
-  constexpr int kBucketPieces = pieces_of(FIX);
+  constexpr int kBucketPieces = pieces_of(FIX, KEYS);
+  using LT = list_t<FIX>;
   constexpr int SB = 1 << V;
   const FastParams& p = bp.fp;
   static_assert(PACKED || !WIDE, "n > 32 needs the packed filter");
@@ -249,7 +264,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
   const uint32_t one = p.one;
   const uint32_t colmask = p.z0_init;  // real columns (n <= 31: bit 31 is padding)
   const uint32_t colmask1 = p.z1_init;  // n > 32: real columns of the secondary word
-  const int k1 = (WIDE ? 32 : p.n) - 1, k2 = k1 - 1;
+  const int k1 = (WIDE ? 32 : p.n) - 1;  // key columns k1, k1-1 (, k1-2)
   unsigned long long n_items = 0;
 
   for (;;) {
@@ -285,13 +300,13 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
     uint32_t Zp[PACKED ? K / 2 : 1], Gp[PACKED ? K / 2 : 1];
     uint32_t spm = 0;  // bit k: parity of slot k's subset
     uint32_t vmask = 0;  // bit k: slot k holds a real A subset (not padding)
-    const uint16_t* Lp = bp.list + (b * kBucketPieces + q) * 1024;
+    const LT* Lp = static_cast<const LT*>(bp.list) + (b * kBucketPieces + q) * 1024;
     {
       auto slot = [&](int k, uint32_t& z, uint32_t& g) {
         const uint32_t s = Lp[32 * k + lane];
         z = colmask;
         g = 0;
-        if (s == kBucketDummy) {
+        if (s == (uint32_t)(LT)~0u) {  // dummy slot
           // n <= 31: -1 in padding column 31 (B side: +1), never a full sum;
           // n = 32 has no padding column: the verify and exact paths test vmask
           if (p.n <= 31) g = 0x80000000u;
@@ -326,11 +341,25 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
       }
     }
     // forbidden key trits of this piece: f = -x (mod 3)
-    const uint32_t x1 = grp / 3, x2 = grp % 3;
-    const uint32_t f1 = (3 - x1) % 3, f2 = (3 - x2) % 3;
-    const uint32_t F0 = (f1 == 0 ? 1u << k1 : 0u) | (f2 == 0 ? 1u << k2 : 0u);
-    const uint32_t F1 = (f1 == 1 ? 1u << k1 : 0u) | (f2 == 1 ? 1u << k2 : 0u);
-    const uint32_t F2 = (f1 == 2 ? 1u << k1 : 0u) | (f2 == 2 ? 1u << k2 : 0u);
+    uint32_t F0, F1, F2;
+    if constexpr (KEYS == 2) {
+      const int k2 = k1 - 1;
+      const uint32_t x1 = grp / 3, x2 = grp % 3;
+      const uint32_t f1 = (3 - x1) % 3, f2 = (3 - x2) % 3;
+      F0 = (f1 == 0 ? 1u << k1 : 0u) | (f2 == 0 ? 1u << k2 : 0u);
+      F1 = (f1 == 1 ? 1u << k1 : 0u) | (f2 == 1 ? 1u << k2 : 0u);
+      F2 = (f1 == 2 ? 1u << k1 : 0u) | (f2 == 2 ? 1u << k2 : 0u);
+    } else {
+      F0 = F1 = F2 = 0;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const uint32_t x = (i == 0 ? grp / 9 : i == 1 ? grp / 3 : grp) % 3;
+        const uint32_t f = (3 - x) % 3, bit = 1u << (k1 - i);
+        F0 |= f == 0 ? bit : 0u;
+        F1 |= f == 1 ? bit : 0u;
+        F2 |= f == 2 ? bit : 0u;
+      }
+    }
     // B side: v2 for S2 = gray(A0) on rows >= FIX (low bits empty)
     uint32_t z2, u2;
     uint32_t z2w = 0, u2w = 0;  // n > 32: secondary word of the entry state
@@ -595,29 +624,44 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) 
   queue_done(p, lane);
 }
 
-int bucket_pieces(int fix) { return pieces_of(fix); }
+int bucket_pieces(BucketCfg c) { return pieces_of(c.fix, c.keys); }
 int bucket_v(bool packed) { return packed ? 5 : 4; }  // log2 superblock length
-// 13 rows when the B side is short (n < 27: items are one matrix's whole B
-// side, and a 13-row A side doubles its length); 14 otherwise
-int bucket_fix(int n, bool packed) { return (packed && n < 27) ? 13 : 14; }
+size_t bucket_list_elem(BucketCfg c) { return c.fix > 15 ? 4 : 2; }
 
-cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, int fix, uint16_t* list, uint32_t* ptab,
+// Unpacked pair tests: 14 rows, 2 keys.  Packed filter: a 13-row A side for
+// n < 28, where items are one matrix's whole B side and a short A side makes
+// them longer; from n = 28 a 17-row A side in 27 buckets of three key
+// columns (the B side still has >= 64 superblocks per matrix), which skips
+// 19/27 of the steps instead of 5/9 and fills its pieces better.
+BucketCfg bucket_cfg(int n, bool packed) {
+  if (!packed) return BucketCfg{14, 2};
+  if (n < 28) return BucketCfg{13, 2};
+  return BucketCfg{17, 3};
+}
+
+cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, BucketCfg c, void* list, uint32_t* ptab,
                                 cudaStream_t st) {
-  k_bucket_group<<<(unsigned)B, 256, 0, st>>>(rows, n, fix, list, ptab);
+  const unsigned grid = (unsigned)B;
+  if (c.fix == 13 && c.keys == 2) k_bucket_group<13, 2><<<grid, 512, 0, st>>>(rows, n, (uint16_t*)list, ptab);
+  else if (c.fix == 14 && c.keys == 2) k_bucket_group<14, 2><<<grid, 512, 0, st>>>(rows, n, (uint16_t*)list, ptab);
+  else if (c.fix == 17 && c.keys == 3) k_bucket_group<17, 3><<<grid, 512, 0, st>>>(rows, n, (uint32_t*)list, ptab);
+  else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 
 cudaError_t launch_walk_bucket(int grid, const BucketParams& bp, bool packed, cudaStream_t st) {
-  if (bp.fp.n > 32) k_walk_bucket<5, 4, true, true, 14><<<grid, 128, 0, st>>>(bp);
-  else if (!packed) k_walk_bucket<4, 4, false, false, 14><<<grid, 128, 0, st>>>(bp);
-  else if (bucket_fix(bp.fp.n, true) == 13) k_walk_bucket<5, 4, true, false, 13><<<grid, 128, 0, st>>>(bp);
-  else k_walk_bucket<5, 4, true, false, 14><<<grid, 128, 0, st>>>(bp);
+  const BucketCfg c = bucket_cfg(bp.fp.n, packed);
+  if (c.fix != bp.fix || c.keys != bp.keys) return cudaErrorInvalidValue;
+  if (bp.fp.n > 32) k_walk_bucket<5, 4, true, true, 17, 3><<<grid, 128, 0, st>>>(bp);
+  else if (!packed) k_walk_bucket<4, 4, false, false, 14, 2><<<grid, 128, 0, st>>>(bp);
+  else if (c.fix == 13) k_walk_bucket<5, 4, true, false, 13, 2><<<grid, 128, 0, st>>>(bp);
+  else k_walk_bucket<5, 4, true, false, 17, 3><<<grid, 128, 0, st>>>(bp);
   return cudaGetLastError();
 }
 
 const void* walk_bucket_symbol(bool packed) {
-  return packed ? reinterpret_cast<const void*>(&k_walk_bucket<5, 4, true, false, 14>)
-                : reinterpret_cast<const void*>(&k_walk_bucket<4, 4, false, false, 14>);
+  return packed ? reinterpret_cast<const void*>(&k_walk_bucket<5, 4, true, false, 13, 2>)
+                : reinterpret_cast<const void*>(&k_walk_bucket<4, 4, false, false, 14, 2>);
 }
 
 }  // namespace tp
