@@ -105,7 +105,6 @@ struct BucketParams {
   const uint32_t* ptab;         // [B][pieces] bucket | valid count << 16 (count 0 = unused)
   unsigned long long* tested;   // += pairs actually tested (compatible steps x 1024), or nullptr
   unsigned long long s_end;     // end of the superblock region
-  int fix, keys;                // bucket configuration (bucket_cfg)
 };
 struct BucketCfg {
   int fix;   // A side: rows 0..fix-1

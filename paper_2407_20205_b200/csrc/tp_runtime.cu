@@ -322,8 +322,6 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
       f.dense_ok = 1;
       f.static_items = 0;
       pl.bkp.list = pl.bucket_list;
-      pl.bkp.fix = cfg.fix;
-      pl.bkp.keys = cfg.keys;
       pl.bkp.ptab = pl.bucket_ptab;
       pl.bkp.tested = d.bucket_tested;
       pl.bkp.s_end = s1;

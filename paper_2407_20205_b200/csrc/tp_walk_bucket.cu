@@ -236,10 +236,31 @@ static __device__ __noinline__ unsigned long long bucket_exact_wide(const uint4 
   return (unsigned long long)ev | ((unsigned long long)odd << 32);
 }
 
+// Kernel argument: the 3-key kernels also carry their configuration.  The
+// two parameter layouts are the ones measured fastest for each kernel: with
+// the larger block ptxas schedules the filter loop differently, which costs
+// the 2-key kernel 4 % on C2 and gains the 3-key kernels 3-5 % on C3-C5.
+struct BucketParamsCfg {  // BucketParams' fields, then the configuration
+  FastParams fp;
+  const void* list;
+  const uint32_t* ptab;
+  unsigned long long* tested;
+  unsigned long long s_end;
+  int fix, keys;
+};
+template <int KEYS>
+struct BucketArg {
+  using type = BucketParams;
+};
+template <>
+struct BucketArg<3> {
+  using type = BucketParamsCfg;
+};
+
 }  // namespace
 
 template <int V, int WARPS, bool PACKED, bool WIDE, int FIX, int KEYS>
-__global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(BucketParams bp) {
+__global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename BucketArg<KEYS>::type bp) {
   constexpr int KB = 5;
   constexpr int K = 1 << KB;
   constexpr int kBucketPieces = pieces_of(FIX, KEYS);
@@ -651,11 +672,11 @@ cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, BucketCf
 
 cudaError_t launch_walk_bucket(int grid, const BucketParams& bp, bool packed, cudaStream_t st) {
   const BucketCfg c = bucket_cfg(bp.fp.n, packed);
-  if (c.fix != bp.fix || c.keys != bp.keys) return cudaErrorInvalidValue;
-  if (bp.fp.n > 32) k_walk_bucket<5, 4, true, true, 17, 3><<<grid, 128, 0, st>>>(bp);
+  const BucketParamsCfg bc{bp.fp, bp.list, bp.ptab, bp.tested, bp.s_end, c.fix, c.keys};
+  if (bp.fp.n > 32) k_walk_bucket<5, 4, true, true, 17, 3><<<grid, 128, 0, st>>>(bc);
   else if (!packed) k_walk_bucket<4, 4, false, false, 14, 2><<<grid, 128, 0, st>>>(bp);
   else if (c.fix == 13) k_walk_bucket<5, 4, true, false, 13, 2><<<grid, 128, 0, st>>>(bp);
-  else k_walk_bucket<5, 4, true, false, 17, 3><<<grid, 128, 0, st>>>(bp);
+  else k_walk_bucket<5, 4, true, false, 17, 3><<<grid, 128, 0, st>>>(bc);
   return cudaGetLastError();
 }
 
