@@ -487,16 +487,17 @@ def test_tensor_core_pair_test_exact(gpu, oracle, monkeypatch):
 
 
 def test_bucketed_pair_walk_exact(gpu, oracle, monkeypatch):
-    """The bucketed pair walk (tp_walk_bucket.cu; the default for batches of
-    21 <= n <= 31, TRITPERM_BUCKET=1 packed filter / 2 pair tests) against the
-    packed walk (TRITPERM_BUCKET=0) and the oracle: full traversals, uniform,
-    sparse and all-ones matrices; raw partials bit for bit (only zero terms are
+    """The bucketed pair walk on batches (tp_walk_bucket.cu; TRITPERM_BUCKET=1
+    packed filter -- 13-row A side / 2 key columns below n = 28, 17 rows / 3
+    key columns from n = 28 -- and 2 = unpacked pair tests) against the packed
+    walk (TRITPERM_BUCKET=0) and the oracle: full traversals, uniform, sparse
+    and all-ones matrices; raw partials bit for bit (only zero terms are
     skipped)."""
     from paper_2407_20205_b200 import fixtures
 
     r = np.random.default_rng(31)
     cases = [fixtures.uniform_batch(n, 13, 0, B) for n, B in ((21, 48), (22, 7), (24, 40), (27, 3), (31, 2))]
-    for n in (21, 26):
+    for n in (21, 26, 29):
         sp = ((r.random((5, n, n)) < 0.25) * r.integers(1, 3, (5, n, n))).astype(np.uint8)
         cases.append(np.concatenate([sp, np.ones((2, n, n), np.uint8)]))
     for e in cases:
