@@ -175,6 +175,11 @@ static __device__ __noinline__ unsigned long long bucket_exact_packed(const uint
   return (unsigned long long)bev | ((unsigned long long)bodd << 32);
 }
 
+// List row of physical slot k = w + 16 h (packed word w, half h): 2 w + h.
+// The first 2W rows of a piece then fill packed words 0..W-1, so a piece
+// with at most 64 W real slots runs the filter on W words only.
+__device__ __forceinline__ uint32_t lrow(int k) { return 2u * (uint32_t)(k & 15) + ((uint32_t)k >> 4); }
+
 // n > 32: the secondary word (columns 32..n-1) of A subset s, from scratch.
 __device__ __forceinline__ void a_word1(const RowRec* R, uint32_t s, uint32_t z1i, uint32_t& z, uint32_t& g) {
   z = z1i;
@@ -210,7 +215,7 @@ static __device__ __noinline__ unsigned long long bucket_exact_wide(const uint4 
   for (int k = 0; k < 32; ++k) {
     if (!((vmask >> k) & 1u)) continue;
     uint32_t za1, ga1;
-    a_word1(R, Lp[32 * k + lane], z1i, za1, ga1);
+    a_word1(R, Lp[32 * lrow(k) + lane], z1i, za1, ga1);
     const uint4 a4 = A2[k & 15][lane];
     const uint32_t za = k < 16 ? a4.x : a4.z, ga = k < 16 ? a4.y : a4.w;
     const uint32_t kp = (spm >> k) & 1u;
@@ -309,6 +314,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
     const uint32_t pt = bp.ptab[b * kBucketPieces + q];
     if ((pt >> 16) == 0) continue;  // unused piece
     const uint32_t grp = pt & 0xFFFFu;
+    const uint32_t nwd = ((pt >> 16) + 63u) >> 6;  // packed words holding the piece's real slots
     __syncwarp();
     load_rows(R, p.rows + b * 64, lane, p.n);
     __syncwarp();
@@ -324,7 +330,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
     const LT* Lp = static_cast<const LT*>(bp.list) + (b * kBucketPieces + q) * 1024;
     {
       auto slot = [&](int k, uint32_t& z, uint32_t& g) {
-        const uint32_t s = Lp[32 * k + lane];
+        const uint32_t s = Lp[32 * lrow(k) + lane];
         z = colmask;
         g = 0;
         if (s == (uint32_t)(LT)~0u) {  // dummy slot
@@ -398,7 +404,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
       u2w = pair_u2(zw, gw);
     }
     uint32_t ev = 0, odd = 0;
-    uint32_t tested_steps = 0;  // compatible steps of this item (x 1024 pairs)
+    uint32_t tested_steps = 0;  // compatible steps of this item (x the slots the filter tests)
     // exact evaluation of every pair of the superblock from H (replays, dense mode)
     // (only the steps in `mask`: incompatible steps have no full term)
     auto exact_block = [&](uint32_t& bev, uint32_t& bodd, uint32_t mask) {
@@ -481,6 +487,10 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
           // (step a) / 16 + w (step b) of M = a pass of word w; nonzero masks
           // go to this lane's list E for the exact verify after the loop
           uint32_t cm = cmask, ne = 0;
+          // W packed words hold every real slot of the piece (the rest are
+          // padding): 15 for most 2-key pieces (<= 960 of 1024 slots)
+          auto filter = [&](auto Wc) {
+          constexpr int W = decltype(Wc)::value;
           while (cm) {
             const uint32_t ja = __ffs(cm) - 1;
             cm &= cm - 1;
@@ -489,7 +499,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
             const uint4 ha = H[ja];
             const uint4 hb = H[jb == 0xFFu ? ja : jb];
             uint32_t M = 0;
-            static_for<K / 2>([&](auto wc) {
+            static_for<W>([&](auto wc) {
               constexpr int w = decltype(wc)::value;
               packed_test<(1u << w)>(Zp[w], Gp[w], ha.z, ha.w, M, one, cneg);
               packed_test<(1u << (16 + w))>(Zp[w], Gp[w], hb.z, hb.w, M, one, cneg);
@@ -500,6 +510,12 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
               ++ne;
             }
           }
+          };
+          // (2-key kernels only: in the 3-key kernels the extra loop copies
+          // cost more in schedule quality than the 4 % of tests they save)
+          if (KEYS == 3 || nwd > 15) filter(std::integral_constant<int, 16>{});
+          else if (nwd > 12) filter(std::integral_constant<int, 15>{});
+          else filter(std::integral_constant<int, 12>{});
           if (__any_sync(FULL, ne > (uint32_t)ECAP)) {
             // a lane's pass list overflowed (event-dense matrix): evaluate the
             // superblock's compatible steps exactly instead
@@ -532,7 +548,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
                     uint32_t par = 0;
                     if constexpr (WIDE) {
                       // the primary columns are nonzero: test the secondary ones
-                      const uint32_t r = bucket_wide_term(R, Lp[32 * k + lane], H1[j], colmask1);
+                      const uint32_t r = bucket_wide_term(R, Lp[32 * lrow(k) + lane], H1[j], colmask1);
                       if (!r) continue;
                       par = r >> 1;
                     }
@@ -640,7 +656,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
       }
     }
     warp_flush(p.pm + 2 * b, ev - odd, odd, lane);
-    if (bp.tested && lane == 0) atomicAdd(bp.tested, 1024ull * tested_steps);
+    if (bp.tested && lane == 0) atomicAdd(bp.tested, (PACKED && KEYS == 2 ? 64ull * (nwd > 15 ? 16 : nwd > 12 ? 15 : 12) : 1024ull) * tested_steps);
   }
   queue_done(p, lane);
 }
