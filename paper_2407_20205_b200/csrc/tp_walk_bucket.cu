@@ -85,12 +85,16 @@ __global__ void __launch_bounds__(512) k_bucket_group(const RowRec* rows, int n,
   auto pat = [&](uint32_t s) -> uint32_t { return comb[tab[0][s & ((1u << TB) - 1u)]][tab[1][s >> TB]]; };
   for (uint32_t s = threadIdx.x; s < (1u << FIX); s += blockDim.x) atomicAdd(&cw[warp][pat(s)], 1u);
   __syncthreads();
+  if (threadIdx.x < (uint32_t)NB) {  // bucket totals, one thread per bucket
+    uint32_t c = 0;
+    for (int w = 0; w < NW; ++w) c += cw[w][threadIdx.x];
+    cnt[threadIdx.x] = c;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t piece = 0;
     for (int g = 0; g < NB; ++g) {
-      uint32_t c = 0;
-      for (int w = 0; w < NW; ++w) c += cw[w][g];
-      cnt[g] = c;
+      const uint32_t c = cnt[g];
       pstart[g] = piece;
       pos[g] = piece * 1024u;
       const uint32_t np = (c + 1023u) / 1024u;
