@@ -1,28 +1,33 @@
-// tp_walk_bucket.cu -- the pair walk with the A side bucketed by two key
-// columns (full traversals; n <= 32 for the packed filter, n <= 31 for the
-// unpacked pair tests).
+// tp_walk_bucket.cu -- the pair walk with the A side bucketed by key columns:
+// the default walk for 21 <= n <= 64 (full traversals and the superblock-
+// aligned middle of step ranges).
 //
 // The pair walk (tp_walk_pair.cu) tests every (A vector, B state) pair.  A pair
 // whose sum has a zero in ANY column is a zero term, so pairs can be skipped
 // wholesale by looking at a few "key" columns first:
 //
-//   * the A side is rows 0..13 (16384 A vectors per matrix).  k_bucket_group
-//     sorts them by their trits (x1, x2) on the key columns k1 = n-1,
-//     k2 = n-2 into 9 buckets and cuts each bucket into pieces of 1024
+//   * the A side is rows 0..FIX-1 (FIX = 13 below n = 28, 17 from n = 28;
+//     bucket_cfg).  k_bucket_group sorts its 2^FIX subsets by their trits on
+//     KEYS key columns (n-1, n-2 and, for KEYS = 3, n-3; 31, 30, 29 for
+//     n > 32) into 3^KEYS buckets and cuts each bucket into pieces of 1024
 //     (= 32 lanes x 32 slots, the pair walk's A side per warp; the last piece
 //     of a bucket is padded with dummy slots);
-//   * a warp takes one piece, so all its A vectors share (x1, x2), and walks
-//     the B side (rows 14..n-1) in Gray order as usual;
-//   * a B state y is compatible with the piece iff y1 != -x1 and y2 != -x2;
-//     otherwise every one of the warp's 1024 pairs with it has a zero key
-//     column.  Compatibility is warp-uniform, so the 32 pair tests of an
-//     incompatible step are skipped by a uniform branch.
+//   * a warp takes one piece, so all its A vectors share their key trits x,
+//     and walks B-side superblocks (rows FIX..n-1) in Gray order as usual;
+//   * a B state y is compatible with the piece iff y_k != -x_k on every key
+//     column; otherwise every one of the warp's 1024 pairs with it has a zero
+//     key column.  Compatibility is warp-uniform: the packed filter runs on
+//     the compatible steps only.
 //
-// On uniform inputs 4/9 of the steps are compatible, so the pair tests drop
-// to 44 % (plus ~11 % of dummy slots), and the sum is unchanged: only zero
-// terms are skipped, so raw partials equal chunk_sum (src/_kernels.py:90-128)
-// bit for bit.  Dummy slots carry a -1 in padding column 31 (the B side has
-// +1 there), so their sums always have a zero column and never count.
+// On uniform inputs 4/9 (KEYS = 2) or 8/27 (KEYS = 3) of the steps are
+// compatible; with the padding of partly filled pieces 47 % / 31 % of all
+// pairs are tested.  The sum is unchanged: only zero terms are skipped, so
+// raw partials equal chunk_sum (src/_kernels.py:90-128) bit for bit.  Dummy
+// slots carry a -1 in padding column 31 for n <= 31 (the B side has +1
+// there), so their sums always have a zero column; for n >= 32 they are the
+// zero vector and the verify and exact paths exclude them by a slot mask.
+// For n > 32 the filter and verify cover the 32 primary columns, and a pair
+// whose primary columns are all nonzero gets its secondary word tested.
 #include <type_traits>
 
 #include "tp_walk_common.cuh"
