@@ -500,22 +500,37 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
           // padding): 15 for most 2-key pieces (<= 960 of 1024 slots)
           auto filter = [&](auto Wc) {
           constexpr int W = decltype(Wc)::value;
-          while (cm) {
+          // two compatible steps per iteration while two remain ...
+          while (cm & (cm - 1)) {
             const uint32_t ja = __ffs(cm) - 1;
             cm &= cm - 1;
-            const uint32_t jb = cm ? (uint32_t)(__ffs(cm) - 1) : 0xFFu;
-            if (cm) cm &= cm - 1;
+            const uint32_t jb = __ffs(cm) - 1;
+            cm &= cm - 1;
             const uint4 ha = H[ja];
-            const uint4 hb = H[jb == 0xFFu ? ja : jb];
+            const uint4 hb = H[jb];
             uint32_t M = 0;
             static_for<W>([&](auto wc) {
               constexpr int w = decltype(wc)::value;
               packed_test<(1u << w)>(Zp[w], Gp[w], ha.z, ha.w, M, one, cneg);
               packed_test<(1u << (16 + w))>(Zp[w], Gp[w], hb.z, hb.w, M, one, cneg);
             });
-            if (jb == 0xFFu) M &= 0xFFFFu;
             if (M) {
               if (ne < (uint32_t)ECAP) E[ne][lane] = make_uint2(M, ja | (jb << 8));
+              ++ne;
+            }
+          }
+          // ... and an odd last step alone (half the tests)
+          if (cm) {
+            const uint32_t ja = __ffs(cm) - 1;
+            cm = 0;
+            const uint4 ha = H[ja];
+            uint32_t M = 0;
+            static_for<W>([&](auto wc) {
+              constexpr int w = decltype(wc)::value;
+              packed_test<(1u << w)>(Zp[w], Gp[w], ha.z, ha.w, M, one, cneg);
+            });
+            if (M) {
+              if (ne < (uint32_t)ECAP) E[ne][lane] = make_uint2(M, ja | (0xFFu << 8));
               ++ne;
             }
           }
