@@ -11,8 +11,18 @@ all-reduce when N > 1).  Metric: Gray-code subset terms/s = 2^n * matrices/s.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c1|c3|c4|c5]
   python bench.py --impl reference ...   # the reference's CPU path (oracle port)
 
-Under torchrun (N > 1) every rank takes its own 16,384 trials (weak scaling)
-and the 3-bin histogram meets in one NCCL all-reduce per step.
+--gpus N > 1 without torchrun re-launches itself under
+`python -m torch.distributed.run --nproc-per-node N` (one rank per GPU).
+At N > 1 every rank takes its own 16,384 trials (weak scaling) and the
+3-bin histogram meets in one NCCL all-reduce per step.
+
+Every line also carries a "c5_strong" record: the north_star's scaling
+target, C5's seed-0 50x50 matrix on a fixed 2^44-step window split over the
+ranks by the split_steps rule (src/permanent.py:221-229), one 16-byte NCCL
+all-reduce of the (plus, minus) counters inside each timed step
+(communicator set-up excluded), the per-rank device times, and the
+efficiency E(N) = T(1) / (N T(N)) with T(1) measured in the same run by rank
+0 alone on the whole window.
 """
 
 from __future__ import annotations
@@ -54,7 +64,41 @@ def parse():
     ap.add_argument("--graph", type=int, default=None,
                     help="replay each step from a CUDA graph (default: on for the single small matrix c1)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample time")
+    ap.add_argument("--c5-steps", type=int, default=3, help="timed steps of the c5_strong record (0: skip it)")
+    ap.add_argument("--selftest-cpu", action="store_true",
+                    help="CPU plumbing test of the launcher, rank split and collective (gloo; no GPU "
+                         "compute: the per-rank counts are zero)")
     return ap.parse_args()
+
+
+def free_port() -> int:
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_under_torchrun(args) -> int:
+    """--gpus N > 1 outside torchrun: one rank per GPU, as the driver would
+    launch it (rendezvous on 127.0.0.1)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def rank_part(lo: int, span: int, rank: int, world: int):
+    """Part `rank` of [lo, lo + span) by the split_steps edge rule
+    (src/permanent.py:227-229; paper_2407_20205_b200.parallel.rank_range)."""
+    return lo + span * rank // world, lo + span * (rank + 1) // world
+
+
+def workload_config(wl: str) -> dict:
+    """The config dict both arms print (identical keys and values)."""
+    n, B, desc = WORKLOADS[wl]
+    return {"workload": desc, "n": n, "batch": B, "seed": SEED}
 
 
 # ---------------------------------------------------------------------------
@@ -173,6 +217,63 @@ def cpu_rate(workload: str, target_s: float, threads: int):
     return span / dt, f"steps [{lo}, {lo}+2^{int(math.log2(span))}) of the matrix, split over {threads} threads", span, dt
 
 
+REF_PATH = os.path.join(REPO, "baseline", "_ref")
+
+
+def numba_reference_rate(workload: str, target_s: float, threads: int):
+    """The UNMODIFIED reference package (baseline/_ref, installed from
+    /root/reference with pip --no-deps) through its own public API, numba
+    kernels and thread pool: montecarlo_zero (src/experiments.py:158-190) on a
+    bounded trial count for c2, chunk_sum (src/_kernels.py:90-128) over a
+    window split across a ThreadPool the way perm_mod3_parallel does
+    (src/permanent.py:232-255) otherwise.  None if it is not installed."""
+    if not os.path.isdir(os.path.join(REF_PATH, "tritperm")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/tritperm_numba_cache")
+    if REF_PATH not in sys.path:
+        sys.path.insert(0, REF_PATH)
+    from concurrent.futures import ThreadPoolExecutor
+
+    from tritperm import _kernels as rk
+    from tritperm import experiments as rexp
+
+    n, B, _ = WORKLOADS[workload]
+    if workload == "c2":
+        rexp.montecarlo_zero(n, threads, seed=SEED, jobs=threads)  # JIT warm-up
+        t0 = time.perf_counter()
+        rexp.montecarlo_zero(n, threads, seed=SEED, jobs=threads)
+        dt = time.perf_counter() - t0
+        trials = int(max(threads, min(B, threads * target_s / max(dt, 1e-6))))
+        t0 = time.perf_counter()
+        r = rexp.montecarlo_zero(n, trials, seed=SEED, jobs=threads)
+        dt = time.perf_counter() - t0
+        return {"value": trials * (1 << n) / dt, "unit": "terms/s", "cores": threads, "seconds": round(dt, 2),
+                "sample": f"tritperm.montecarlo_zero({n}, {trials}, seed={SEED}, jobs={threads}) "
+                          f"-> zero_count {r.zero_count} (first {trials} of the {B} trials)"}
+    m = rexp.sample_trial_matrix(n, 0, SEED)
+    mags, sgns = m.planes()
+    lo = 1 if workload != "c5" else (1 << 40)
+
+    def run(span):
+        edges = [lo + span * k // threads for k in range(threads + 1)]
+        with ThreadPoolExecutor(max_workers=threads) as ex:
+            return sum(ex.map(lambda k: int(rk.chunk_sum(mags, sgns, n, edges[k], edges[k + 1])), range(threads)))
+
+    run(1 << 16)  # JIT warm-up
+    span = 1 << 22
+    t0 = time.perf_counter()
+    run(span)
+    dt = time.perf_counter() - t0
+    span = min((1 << n) - lo, max(span, int(span * target_s / max(dt, 1e-6))))
+    span = 1 << max(10, int(math.log2(span)))
+    t0 = time.perf_counter()
+    run(span)
+    dt = time.perf_counter() - t0
+    return {"value": span / dt, "unit": "terms/s", "cores": threads, "seconds": round(dt, 2),
+            "sample": f"tritperm._kernels.chunk_sum over steps [{lo}, {lo}+2^{int(math.log2(span))}) of "
+                      f"sample_trial_matrix({n}, 0, {SEED}), {threads} ThreadPool parts"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -180,13 +281,21 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     n, B, desc = WORKLOADS[args.workload]
     per_step = max(1.0, min(6.0, 120.0 / max(1, args.steps + args.warmup)))
-    rates = []
+    rates, secs, terms = [], [], []
     sample = None
     for k in range(args.warmup + args.steps):
-        rate, sample, _, _ = cpu_rate(args.workload, per_step, threads)
+        rate, sample, t, dt = cpu_rate(args.workload, per_step, threads)
         if k >= args.warmup:
             rates.append(rate)
+            secs.append(dt)
+            terms.append(t)
     value = statistics.median(rates)
+    numba = None
+    if os.environ.get("TRITPERM_BENCH_NUMBA", "1") != "0":
+        try:
+            numba = numba_reference_rate(args.workload, 8.0, threads)
+        except Exception as exc:  # report, never fail the arm
+            numba = {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
     line = {
         "impl": "reference",
         "metric": "gray_code_subset_terms_per_s",
@@ -195,18 +304,145 @@ def run_reference(args):
         "n_gpus": args.gpus,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": terms_per_step(args.workload, args) / value * 1e3,
+        # each step is a bounded sample of the workload, measured as is (not
+        # extrapolated to the full workload)
+        "ms_per_step": statistics.median(secs) * 1e3,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "u32",
         "data": "synthetic (reference trial stream)",
-        "config": {"workload": desc, "n": n, "batch": B, "seed": SEED},
+        "config": workload_config(args.workload),
+        "sample_per_step": {"terms": int(statistics.median(terms)), "of_workload_terms": terms_per_step(args.workload, args),
+                            "seconds": round(statistics.median(secs), 3), "what": sample},
         "cpu_baseline": {"value": value, "unit": "terms/s", "cores": threads, "kind": "port",
                          "sample": f"oracle/oracle.c chunk_sum (restatement of src/_kernels.py:90-128), {sample}"},
+        "reference_numba": numba,
         "e2e": {"value": value, "unit": "terms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+# C5 strong scaling (north_star: >= 90 % at 8 GPUs on the n = 50 run)
+# ---------------------------------------------------------------------------
+
+def c5_strong(args, rank: int, world: int, use_dist: bool, dev):
+    """Fixed 2^k-step window of C5's matrix split over the ranks; per step:
+    zero the counters, walk this rank's part, one 16-byte all-reduce.  Device
+    times (CUDA events on the launching stream), max over ranks per step."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2407_20205_b200 import _kernels
+
+    n = 50
+    a = make_entries("c5", 0)[0]
+    span = 1 << args.c5_log2_steps
+    lo0 = 1 << 40
+    plo, phi = rank_part(lo0, span, rank, world)
+    d_e = torch.from_numpy(np.ascontiguousarray(a[None])).to(dev)
+    d_rows = torch.empty((1, _kernels.ROWREC_BYTES), dtype=torch.uint8, device=dev)
+    d_pm = torch.zeros(2, dtype=torch.int64, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    _kernels.pack_async(d_e.data_ptr(), 1, n, d_rows.data_ptr(), st)
+
+    def step(lo, hi, reduce):
+        d_pm.zero_()
+        _kernels.walk_range_async(d_rows.data_ptr(), n, lo, hi, d_pm.data_ptr(), st)
+        if reduce:
+            dist.all_reduce(d_pm)
+
+    step(plo, phi, use_dist)  # warm-up (also creates the NCCL communicator, outside the timed steps)
+    torch.cuda.synchronize()
+    mine, step_max = [], []
+    for _ in range(args.c5_steps):
+        if use_dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        step(plo, phi, use_dist)
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1)
+        mine.append(t)
+        if use_dist:
+            tt = torch.tensor([t], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt.item())
+        step_max.append(t)
+    pm = d_pm.cpu().tolist()
+    per_rank = [statistics.mean(mine)]
+    if use_dist:
+        g = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in range(world)]
+        dist.all_gather(g, torch.tensor([statistics.mean(mine)], dtype=torch.float64, device=dev))
+        per_rank = [float(x.item()) for x in g]
+    t_n = statistics.mean(step_max)
+    t_1, pm1 = t_n, pm
+    if world > 1:
+        # T(1): rank 0 alone on the whole window, same kernels, no collective
+        dist.barrier()
+        if rank == 0:
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            step(lo0, lo0 + span, False)
+            e1.record()
+            torch.cuda.synchronize()
+            t_1 = e0.elapsed_time(e1)
+            pm1 = d_pm.cpu().tolist()
+        dist.barrier()
+    return {
+        "workload": f"C5 matrix (seed 0, trial 0), steps [2^40, 2^40 + 2^{args.c5_log2_steps}) split over "
+                    f"{world} rank(s) by the split_steps rule",
+        "n_ranks": world, "steps": args.c5_steps, "terms_per_step": span,
+        "ms_per_step": t_n, "per_rank_ms": per_rank, "value": span / (t_n * 1e-3), "unit": "terms/s",
+        "collective": "one 16-byte NCCL all_reduce of (plus, minus) per step" if use_dist else "none (1 rank)",
+        "t1_ms": t_1, "efficiency": t_1 / (world * t_n),
+        "partial": int(pm[0] - pm[1]), "partial_1rank": int(pm1[0] - pm1[1]),
+    }
+
+
+def run_selftest_cpu(args):
+    """CPU plumbing of the N-rank path (gloo): launcher, rank split, one
+    all-reduce of the counters per step, max over ranks, the JSON line.  No
+    compute runs (the counts are zero); the B200 path needs a GPU."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    span = 1 << args.c5_log2_steps
+    plo, phi = rank_part(1 << 40, span, rank, world)
+    parts = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+    mine = torch.tensor([plo, phi], dtype=torch.int64)
+    if world > 1:
+        dist.all_gather(parts, mine)
+    else:
+        parts = [mine]
+    times = []
+    for _ in range(max(1, args.c5_steps)):
+        t0 = time.perf_counter()
+        pm = torch.zeros(2, dtype=torch.int64)
+        if world > 1:
+            dist.all_reduce(pm)
+        times.append((time.perf_counter() - t0) * 1e3)
+    if rank == 0:
+        edges = [tuple(int(v) for v in p.tolist()) for p in parts]
+        print(json.dumps({"metric": "gray_code_subset_terms_per_s", "selftest": True, "n_gpus": world,
+                          "config": workload_config(args.workload),
+                          "c5_strong": {"n_ranks": world, "parts": edges, "terms_per_step": span,
+                                        "covers_window": edges[0][0] == 1 << 40 and edges[-1][1] == (1 << 40) + span
+                                        and all(a[1] == b[0] for a, b in zip(edges, edges[1:])),
+                                        "ms_per_step": statistics.mean(times), "partial": int(pm[0] - pm[1])}}))
+    if world > 1:
+        dist.destroy_process_group()
 
 
 # ---------------------------------------------------------------------------
@@ -215,10 +451,15 @@ def run_reference(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
     if args.graph is None:
         args.graph = 1 if args.workload == "c1" else 0
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.selftest_cpu:
+        run_selftest_cpu(args)
         return
 
     import numpy as np
@@ -440,6 +681,10 @@ def main():
         e2e = {"value": span / e2e_s, "unit": "terms/s", "h2d_bytes_per_step": 64 * 32,
                "d2h_bytes_per_step": 16, "api": "paper_2407_20205_b200.perm_chunk -> tp_range_sum"}
 
+    strong = None
+    if args.c5_steps > 0:
+        strong = c5_strong(args, rank, world, use_dist, dev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -462,10 +707,11 @@ def main():
             "vs_baseline": None,
             "dtype": "u32",
             "data": "synthetic (reference per-trial splitmix64 stream; no dataset involved)",
-            "config": {"workload": desc, "n": n, "batch": B, "seed": SEED, "parallelism": f"dp{world}",
-                       "l2": "flushed between steps (256 MiB memset, untimed by the walk events)",
-                       "cuda_graph": bool(graph is not None),
-                       "terms_per_step": job_terms},
+            "config": workload_config(wl),
+            "run": {"parallelism": f"dp{world}",
+                    "l2": "flushed between steps (256 MiB memset, untimed by the walk events)",
+                    "cuda_graph": bool(graph is not None),
+                    "terms_per_step": job_terms},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "LOP3 ops/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": kernel_name + " (csrc/" + ("tp_walk_bucket.cu" if "bucket" in kernel_name
@@ -483,6 +729,7 @@ def main():
             "e2e": e2e,
             "gpu_launches": launches,
             "cpu_baseline": cpu,
+            "c5_strong": strong,
         }
         print(json.dumps(line))
     if use_dist:

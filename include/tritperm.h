@@ -9,8 +9,12 @@
  *
  *   tp_range_sum        <- _kernels.chunk_sum        src/_kernels.py:90-128
  *                          (called at src/permanent.py:194,248,251)
+ *   tp_range_sum_ex     <- _kernels.chunk_sum for n = 64 (the reference's
+ *                          big-int twin, src/permanent.py:157-178,192-196)
  *   tp_range_sum_multi  <- the ThreadPool fan-out of perm_mod3_parallel
  *                          src/permanent.py:232-255 (one range per device)
+ *   tp_range_sum_nccl   <- the same, with sum(partials) (:255) as one
+ *                          ncclAllReduce of the counters across the devices
  *   tp_mc_zero_count    <- _kernels.mc_zero_count    src/_kernels.py:245-255
  *                          (called at src/experiments.py:180,183,186)
  *   tp_mc_sample_entries<- _kernels.mc_sample_entries src/_kernels.py:258-272
@@ -37,7 +41,12 @@
  * library-owned stream and a cached workspace per device and are serialised
  * per device.  *_async calls enqueue on the caller's `stream` argument, a
  * cudaStream_t with the usual CUDA meaning (NULL/0 = the legacy default
- * stream), and return without synchronising.
+ * stream), and return without synchronising.  Every device buffer an
+ * *_async call needs internally (row records, bucket tables) is allocated
+ * stream-ordered on that stream (cudaMallocAsync/cudaFreeAsync) and private
+ * to the call: concurrent calls on different streams never share memory,
+ * the calls may be captured into CUDA graphs, and no call synchronises the
+ * device.
  */
 #ifndef TRITPERM_H
 #define TRITPERM_H
@@ -74,6 +83,14 @@ int tp_range_sum(const uint64_t *mags, const uint64_t *sgns, int n,
                  uint64_t lo, uint64_t hi, int device,
                  uint64_t *plus, uint64_t *minus);
 
+/* tp_range_sum extended to n = 64, where the end 2^64 does not fit a
+ * uint64: the range is [lo, hi) if hi_is_2_64 == 0 (any lo <= hi), or
+ * [lo, 2^64) if hi_is_2_64 != 0 (then n must be 64 and hi 0).  For n <= 63 it
+ * is tp_range_sum. */
+int tp_range_sum_ex(const uint64_t *mags, const uint64_t *sgns, int n,
+                    uint64_t lo, uint64_t hi, int hi_is_2_64, int device,
+                    uint64_t *plus, uint64_t *minus);
+
 /* Same, asynchronous: the counters {plus, minus} are ADDED into the device
  * buffer d_pm[2] on `stream`.  Used by the one-process-per-GPU path, which all-reduces d_pm
  * with NCCL. */
@@ -87,6 +104,15 @@ int tp_range_sum_async(const uint64_t *mags, const uint64_t *sgns, int n,
 int tp_range_sum_multi(const uint64_t *mags, const uint64_t *sgns, int n,
                        uint64_t lo, uint64_t hi, const int *devices, int ndev,
                        uint64_t *plus, uint64_t *minus);
+
+/* Same split, but the per-device counters meet on the devices in ONE
+ * in-place ncclAllReduce (uint64[2], sum) over a communicator clique the
+ * library creates once per device list (ncclCommInitAll, cached) and device
+ * 0's copy is read back.  NCCL is dlopen'ed on first use (libnccl.so.2);
+ * TP_E_CUDA if it is unavailable.  Devices are locked in ascending id order. */
+int tp_range_sum_nccl(const uint64_t *mags, const uint64_t *sgns, int n,
+                      uint64_t lo, uint64_t hi, const int *devices, int ndev,
+                      uint64_t *plus, uint64_t *minus);
 
 /* Batch of B matrices, uint8 entries [B][n][n] (host memory; values reduced
  * mod 3, so {0,1,2} classes or any non-negative integers), 1 <= n <= 64.
@@ -135,7 +161,8 @@ int tp_exact_census(int n, int device, int64_t *zeros, int64_t *plus, int64_t *m
 /* Which walk kernel serves full traversals of `batch` matrices of size n
  * (batch = 1: a single matrix or a range), and its LOP3 count per subset
  * term (3 for the lane/wide walks, 2 for the pair walks, 1.5 for the packed
- * walks).  For the bucketed walk (batches, 21 <= n <= 31) the count is per
+ * walks).  For the bucketed walk (21 <= n <= 64: batches, single matrices
+ * and the aligned middle of ranges that fill the GPU) the count is per
  * TESTED pair: it skips the pairs its key columns prove zero, and
  * tp_walk_tested reports how many it tested. */
 int tp_walk_info(int n, long long batch, char *name, int name_len, double *lop3_per_term);

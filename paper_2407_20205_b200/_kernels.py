@@ -48,6 +48,10 @@ SIGNATURES = {
     "tp_device_info": (ctypes.c_int, [ctypes.c_int, _ip, _ip, _ip, _ip]),
     "tp_range_sum": (ctypes.c_int, [_u64p, _u64p, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
                                     _u64p, _u64p]),
+    "tp_range_sum_ex": (ctypes.c_int, [_u64p, _u64p, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
+                                       ctypes.c_int, _u64p, _u64p]),
+    "tp_range_sum_nccl": (ctypes.c_int, [_u64p, _u64p, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, _ip,
+                                         ctypes.c_int, _u64p, _u64p]),
     "tp_range_sum_async": (ctypes.c_int, [_u64p, _u64p, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64,
                                           ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
     "tp_range_sum_multi": (ctypes.c_int, [_u64p, _u64p, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, _ip,
@@ -145,14 +149,30 @@ def _planes(mags, sgns, n: int) -> Tuple[np.ndarray, np.ndarray]:
     return mags, sgns
 
 
+def _check_bounds(n: int, lo: int, hi: int) -> None:
+    """Range bounds in Python ints, before any uint64 conversion (ctypes would
+    silently wrap 2**64 to 0)."""
+    if not 1 <= n <= 64:
+        raise ValueError(f"need 1 <= n <= 64, got n={n}")
+    if not 0 <= lo <= hi <= (1 << n):
+        raise ValueError(f"need 0 <= lo <= hi <= 2**n, got lo={lo} hi={hi} n={n}")
+
+
 def chunk_counts(mags, sgns, n: int, lo: int, hi: int, device: Optional[int] = None) -> Tuple[int, int]:
-    """(plus, minus) term counts over Gray steps [lo, hi)."""
+    """(plus, minus) term counts over Gray steps [lo, hi); n <= 64 (the end
+    2**64 of a 64-row walk goes through tp_range_sum_ex's carry flag)."""
+    _check_bounds(n, lo, hi)
     mags, sgns = _planes(mags, sgns, n)
     dev = default_device() if device is None else device
     p = ctypes.c_uint64()
     m = ctypes.c_uint64()
-    _check(lib().tp_range_sum(mags.ctypes.data_as(_u64p), sgns.ctypes.data_as(_u64p), n, lo, hi, dev,
-                              ctypes.byref(p), ctypes.byref(m)))
+    if n == 64:
+        end64 = hi == 1 << 64
+        _check(lib().tp_range_sum_ex(mags.ctypes.data_as(_u64p), sgns.ctypes.data_as(_u64p), n, lo,
+                                     0 if end64 else hi, 1 if end64 else 0, dev, ctypes.byref(p), ctypes.byref(m)))
+    else:
+        _check(lib().tp_range_sum(mags.ctypes.data_as(_u64p), sgns.ctypes.data_as(_u64p), n, lo, hi, dev,
+                                  ctypes.byref(p), ctypes.byref(m)))
     return int(p.value), int(m.value)
 
 
@@ -162,14 +182,22 @@ def chunk_sum(mags, sgns, n: int, lo: int, hi: int) -> int:
     return p - m
 
 
-def chunk_counts_multi(mags, sgns, n: int, lo: int, hi: int, devices) -> Tuple[int, int]:
-    """(plus, minus) over [lo, hi) split across `devices` (one process)."""
+def chunk_counts_multi(mags, sgns, n: int, lo: int, hi: int, devices, nccl: bool = True) -> Tuple[int, int]:
+    """(plus, minus) over [lo, hi) split across `devices` (one process).
+
+    nccl=True: the per-device counters meet in one ncclAllReduce inside the
+    library (tp_range_sum_nccl); False: summed on the host
+    (tp_range_sum_multi)."""
+    _check_bounds(n, lo, hi)
+    if n > 63:
+        raise ValueError("the multi-device range API needs n <= 63")
     mags, sgns = _planes(mags, sgns, n)
     devs = (ctypes.c_int * len(devices))(*devices)
     p = ctypes.c_uint64()
     m = ctypes.c_uint64()
-    _check(lib().tp_range_sum_multi(mags.ctypes.data_as(_u64p), sgns.ctypes.data_as(_u64p), n, lo, hi, devs,
-                                    len(devices), ctypes.byref(p), ctypes.byref(m)))
+    fn = lib().tp_range_sum_nccl if nccl else lib().tp_range_sum_multi
+    _check(fn(mags.ctypes.data_as(_u64p), sgns.ctypes.data_as(_u64p), n, lo, hi, devs, len(devices),
+              ctypes.byref(p), ctypes.byref(m)))
     return int(p.value), int(m.value)
 
 

@@ -97,12 +97,14 @@ cudaError_t launch_walk_tc(int grid, const TcParams& p, cudaStream_t st);
 // Bucketed pair walk (tp_walk_bucket.cu): 21 <= n <= 64, full traversals and
 // the superblock-aligned middle of ranges.  Items (matrix, piece, chunk);
 // chunk c covers B-side superblocks [F0 + c * nblk, min(F0 + (c + 1) * nblk,
-// s_end)) (superblocks of 2^bucket_v B steps, a B step = 2^14 reference
-// steps); list/ptab come from launch_bucket_group.
+// s_end)) (superblocks of 2^bucket_v B steps, a B step = 2^FIX reference
+// steps).  tab/ptab come from launch_bucket_group: per matrix a compact
+// table of the A side's two halves sorted by their key-column pattern (the
+// pieces' slots are decoded from it, nothing per piece is materialised).
 struct BucketParams {
   FastParams fp;                // items = B * bucket_pieces(cfg) * chunks; F0, nblk in superblocks
-  const void* list;             // [B][pieces][1024] A subsets, uint16 or uint32 (all ones = dummy slot)
-  const uint32_t* ptab;         // [B][pieces] bucket | valid count << 16 (count 0 = unused)
+  const void* tab;              // [B][bucket_tab_bytes] half tables (offsets, subsets, vectors)
+  const uint32_t* ptab;         // [B][pieces] bucket | count << 8 | piece-in-bucket << 20 (count 0 = unused)
   unsigned long long* tested;   // += pairs actually tested (compatible steps x 1024), or nullptr
   unsigned long long s_end;     // end of the superblock region
 };
@@ -112,9 +114,9 @@ struct BucketCfg {
 };
 BucketCfg bucket_cfg(int n, bool packed);
 int bucket_pieces(BucketCfg c);
-size_t bucket_list_elem(BucketCfg c);
+size_t bucket_tab_bytes(BucketCfg c, bool wide);  // per matrix
 int bucket_v(bool packed);
-cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, BucketCfg c, void* list, uint32_t* ptab,
+cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, BucketCfg c, void* tab, uint32_t* ptab,
                                 cudaStream_t st);
 cudaError_t launch_walk_bucket(int grid, const BucketParams& bp, bool packed, cudaStream_t st);
 const void* walk_bucket_symbol(bool packed);

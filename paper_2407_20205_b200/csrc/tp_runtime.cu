@@ -3,15 +3,27 @@
 // The runtime replaces the reference's Python/numba orchestration
 // (src/permanent.py:181-255, src/experiments.py:158-190): it plans a step
 // range into fast (superblock-aligned) and generic (masked) work, owns one
-// stream + a grow-only device workspace per device, launches the sm_100a
-// kernels and folds the per-matrix (plus, minus) counters into classes.
+// stream per device, launches the sm_100a kernels and folds the per-matrix
+// (plus, minus) counters into classes.
+//
+// Memory.  Every buffer a call enqueues work on is private to that call and
+// stream-ordered: cudaMallocAsync on the call's stream before the first
+// launch, cudaFreeAsync after the last (struct Scratch), from the device's
+// default memory pool (kept warm: release threshold kPoolKeep).  So two
+// *_async calls in flight on different streams never share memory, a call
+// captured into a CUDA graph gets graph-owned allocations, and no call ever
+// synchronises the device.  Only synchronous calls (which return after their
+// own stream drained, serialised per device) reuse the grow-only d.ws.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -58,8 +70,6 @@ struct Device {
   int next_queue = 0;
   unsigned long long* tc_err = nullptr;  // tensor-path self-check counter (must stay 0)
   unsigned long long* bucket_tested = nullptr;  // pairs tested by the bucketed walk (tp_walk_tested)
-  void* bucket_ws = nullptr;  // bucket lists of the bucketed walk (grow-only)
-  size_t bucket_ws_size = 0;
   int bucket_blocks_per_sm = 0;
   // Pinned staging for the synchronous single-range call (tp_range_sum): the
   // row table and zeroed counters go up in one async copy, the counters come
@@ -112,17 +122,25 @@ int ensure_device(int dev, Device** out) {
     TP_CUDA(cudaMalloc(&d.bucket_tested, sizeof(unsigned long long)));
     TP_CUDA(cudaMemset(d.bucket_tested, 0, sizeof(unsigned long long)));
     TP_CUDA(cudaMallocHost(&d.stage, Device::kStageBytes));
+    // stream-ordered scratch comes from the default pool: keep up to
+    // kPoolKeep bytes cached across calls instead of returning them at
+    // every synchronisation
+    cudaMemPool_t pool;
+    TP_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = (uint64_t)2 << 30;  // kPoolKeep
+    TP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     d.ready = true;
   }
   *out = &d;
   return TP_OK;
 }
 
-// Grow-only workspace.  Caller holds d.mu and has set the device.
+// Grow-only workspace of the SYNCHRONOUS calls only (each drains its stream
+// before returning, and they are serialised by d.mu, so nothing in flight
+// can still use the old buffer).  Caller holds d.mu and has set the device.
 int ensure_ws(Device& d, size_t bytes) {
   if (d.ws_size >= bytes) return TP_OK;
   if (d.ws) {
-    TP_CUDA(cudaDeviceSynchronize());  // async callers may use ws on their own streams
     TP_CUDA(cudaFree(d.ws));
     d.ws = nullptr;
     d.ws_size = 0;
@@ -134,6 +152,31 @@ int ensure_ws(Device& d, size_t bytes) {
 }
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Stream-ordered per-call scratch (see the header comment): take() enqueues
+// a cudaMallocAsync on the call's stream, and the destructor a cudaFreeAsync
+// of everything taken, after the call's launches.
+struct Scratch {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit Scratch(cudaStream_t s) : st(s) {}
+  Scratch(const Scratch&) = delete;
+  ~Scratch() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+  // 0 or TP_E_CUDA (message set, error state cleared)
+  int take(size_t bytes, void** out) {
+    void* p = nullptr;
+    const cudaError_t e = cudaMallocAsync(&p, std::max<size_t>(bytes, 256), st);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(TP_E_CUDA, "cudaMallocAsync(%zu bytes): %s", bytes, cudaGetErrorString(e));
+    }
+    ptrs.push_back(p);
+    *out = p;
+    return TP_OK;
+  }
+};
 
 // Workspace carve-up for a batch of B matrices.
 struct Carve {
@@ -169,8 +212,9 @@ struct Plan {
   long long bucket_B = 0;
   bool bucket_packed = true;
   tp::BucketCfg bucket_cfg{14, 2};
-  void* bucket_list = nullptr;
+  void* bucket_tab = nullptr;
   uint32_t* bucket_ptab = nullptr;
+  bool host_last = false;  // n = 64, range end 2^64: step 2^64-1 is left to the host (range_sum_impl)
   bool tc = false;  // tensor-core pair test covers the whole plan
   tp::TcParams tcp{};
   int tc_grid = 0;
@@ -237,15 +281,18 @@ unsigned long long* take_queue(Device& d) {
 
 // full = true: the whole range [0, 2^n) of every matrix (n <= 64), planned
 // directly in high steps so n = 64 does not overflow; lo/hi are then unused.
-// Otherwise the reference step range [lo, hi) (hi <= 2^63).
+// Otherwise the reference step range [lo, hi), or [lo, 2^64) when end64 (n =
+// 64, hi ignored; the generic walk's masks cannot express the last step, so
+// a plan whose generic tail reaches it sets host_last).
 //
 // Layout: the fast kernel takes the L-aligned part of the fully covered fast
 // units; the generic kernel takes the rest (range heads/tails, small n) in
-// pieces of kGenericPiece high steps so it parallelises.
+// pieces of kGenericPiece high steps so it parallelises.  The bucketed
+// walk's tables are taken from the call's stream-ordered scratch `sc`.
 constexpr unsigned long long kGenericPiece = 64;
 
-void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, unsigned long long hi, bool full,
-               const RowRec* rows, unsigned long long* pm, Plan& pl) {
+int make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, unsigned long long hi, bool full,
+              const RowRec* rows, unsigned long long* pm, Scratch& sc, Plan& pl, bool end64 = false) {
   pl = Plan();
   pl.nw = n <= 32 ? 1 : 2;
   // Bucketed pair walk over the superblocks [s0, s1) the step range covers
@@ -254,7 +301,7 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
   // superblocks).
   bool bucket_mid = false;
   unsigned long long mid0 = 0, mid1 = 0;  // bucket region in 32-step units (ranges)
-  if (bucket_applies(n, B) && (full || lo < hi)) {
+  if (bucket_applies(n, B) && (full || end64 || lo < hi)) {
     const bool packed = n > 31 || bucket_mode() != 2;  // 2: the unpacked pair tests
     const tp::BucketCfg cfg = tp::bucket_cfg(n, packed);
     const int fix = cfg.fix;  // A side: rows 0..fix-1
@@ -267,7 +314,7 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
     } else {
       const unsigned long long lo0 = lo == 1 ? 0 : lo;  // step 0 contributes 0
       s0 = (lo0 >> sbl) + ((lo0 & ((1ull << sbl) - 1)) ? 1 : 0);
-      s1 = hi >> sbl;
+      s1 = end64 ? 1ull << (64 - sbl) : hi >> sbl;
     }
     // the region must fill the GPU: B * 2^(sbl) * (s1 - s0) >= 2^26
     const bool big = s1 > s0 && (s1 - s0 >= (1ull << (26 - sbl)) || B * (s1 - s0) >= (1ull << (26 - sbl)));
@@ -287,23 +334,18 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
     while (nblk > 1 && (items_of(nblk) < 4 * warps || (nblk > 1024 && items_of(nblk) < per_warp * warps)))
       nblk = (nblk + 1) / 2;
     const unsigned long long chunks = (total + nblk - 1) / nblk;
-    const size_t need = (size_t)B * P * (1024 * tp::bucket_list_elem(cfg) + sizeof(uint32_t));
-    const size_t kBucketWsMax = (size_t)4 << 30;  // larger batches take the default walk
-    if (big && need <= kBucketWsMax && d.bucket_ws_size < need) {
-      cudaDeviceSynchronize();  // earlier launches may still read the old lists
-      if (d.bucket_ws) cudaFree(d.bucket_ws);
-      d.bucket_ws = nullptr;
-      d.bucket_ws_size = 0;
-      if (cudaMalloc(&d.bucket_ws, need) == cudaSuccess) d.bucket_ws_size = need;
-    }
-    if (big && need <= kBucketWsMax && d.bucket_ws_size >= need) {
+    if (big) {
+      // per matrix: the half table (2-14 KB) and the piece table; no cap,
+      // any batch fits (C2: 33 MB; a 65,536-trial n >= 33 slab: 0.9 GB)
+      const size_t tb = align_up(tp::bucket_tab_bytes(cfg, n > 32) * (size_t)B, 256);
+      void* mem = nullptr;
+      if (int rc = sc.take(tb + (size_t)B * P * sizeof(uint32_t), &mem)) return rc;
       pl.bucket = true;
       pl.bucket_packed = packed;
       pl.bucket_B = (long long)B;
       pl.bucket_cfg = cfg;
-      pl.bucket_list = d.bucket_ws;
-      pl.bucket_ptab = reinterpret_cast<uint32_t*>(static_cast<char*>(d.bucket_ws) +
-                                                   (size_t)B * P * 1024 * tp::bucket_list_elem(cfg));
+      pl.bucket_tab = mem;
+      pl.bucket_ptab = reinterpret_cast<uint32_t*>(static_cast<char*>(mem) + tb);
       tp::FastParams& f = pl.bkp.fp;
       f.rows = rows;
       f.pm = pm;
@@ -321,13 +363,13 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
       f.trace = nullptr;
       f.dense_ok = 1;
       f.static_items = 0;
-      pl.bkp.list = pl.bucket_list;
+      pl.bkp.tab = pl.bucket_tab;
       pl.bkp.ptab = pl.bucket_ptab;
       pl.bkp.tested = d.bucket_tested;
       pl.bkp.s_end = s1;
       const unsigned long long ctas = (unsigned long long)d.sm_count * d.bucket_blocks_per_sm;
       pl.bucket_grid = (int)std::max<unsigned long long>(1, std::min(ctas, (f.items + 3) / 4));
-      if (full) return;
+      if (full) return TP_OK;
       bucket_mid = true;
       mid0 = s0 << (sbl - 5);
       mid1 = s1 << (sbl - 5);
@@ -351,7 +393,7 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
     pl.tcp.c0 = 0;
     tp::tc_layout(n, &pl.tcp.R, &pl.tcp.ks);
     pl.tc_grid = (int)std::min<unsigned long long>(pl.tcp.items, (unsigned long long)d.sm_count);
-    return;
+    return TP_OK;
   }
   pl.variant = choose_variant(n, B);
   const int V = tp::fast_v(pl.variant);
@@ -373,17 +415,17 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
     pl.gp.hi = n >= 5 ? ~0ull : (1ull << n);  // n < 5: lanes >= 2^n inactive
     pl.gp.masked = n < 5 ? 1 : 0;
   } else {
-    if (lo >= hi) return;
+    if (lo >= hi && !end64) return TP_OK;
     if (lo == 1) lo = 0;  // step 0 (the empty subset) contributes 0 for n >= 1
-    a_lo = lo >> 5;
-    a_hi = (hi + 31) >> 5;
-    A0 = (lo + 31) >> 5;
-    A1 = hi >> 5;
+    a_lo = lo >> 5;  // (no lo + 31 / hi + 31: n = 64 bounds may be within 31 of 2^64)
+    a_hi = end64 ? 1ull << 59 : (hi >> 5) + ((hi & 31) ? 1 : 0);
+    A0 = (lo >> 5) + ((lo & 31) ? 1 : 0);
+    A1 = end64 ? 1ull << 59 : hi >> 5;
     pl.gp.lo = lo;
-    pl.gp.hi = hi;
+    pl.gp.hi = end64 ? ~0ull : hi;  // end64: the mask keeps i < 2^64 - 1
     pl.gp.masked = 1;
   }
-  if (B == 0) return;
+  if (B == 0) return TP_OK;
 
   // Fast region, in fast units of 2^U high steps, superblocks of 2^V units.
   const unsigned long long A0u = (A0 + (1ull << U) - 1) >> U, A1u = A1 >> U;
@@ -463,13 +505,18 @@ void make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, un
     const unsigned long long need = (pl.gp.items + 7) / 8;
     pl.generic_grid = (int)std::max<unsigned long long>(1, std::min(max_grid, need));
   }
+  // end64: the generic tail, if it reaches the end, masks out step 2^64 - 1
+  pl.host_last = end64 && pl.gp.pieces[1] > 0 && g1b == (1ull << 59);
+  if (end64 && pl.gp.pieces[1] == 0 && pl.gp.pieces[0] > 0 && g0b == (1ull << 59)) pl.host_last = true;
+  return TP_OK;
 }
 
 // Enqueue the walk of plan `pl`; returns launches in *launches.
 int run_plan(const Plan& pl, cudaStream_t st, int* launches) {
   int nl = 0;
   if (pl.bucket) {  // (ranges: plus the generic head and tail below)
-    TP_CUDA(tp::launch_bucket_group(pl.bkp.fp.rows, pl.bucket_B, pl.bkp.fp.n, pl.bucket_cfg, pl.bucket_list, pl.bucket_ptab, st));
+    TP_CUDA(tp::launch_bucket_group(pl.bkp.fp.rows, pl.bucket_B, pl.bkp.fp.n, pl.bucket_cfg, pl.bucket_tab,
+                                    pl.bucket_ptab, st));
     TP_CUDA(tp::launch_walk_bucket(pl.bucket_grid, pl.bkp, pl.bucket_packed, st));
     nl += 2;
   }
@@ -514,34 +561,229 @@ int check_planes(const uint64_t* mags, const uint64_t* sgns, int n) {
   return TP_OK;
 }
 
-// Enqueue one range of one matrix on device d (caller holds d.mu, device set).
-// Counters are added into d_pm[0..1].
+// Enqueue one range of one matrix on device d (caller holds d.mu, device
+// set); the counters are added into d_pm[0..1].  Rows go into the call's
+// own scratch (stream-ordered on st).
 int enqueue_range(Device& d, const uint64_t* mags, const uint64_t* sgns, int n, uint64_t lo, uint64_t hi,
                   unsigned long long* d_pm, cudaStream_t st) {
-  Carve cv;
-  cv.take<RowRec>(nullptr, 64);
-  cv.take<unsigned long long>(nullptr, 1);
-  int rc = ensure_ws(d, cv.off);
-  if (rc) return rc;
-  Carve c2;
-  char* base = static_cast<char*>(d.ws);
-  RowRec* rows = c2.take<RowRec>(base, 64);
+  Scratch sc(st);
+  void* mem = nullptr;
+  if (int rc = sc.take(64 * sizeof(RowRec), &mem)) return rc;
+  RowRec* rows = static_cast<RowRec*>(mem);
   RowRec h[64];
   planes_to_rows(mags, sgns, n, h);
   TP_CUDA(cudaMemcpyAsync(rows, h, sizeof h, cudaMemcpyHostToDevice, st));
   Plan pl;
-  make_plan(d, n, 1, lo, hi, false, rows, d_pm, pl);
+  if (int rc = make_plan(d, n, 1, lo, hi, false, rows, d_pm, sc, pl)) return rc;
   // The H2D above is from pageable memory: it returns once `h` is staged,
   // so `h` may go out of scope before the stream runs.
   return run_plan(pl, st, nullptr);
 }
 
-int check_range(int n, uint64_t lo, uint64_t hi) {
-  if (n < 1 || n > 63) return fail(TP_E_INVALID, "range API needs 1 <= n <= 63, got n=%d", n);
+// end64: the range end is 2^64 (n = 64 only; hi must then be 0); allow64:
+// the caller can take n = 64 (tp_range_sum_ex), whose every u64 hi is <= 2^n.
+int check_range(int n, uint64_t lo, uint64_t hi, bool end64 = false, bool allow64 = false) {
+  if (end64) {
+    if (n != 64 || hi != 0) return fail(TP_E_INVALID, "an end of 2^64 needs n = 64 and hi = 0");
+    return TP_OK;
+  }
+  if (n == 64 && allow64) {
+    if (lo > hi) return fail(TP_E_INVALID, "need lo <= hi, got lo=%llu hi=%llu", (unsigned long long)lo,
+                             (unsigned long long)hi);
+    return TP_OK;
+  }
+  if (n < 1 || n > 63) return fail(TP_E_INVALID, "range API needs 1 <= n <= 63 (n = 64: tp_range_sum_ex), got n=%d", n);
   const uint64_t last = 1ull << n;
   if (!(lo <= hi && hi <= last))
     return fail(TP_E_INVALID, "need 0 <= lo <= hi <= 2**n, got lo=%llu hi=%llu n=%d", (unsigned long long)lo,
                 (unsigned long long)hi, n);
+  return TP_OK;
+}
+
+// Term of the last step 2^64 - 1 of an n = 64 walk: subset gray(2^64 - 1) =
+// {row 63}; full iff row 63 has no zero entry; sign (-1)^(popc(sgn) + 1).
+void last_step_term(const uint64_t* mags, const uint64_t* sgns, uint64_t* plus, uint64_t* minus) {
+  if (mags[63] != ~0ull) return;
+  if (__builtin_popcountll(sgns[63]) & 1) ++*plus;
+  else ++*minus;
+}
+
+// The synchronous single-range call behind tp_range_sum / tp_range_sum_ex.
+int range_sum_impl(const uint64_t* mags, const uint64_t* sgns, int n, uint64_t lo, uint64_t hi, bool end64,
+                   int device, uint64_t* plus, uint64_t* minus, bool allow64 = false) {
+  int rc = check_range(n, lo, hi, end64, allow64);
+  if (rc) return rc;
+  if ((rc = check_planes(mags, sgns, n))) return rc;
+  if (!plus || !minus) return fail(TP_E_INVALID, "plus/minus must not be NULL");
+  Device* d;
+  if ((rc = ensure_device(device, &d))) return rc;
+  std::lock_guard<std::mutex> lk(d->mu);
+  TP_CUDA(cudaSetDevice(device));
+  // device layout = staging layout: 64 RowRec, then the (plus, minus) counters
+  if ((rc = ensure_ws(*d, Device::kStageBytes))) return rc;
+  RowRec* hrows = static_cast<RowRec*>(d->stage);
+  unsigned long long* hpm = reinterpret_cast<unsigned long long*>(hrows + 64);
+  planes_to_rows(mags, sgns, n, hrows);
+  hpm[0] = hpm[1] = 0;
+  RowRec* rows = static_cast<RowRec*>(d->ws);
+  unsigned long long* pm = reinterpret_cast<unsigned long long*>(rows + 64);
+  TP_CUDA(cudaMemcpyAsync(rows, hrows, Device::kStageBytes, cudaMemcpyHostToDevice, d->stream));
+  Plan pl;
+  {
+    Scratch sc(d->stream);
+    if ((rc = make_plan(*d, n, 1, lo, hi, false, rows, pm, sc, pl, end64))) return rc;
+    if ((rc = run_plan(pl, d->stream, nullptr))) return rc;
+  }
+  TP_CUDA(cudaMemcpyAsync(hpm, pm, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, d->stream));
+  TP_CUDA(cudaStreamSynchronize(d->stream));
+  *plus = hpm[0];
+  *minus = hpm[1];
+  if (pl.host_last) last_step_term(mags, sgns, plus, minus);
+  return TP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded on first use (dlopen of libnccl.so.2: the copy torch already
+// loaded if any, else the system one), so the library has no link-time
+// dependency on it.  One communicator clique per device list, cached.
+// ---------------------------------------------------------------------------
+struct Nccl {
+  bool tried = false, ok = false;
+  std::string why;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  std::map<std::vector<int>, std::vector<ncclComm_t>> comms;
+};
+Nccl g_nccl;
+std::mutex g_nccl_mu;
+
+int nccl_load() {
+  Nccl& N = g_nccl;
+  if (!N.tried) {
+    N.tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      N.why = dlerror() ? dlerror() : "dlopen failed";
+    } else {
+      N.CommInitAll = reinterpret_cast<decltype(N.CommInitAll)>(dlsym(h, "ncclCommInitAll"));
+      N.AllReduce = reinterpret_cast<decltype(N.AllReduce)>(dlsym(h, "ncclAllReduce"));
+      N.GroupStart = reinterpret_cast<decltype(N.GroupStart)>(dlsym(h, "ncclGroupStart"));
+      N.GroupEnd = reinterpret_cast<decltype(N.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
+      N.GetErrorString = reinterpret_cast<decltype(N.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+      N.ok = N.CommInitAll && N.AllReduce && N.GroupStart && N.GroupEnd && N.GetErrorString;
+      if (!N.ok) N.why = "libnccl.so.2 lacks a required symbol";
+    }
+  }
+  if (!N.ok) return fail(TP_E_CUDA, "NCCL unavailable: %s", N.why.c_str());
+  return TP_OK;
+}
+
+#define TP_NCCL(call)                                                                                  \
+  do {                                                                                                 \
+    ncclResult_t r_ = (call);                                                                          \
+    if (r_ != ncclSuccess) return fail(TP_E_CUDA, "%s: %s", #call, g_nccl.GetErrorString(r_));         \
+  } while (0)
+
+// Multi-device split of one range (shared by tp_range_sum_multi and
+// tp_range_sum_nccl): part k of split_steps' rule goes to devices[k]; every
+// part is enqueued before any is waited on.  use_nccl: the per-device
+// counters meet in one ncclAllReduce over the clique and device 0's copy is
+// read; otherwise each device's counters are read and summed on the host.
+int range_sum_multi_impl(const uint64_t* mags, const uint64_t* sgns, int n, uint64_t lo, uint64_t hi,
+                         const int* devices, int ndev, bool use_nccl, uint64_t* plus, uint64_t* minus) {
+  int rc = check_range(n, lo, hi);
+  if (rc) return rc;
+  if ((rc = check_planes(mags, sgns, n))) return rc;
+  if (!devices || ndev < 1) return fail(TP_E_INVALID, "need at least one device");
+  if (!plus || !minus) return fail(TP_E_INVALID, "plus/minus must not be NULL");
+  for (int k = 0; k < ndev; ++k)
+    for (int q = 0; q < k; ++q)
+      if (devices[q] == devices[k]) return fail(TP_E_INVALID, "device %d listed twice", devices[k]);
+  std::vector<Device*> ds(ndev);
+  for (int k = 0; k < ndev; ++k)
+    if ((rc = ensure_device(devices[k], &ds[k]))) return rc;
+  std::unique_lock<std::mutex> nlk;
+  std::vector<ncclComm_t>* comms = nullptr;
+  if (use_nccl) {
+    nlk = std::unique_lock<std::mutex>(g_nccl_mu);
+    if ((rc = nccl_load())) return rc;
+    const std::vector<int> key(devices, devices + ndev);
+    auto it = g_nccl.comms.find(key);
+    if (it == g_nccl.comms.end()) {  // communicator init is outside every timed path: once per device list
+      std::vector<ncclComm_t> c(ndev);
+      TP_NCCL(g_nccl.CommInitAll(c.data(), ndev, devices));
+      it = g_nccl.comms.emplace(key, std::move(c)).first;
+    }
+    comms = &it->second;
+  }
+  // lock the devices in ascending id order (concurrent calls listing the
+  // same devices in different orders cannot deadlock)
+  std::vector<int> order(ndev);
+  for (int k = 0; k < ndev; ++k) order[k] = k;
+  std::sort(order.begin(), order.end(), [&](int x, int y) { return devices[x] < devices[y]; });
+  std::vector<std::unique_lock<std::mutex>> locks;
+  for (int k : order) locks.emplace_back(ds[k]->mu);
+  std::vector<unsigned long long*> pms(ndev);
+  std::vector<RowRec> h(64);
+  planes_to_rows(mags, sgns, n, h.data());
+  // Split [lo, hi) like split_steps (src/permanent.py:221-229) and enqueue
+  // every part before waiting on any, so the devices run concurrently.
+  const unsigned long long total = hi - lo;
+  for (int k = 0; k < ndev; ++k) {
+    Device& d = *ds[k];
+    TP_CUDA(cudaSetDevice(d.id));
+    Carve cv;
+    cv.take<RowRec>(nullptr, 64);
+    cv.take<unsigned long long>(nullptr, 2);
+    if ((rc = ensure_ws(d, cv.off))) return rc;
+    char* base = static_cast<char*>(d.ws);
+    Carve c2;
+    RowRec* rows = c2.take<RowRec>(base, 64);
+    pms[k] = c2.take<unsigned long long>(base, 2);
+    const unsigned long long plo = lo + (unsigned long long)((unsigned __int128)total * k / ndev);
+    const unsigned long long phi = lo + (unsigned long long)((unsigned __int128)total * (k + 1) / ndev);
+    TP_CUDA(cudaMemsetAsync(pms[k], 0, 2 * sizeof(unsigned long long), d.stream));
+    TP_CUDA(cudaMemcpyAsync(rows, h.data(), 64 * sizeof(RowRec), cudaMemcpyHostToDevice, d.stream));
+    Plan pl;
+    Scratch sc(d.stream);
+    if ((rc = make_plan(d, n, 1, plo, phi, false, rows, pms[k], sc, pl))) return rc;
+    if ((rc = run_plan(pl, d.stream, nullptr))) return rc;
+  }
+  unsigned long long P = 0, M = 0;
+  if (use_nccl) {
+    // the reference's sum(partials) (src/permanent.py:255) as one in-place
+    // all-reduce of the 16-byte counters over the clique
+    TP_NCCL(g_nccl.GroupStart());
+    for (int k = 0; k < ndev; ++k)
+      TP_NCCL(g_nccl.AllReduce(pms[k], pms[k], 2, ncclUint64, ncclSum, (*comms)[k], ds[k]->stream));
+    TP_NCCL(g_nccl.GroupEnd());
+    unsigned long long hp[2];
+    TP_CUDA(cudaSetDevice(ds[0]->id));
+    TP_CUDA(cudaMemcpyAsync(hp, pms[0], sizeof hp, cudaMemcpyDeviceToHost, ds[0]->stream));
+    for (int k = 0; k < ndev; ++k) {
+      TP_CUDA(cudaSetDevice(ds[k]->id));
+      TP_CUDA(cudaStreamSynchronize(ds[k]->stream));
+    }
+    P = hp[0];
+    M = hp[1];
+  } else {
+    for (int k = 0; k < ndev; ++k) {
+      Device& d = *ds[k];
+      TP_CUDA(cudaSetDevice(d.id));
+      unsigned long long hp[2];
+      TP_CUDA(cudaMemcpyAsync(hp, pms[k], sizeof hp, cudaMemcpyDeviceToHost, d.stream));
+      TP_CUDA(cudaStreamSynchronize(d.stream));
+      P += hp[0];
+      M += hp[1];
+    }
+  }
+  *plus = P;
+  *minus = M;
   return TP_OK;
 }
 
@@ -552,7 +794,7 @@ int check_range(int n, uint64_t lo, uint64_t hi) {
 // ===========================================================================
 extern "C" {
 
-int tp_version(void) { return 100; }
+int tp_version(void) { return 200; }
 
 const char* tp_last_error(void) { return g_err; }
 
@@ -586,31 +828,13 @@ int tp_device_info(int device, int* sm_count, int* max_clock_khz, int* cc_major,
 
 int tp_range_sum(const uint64_t* mags, const uint64_t* sgns, int n, uint64_t lo, uint64_t hi, int device,
                  uint64_t* plus, uint64_t* minus) {
-  int rc = check_range(n, lo, hi);
-  if (rc) return rc;
-  if ((rc = check_planes(mags, sgns, n))) return rc;
-  if (!plus || !minus) return fail(TP_E_INVALID, "plus/minus must not be NULL");
-  Device* d;
-  if ((rc = ensure_device(device, &d))) return rc;
-  std::lock_guard<std::mutex> lk(d->mu);
-  TP_CUDA(cudaSetDevice(device));
-  // device layout = staging layout: 64 RowRec, then the (plus, minus) counters
-  if ((rc = ensure_ws(*d, Device::kStageBytes))) return rc;
-  RowRec* hrows = static_cast<RowRec*>(d->stage);
-  unsigned long long* hpm = reinterpret_cast<unsigned long long*>(hrows + 64);
-  planes_to_rows(mags, sgns, n, hrows);
-  hpm[0] = hpm[1] = 0;
-  RowRec* rows = static_cast<RowRec*>(d->ws);
-  unsigned long long* pm = reinterpret_cast<unsigned long long*>(rows + 64);
-  TP_CUDA(cudaMemcpyAsync(rows, hrows, Device::kStageBytes, cudaMemcpyHostToDevice, d->stream));
-  Plan pl;
-  make_plan(*d, n, 1, lo, hi, false, rows, pm, pl);
-  if ((rc = run_plan(pl, d->stream, nullptr))) return rc;
-  TP_CUDA(cudaMemcpyAsync(hpm, pm, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, d->stream));
-  TP_CUDA(cudaStreamSynchronize(d->stream));
-  *plus = hpm[0];
-  *minus = hpm[1];
-  return TP_OK;
+  return range_sum_impl(mags, sgns, n, lo, hi, false, device, plus, minus);
+}
+
+
+int tp_range_sum_ex(const uint64_t* mags, const uint64_t* sgns, int n, uint64_t lo, uint64_t hi, int hi_is_2_64,
+                    int device, uint64_t* plus, uint64_t* minus) {
+  return range_sum_impl(mags, sgns, n, lo, hi, hi_is_2_64 != 0, device, plus, minus, true);
 }
 
 int tp_range_sum_async(const uint64_t* mags, const uint64_t* sgns, int n, uint64_t lo, uint64_t hi, int device,
@@ -629,58 +853,12 @@ int tp_range_sum_async(const uint64_t* mags, const uint64_t* sgns, int n, uint64
 
 int tp_range_sum_multi(const uint64_t* mags, const uint64_t* sgns, int n, uint64_t lo, uint64_t hi,
                        const int* devices, int ndev, uint64_t* plus, uint64_t* minus) {
-  int rc = check_range(n, lo, hi);
-  if (rc) return rc;
-  if ((rc = check_planes(mags, sgns, n))) return rc;
-  if (!devices || ndev < 1) return fail(TP_E_INVALID, "need at least one device");
-  if (!plus || !minus) return fail(TP_E_INVALID, "plus/minus must not be NULL");
-  for (int k = 0; k < ndev; ++k)
-    for (int q = 0; q < k; ++q)
-      if (devices[q] == devices[k]) return fail(TP_E_INVALID, "device %d listed twice", devices[k]);
-  std::vector<Device*> ds(ndev);
-  for (int k = 0; k < ndev; ++k)
-    if ((rc = ensure_device(devices[k], &ds[k]))) return rc;
-  std::vector<std::unique_lock<std::mutex>> locks;
-  for (int k = 0; k < ndev; ++k) locks.emplace_back(ds[k]->mu);
-  std::vector<unsigned long long*> pms(ndev);
-  std::vector<RowRec> h(64);
-  planes_to_rows(mags, sgns, n, h.data());
-  // Split [lo, hi) like split_steps (src/permanent.py:221-229) and enqueue
-  // every part before waiting on any, so the devices run concurrently.
-  const unsigned long long total = hi - lo;
-  for (int k = 0; k < ndev; ++k) {
-    Device& d = *ds[k];
-    TP_CUDA(cudaSetDevice(d.id));
-    Carve cv;
-    cv.take<RowRec>(nullptr, 64);
-    cv.take<unsigned long long>(nullptr, 1);
-    cv.take<unsigned long long>(nullptr, 2);
-    if ((rc = ensure_ws(d, cv.off))) return rc;
-    char* base = static_cast<char*>(d.ws);
-    Carve c2;
-    RowRec* rows = c2.take<RowRec>(base, 64);
-    pms[k] = c2.take<unsigned long long>(base, 2);
-    const unsigned long long plo = lo + (unsigned long long)((unsigned __int128)total * k / ndev);
-    const unsigned long long phi = lo + (unsigned long long)((unsigned __int128)total * (k + 1) / ndev);
-    TP_CUDA(cudaMemsetAsync(pms[k], 0, 2 * sizeof(unsigned long long), d.stream));
-    TP_CUDA(cudaMemcpyAsync(rows, h.data(), 64 * sizeof(RowRec), cudaMemcpyHostToDevice, d.stream));
-    Plan pl;
-    make_plan(d, n, 1, plo, phi, false, rows, pms[k], pl);
-    if ((rc = run_plan(pl, d.stream, nullptr))) return rc;
-  }
-  unsigned long long P = 0, M = 0;
-  for (int k = 0; k < ndev; ++k) {
-    Device& d = *ds[k];
-    TP_CUDA(cudaSetDevice(d.id));
-    unsigned long long hp[2];
-    TP_CUDA(cudaMemcpyAsync(hp, pms[k], sizeof hp, cudaMemcpyDeviceToHost, d.stream));
-    TP_CUDA(cudaStreamSynchronize(d.stream));
-    P += hp[0];
-    M += hp[1];
-  }
-  *plus = P;
-  *minus = M;
-  return TP_OK;
+  return range_sum_multi_impl(mags, sgns, n, lo, hi, devices, ndev, false, plus, minus);
+}
+
+int tp_range_sum_nccl(const uint64_t* mags, const uint64_t* sgns, int n, uint64_t lo, uint64_t hi,
+                      const int* devices, int ndev, uint64_t* plus, uint64_t* minus) {
+  return range_sum_multi_impl(mags, sgns, n, lo, hi, devices, ndev, true, plus, minus);
 }
 
 int tp_perm_batch_async(const uint8_t* d_entries, int64_t B, int n, int device, int8_t* d_class, uint64_t* d_pm,
@@ -696,16 +874,13 @@ int tp_perm_batch_async(const uint8_t* d_entries, int64_t B, int n, int device, 
   std::lock_guard<std::mutex> lk(d->mu);
   TP_CUDA(cudaSetDevice(device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);  // 0 = legacy default stream, as in CUDA
-  Carve cv;
-  cv.take<RowRec>(nullptr, (size_t)B * 64);
-  cv.take<unsigned long long>(nullptr, 1);
-  if (!d_pm) cv.take<unsigned long long>(nullptr, (size_t)B * 2);
-  if ((rc = ensure_ws(*d, cv.off))) return rc;
-  char* base = static_cast<char*>(d->ws);
-  Carve c2;
-  RowRec* rows = c2.take<RowRec>(base, (size_t)B * 64);
-  unsigned long long* pm =
-      d_pm ? reinterpret_cast<unsigned long long*>(d_pm) : c2.take<unsigned long long>(base, (size_t)B * 2);
+  Scratch sc(st);
+  void* mem = nullptr;
+  const size_t rbytes = align_up((size_t)B * 64 * sizeof(RowRec), 256);
+  if ((rc = sc.take(rbytes + (d_pm ? 0 : (size_t)B * 2 * sizeof(unsigned long long)), &mem))) return rc;
+  RowRec* rows = static_cast<RowRec*>(mem);
+  unsigned long long* pm = d_pm ? reinterpret_cast<unsigned long long*>(d_pm)
+                                : reinterpret_cast<unsigned long long*>(static_cast<char*>(mem) + rbytes);
   int nl = 0;
   TP_CUDA(cudaMemsetAsync(pm, 0, (size_t)B * 2 * sizeof(unsigned long long), st));
   if (n <= tp::kSmallMaxN) {  // thread per matrix: pack + walk + finalise in one kernel
@@ -717,7 +892,7 @@ int tp_perm_batch_async(const uint8_t* d_entries, int64_t B, int n, int device, 
   TP_CUDA(tp::launch_pack(d_entries, B, n, rows, pack_grid, st));
   nl++;
   Plan pl;
-  make_plan(*d, n, (unsigned long long)B, 0, 0, true, rows, pm, pl);
+  if ((rc = make_plan(*d, n, (unsigned long long)B, 0, 0, true, rows, pm, sc, pl))) return rc;
   if ((rc = run_plan(pl, st, &nl))) return rc;
   if (d_class || d_hist) {
     TP_CUDA(tp::launch_finalize(pm, B, n, d_class, nullptr, reinterpret_cast<long long*>(d_hist), st));
@@ -755,9 +930,11 @@ int tp_walk_async(const void* d_rows, int64_t B, int n, int device, uint64_t* d_
   std::lock_guard<std::mutex> lk(d->mu);
   TP_CUDA(cudaSetDevice(device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);  // 0 = legacy default stream, as in CUDA
+  Scratch sc(st);
   Plan pl;
-  make_plan(*d, n, (unsigned long long)B, 0, 0, true, static_cast<const RowRec*>(d_rows),
-            reinterpret_cast<unsigned long long*>(d_pm), pl);
+  if ((rc = make_plan(*d, n, (unsigned long long)B, 0, 0, true, static_cast<const RowRec*>(d_rows),
+                      reinterpret_cast<unsigned long long*>(d_pm), sc, pl)))
+    return rc;
   return run_plan(pl, st, launches);
 }
 
@@ -771,10 +948,13 @@ int tp_walk_range_async(const void* d_rows, int n, uint64_t lo, uint64_t hi, int
   if ((rc = ensure_device(device, &d))) return rc;
   std::lock_guard<std::mutex> lk(d->mu);
   TP_CUDA(cudaSetDevice(device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Scratch sc(st);
   Plan pl;
-  make_plan(*d, n, 1, lo, hi, false, static_cast<const RowRec*>(d_rows), reinterpret_cast<unsigned long long*>(d_pm),
-            pl);
-  return run_plan(pl, static_cast<cudaStream_t>(stream), launches);
+  if ((rc = make_plan(*d, n, 1, lo, hi, false, static_cast<const RowRec*>(d_rows),
+                      reinterpret_cast<unsigned long long*>(d_pm), sc, pl)))
+    return rc;
+  return run_plan(pl, st, launches);
 }
 
 int tp_finalize_async(const uint64_t* d_pm, int64_t B, int n, int device, int8_t* d_class, int64_t* d_hist,
@@ -938,7 +1118,8 @@ int tp_perm_batch(const uint8_t* entries, int64_t B, int n, int device, int8_t* 
     const int pack_grid = (int)std::min<long long>((B + 7) / 8, (long long)d->sm_count * 8);
     TP_CUDA(tp::launch_pack(dent, B, n, rows, pack_grid, st));
     Plan pl;
-    make_plan(*d, n, (unsigned long long)B, 0, 0, true, rows, pm, pl);
+    Scratch sc(st);
+    if ((rc = make_plan(*d, n, (unsigned long long)B, 0, 0, true, rows, pm, sc, pl))) return rc;
     if ((rc = run_plan(pl, st, nullptr))) return rc;
     TP_CUDA(tp::launch_finalize(pm, B, n, dcls, dpart, dhist, st));
   }
@@ -999,7 +1180,8 @@ static int mc_run(int n, int64_t t0, int64_t count, uint64_t seed, int device, i
       TP_CUDA(cudaMemsetAsync(pm, 0, (size_t)B * 2 * sizeof(unsigned long long), st));
       TP_CUDA(tp::launch_sample(n, t0 + s0, B, seed, rows, nullptr, st));
       Plan pl;
-      make_plan(*d, n, (unsigned long long)B, 0, 0, true, rows, pm, pl);
+      Scratch sc(st);
+      if ((rc = make_plan(*d, n, (unsigned long long)B, 0, 0, true, rows, pm, sc, pl))) return rc;
       if ((rc = run_plan(pl, st, nullptr))) return rc;
       TP_CUDA(tp::launch_finalize(pm, B, n, dcls, nullptr, dhist, st));
     }

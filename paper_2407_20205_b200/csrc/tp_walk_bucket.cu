@@ -38,85 +38,197 @@ namespace {
 
 // Bucket configurations (bucket_cfg): A side = rows 0..FIX-1, sorted by the
 // trits of KEYS key columns into 3^KEYS buckets; pieces per matrix:
-// 2^(FIX-10) full ones plus one partial per bucket.  Lists of FIX > 15 hold
-// uint32 subsets (0xFFFF is a real subset of 16 rows).
+// 2^(FIX-10) full ones plus one partial per bucket.
 __host__ __device__ constexpr int nbuckets(int keys) { return keys == 2 ? 9 : 27; }
 __host__ __device__ constexpr int pieces_of(int fix, int keys) { return (1 << (fix - 10)) + nbuckets(keys); }
-template <int FIX>
-using list_t = typename std::conditional<(FIX > 15), uint32_t, uint16_t>::type;
+__host__ __device__ constexpr int align16(int x) { return (x + 15) & ~15; }
+
+// Key pattern arithmetic: a pattern is the base-3 number of the trits on the
+// key columns (first key column most significant); the pattern of a sum is
+// the digit-wise sum mod 3.
+template <int KEYS>
+__host__ __device__ __forceinline__ uint32_t pat_sub(uint32_t g, uint32_t a) {
+  uint32_t r = 0, m = 1;
+#pragma unroll
+  for (int i = 0; i < KEYS; ++i) {
+    r += ((g % 3u + 3u - a % 3u) % 3u) * m;
+    g /= 3u;
+    a /= 3u;
+    m *= 3u;
+  }
+  return r;
+}
+
+// Per-matrix bucket table.  The A side (rows 0..FIX-1) splits into a low
+// half (rows 0..TB-1) and a high half (rows TB..FIX-1); an A subset is a pair
+// (low subset, high subset) and its vector the sum of the halves' vectors, so
+// its key pattern is pat(low) + pat(high) digit-wise.  Bucket g is therefore
+// the union over low patterns a of  low_a x high_(g - a),  and the table only
+// holds each half sorted by pattern:
+//   u16 off[2][NB + 1]     start of each pattern's run in the sorted half
+//   u16 sub[N0 + N1]       the sorted subsets (low half, then high half)
+//   vec[N0 + N1]           their vectors: low (z, g) words, high in row form
+//                          (m, a = m ^ s), so slot = one 3-LOP3 add; WIDE
+//                          tables carry both 32-column words (16 bytes)
+// Position p of bucket g is decoded by walking the runs a = 0, 1, ..: run a
+// holds |low_a| * |high_(g-a)| subsets, low index fastest.  A piece of 1024
+// slots is positions [1024 q, 1024 q + 1024) of its bucket (ptab).
+// Replaces the materialised per-piece subset lists of round 1 (2 KB per
+// piece, 35x the input bytes in HBM on C2): a C2 table is 1,968 bytes per
+// matrix against 17 pieces x 2 KB.
+template <int FIX, int KEYS, bool WIDE>
+struct Tab {
+  static constexpr int NB = nbuckets(KEYS);
+  static constexpr int TB = (FIX + 1) / 2, HB = FIX - TB;
+  static constexpr int N0 = 1 << TB, N1 = 1 << HB;
+  static constexpr int VE = WIDE ? 16 : 8;  // bytes per vector entry
+  static constexpr int kSub = align16(4 * (NB + 1));
+  static constexpr int kVec = kSub + align16(2 * (N0 + N1));
+  static constexpr int kBytes = kVec + VE * (N0 + N1);
+};
+
+// Sequential decoder of bucket positions (monotone p): the current run a,
+// its position range [start, end), the halves' run offsets and the low
+// run's length c0.  Reads the table's offsets (L1-resident).
+template <int KEYS>
+struct RunCursor {
+  const uint16_t* off;  // off[0..NB] low half, off[NB+1..2NB+1] high half
+  uint32_t grp, a, start, end, o0, o1, c0;
+  __device__ __forceinline__ void load() {
+    constexpr uint32_t NB = nbuckets(KEYS);
+    const uint32_t ga = pat_sub<KEYS>(grp, a);
+    o0 = off[a];
+    c0 = off[a + 1] - o0;
+    o1 = off[NB + 1 + ga];
+    end = start + c0 * (uint32_t)(off[NB + 2 + ga] - o1);
+  }
+  __device__ __forceinline__ void init(const uint16_t* o, uint32_t g) {
+    off = o;
+    grp = g;
+    a = 0;
+    start = 0;
+    load();
+  }
+  // requires p < the bucket's size and p >= every earlier p
+  __device__ __forceinline__ void seek(uint32_t p) {
+    while (p >= end) {
+      ++a;
+      start = end;
+      load();
+    }
+  }
+  // table indices (low, high) of position p (after seek(p))
+  __device__ __forceinline__ void index(uint32_t p, uint32_t& i0, uint32_t& i1) const {
+    const uint32_t rel = p - start, j = rel / c0;
+    i0 = o0 + (rel - j * c0);
+    i1 = o1 + j;
+  }
+};
 
 // ----------------------------------------------------------------- grouping
-// One CTA per matrix: key digits of all 2^FIX A subsets from two half
-// tables (the low / high rows' subsets) and a digit-wise sum table, a
-// counting sort into the buckets (per-warp counters), pieces of 1024.
-template <int FIX, int KEYS>
-__global__ void __launch_bounds__(512) k_bucket_group(const RowRec* rows, int n, list_t<FIX>* list, uint32_t* ptab) {
-  using LT = list_t<FIX>;
-  constexpr int NB = nbuckets(KEYS), P = pieces_of(FIX, KEYS);
-  constexpr int TB = (FIX + 1) / 2, NW = 16;
-  __shared__ uint8_t tab[2][1 << TB];  // bucket digits of the low / high rows' subsets
-  __shared__ uint8_t comb[NB][NB];     // digit-wise sum mod 3
-  __shared__ uint32_t cw[NW][NB];      // per-warp counts, then scatter positions
-  __shared__ uint32_t cnt[NB], pstart[NB], pos[NB];
-  const RowRec* R = rows + (size_t)blockIdx.x * 64;
-  LT* L = list + (size_t)blockIdx.x * P * 1024;
-  uint32_t* Pt = ptab + (size_t)blockIdx.x * P;
+// One CTA per matrix: every half subset's vector and key pattern, a
+// deterministic counting sort of each half by pattern (rank = earlier
+// entries with the same half and pattern), the table, then the bucket sizes
+// sum_a |low_a| |high_(g-a)| and the pieces (ptab).
+template <int FIX, int KEYS, bool WIDE>
+__global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n, uint8_t* tab, uint32_t* ptab) {
+  using T = Tab<FIX, KEYS, WIDE>;
+  constexpr int NB = T::NB, N0 = T::N0, NE = T::N0 + T::N1, NT = 256, NW = NT / 32;
+  constexpr int EPT = (NE + NT - 1) / NT, NK = 2 * NB, P = pieces_of(FIX, KEYS);
+  __shared__ RowRec R[FIX];
+  __shared__ uint32_t wcnt[NW][NK];  // per-warp key counts of the current round
+  __shared__ uint32_t kcnt[NK];      // key counts of the earlier rounds, then totals
+  __shared__ uint32_t offs[2][NB + 1];
+  __shared__ uint32_t bsize[NB];
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(rows + (size_t)blockIdx.x * 64);
+    if (tid < 2 * FIX) reinterpret_cast<uint4*>(R)[tid] = src[tid];
+  }
+  if (tid < (uint32_t)NK) kcnt[tid] = 0;
+  uint8_t* Tm = tab + (size_t)blockIdx.x * T::kBytes;
   const int k1 = (n < 32 ? n : 32) - 1;  // key columns k1, k1-1 (, k1-2): primary word for n > 32
-  const uint32_t warp = threadIdx.x >> 5;
-  auto trit = [&](int r, int k) -> uint32_t {
-    const uint32_t m = (R[r].m[0] >> k) & 1u, s = (R[r].s[0] >> k) & 1u;
-    return m ? (s ? 2u : 1u) : 0u;
-  };
-  auto enc = [](uint32_t d0, uint32_t d1, uint32_t d2) -> uint32_t {
-    return KEYS == 2 ? 3 * (d0 % 3) + d1 % 3 : 9 * (d0 % 3) + 3 * (d1 % 3) + d2 % 3;
-  };
-  for (uint32_t e = threadIdx.x; e < (2u << TB); e += blockDim.x) {
-    const uint32_t half = e >> TB, sub = e & ((1u << TB) - 1u);
-    uint32_t x[3] = {0, 0, 0};
-    for (int bt = 0; bt < TB; ++bt) {
-      const int r = TB * (int)half + bt;
-      if (r < FIX && ((sub >> bt) & 1u))
-        for (int i = 0; i < KEYS; ++i) x[i] += trit(r, k1 - i);
+  const uint32_t cm0 = n >= 32 ? 0xffffffffu : (1u << n) - 1u;
+  const uint32_t cm1 = n <= 32 ? 0u : n >= 64 ? 0xffffffffu : (1u << (n - 32)) - 1u;
+  uint32_t key[EPT], rank[EPT], sub[EPT];
+  uint4 vec[EPT];
+#pragma unroll
+  for (int q = 0; q < EPT; ++q) {
+    __syncthreads();  // R loaded / the previous round's wcnt consumed
+    for (uint32_t e = tid; e < (uint32_t)(NW * NK); e += NT) wcnt[e / NK][e % NK] = 0;
+    const uint32_t e = (uint32_t)q * NT + tid;
+    const bool act = e < (uint32_t)NE;
+    const uint32_t h = e >= (uint32_t)N0 ? 1u : 0u;
+    const uint32_t s = h ? e - N0 : e;
+    uint32_t z0 = cm0, g0 = 0, z1 = cm1, g1 = 0;
+    if (act) {
+      for (uint32_t x = s; x; x &= x - 1) {
+        const int r = __ffs(x) - 1 + (h ? T::TB : 0);
+        sub_word(z0, g0, R[r].m[0], R[r].a[0]);
+        if (WIDE) sub_word(z1, g1, R[r].m[1], R[r].a[1]);
+      }
     }
-    tab[half][sub] = (uint8_t)enc(x[0], x[1], x[2]);
+    auto trit = [&](int c) -> uint32_t { return ((z0 >> c) & 1u) ? 0u : ((g0 >> c) & 1u) ? 2u : 1u; };
+    const uint32_t pat = KEYS == 2 ? 3u * trit(k1) + trit(k1 - 1) : 9u * trit(k1) + 3u * trit(k1 - 1) + trit(k1 - 2);
+    key[q] = act ? h * NB + pat : 0xFFFFu;
+    sub[q] = s;
+    if (h) {  // high half in row form: the slot adds it with one sub_word
+      const uint32_t m0 = ~z0 & cm0, m1 = ~z1 & cm1;
+      vec[q] = make_uint4(m0, m0 ^ (g0 & m0), m1, m1 ^ (g1 & m1));
+    } else {
+      vec[q] = make_uint4(z0, g0, z1, g1);
+    }
+    const uint32_t mm = __match_any_sync(FULL, key[q]);
+    __syncthreads();  // wcnt cleared
+    if (act && lane == (uint32_t)(__ffs(mm) - 1)) wcnt[warp][key[q]] = __popc(mm);
+    __syncthreads();
+    if (act) {
+      uint32_t r = kcnt[key[q]] + __popc(mm & ((1u << lane) - 1u));
+      for (uint32_t w = 0; w < warp; ++w) r += wcnt[w][key[q]];
+      rank[q] = r;
+    }
+    __syncthreads();
+    if (tid < (uint32_t)NK) {
+      uint32_t c = 0;
+      for (int w = 0; w < NW; ++w) c += wcnt[w][tid];
+      kcnt[tid] += c;
+    }
   }
-  for (uint32_t e = threadIdx.x; e < (uint32_t)(NB * NB); e += blockDim.x) {
-    const uint32_t a = e / NB, c = e % NB;
-    comb[a][c] = KEYS == 2 ? (uint8_t)enc(a / 3 + c / 3, a + c, 0)
-                           : (uint8_t)enc(a / 9 + c / 9, a / 3 + c / 3, a + c);
+  __syncthreads();
+  if (tid < 2) {  // run offsets of each half
+    uint32_t o = 0;
+    for (int a = 0; a < NB; ++a) {
+      offs[tid][a] = o;
+      o += kcnt[tid * NB + a];
+    }
+    offs[tid][NB] = o;
   }
-  for (uint32_t e = threadIdx.x; e < (uint32_t)(NW * NB); e += blockDim.x) cw[e / NB][e % NB] = 0;
   __syncthreads();
-  auto pat = [&](uint32_t s) -> uint32_t { return comb[tab[0][s & ((1u << TB) - 1u)]][tab[1][s >> TB]]; };
-  for (uint32_t s = threadIdx.x; s < (1u << FIX); s += blockDim.x) atomicAdd(&cw[warp][pat(s)], 1u);
-  __syncthreads();
-  if (threadIdx.x < (uint32_t)NB) {  // bucket totals, one thread per bucket
+  if (tid < (uint32_t)(2 * (NB + 1))) reinterpret_cast<uint16_t*>(Tm)[tid] = (uint16_t)offs[tid / (NB + 1)][tid % (NB + 1)];
+  if (tid < (uint32_t)NB) {
     uint32_t c = 0;
-    for (int w = 0; w < NW; ++w) c += cw[w][threadIdx.x];
-    cnt[threadIdx.x] = c;
+    for (uint32_t a = 0; a < (uint32_t)NB; ++a) c += kcnt[a] * kcnt[NB + pat_sub<KEYS>(tid, a)];
+    bsize[tid] = c;
+  }
+  uint16_t* subs = reinterpret_cast<uint16_t*>(Tm + T::kSub);
+#pragma unroll
+  for (int q = 0; q < EPT; ++q) {
+    if (key[q] == 0xFFFFu) continue;
+    const uint32_t h = key[q] >= (uint32_t)NB ? 1u : 0u;
+    const uint32_t idx = h * N0 + offs[h][key[q] - h * NB] + rank[q];
+    subs[idx] = (uint16_t)sub[q];
+    if (WIDE) reinterpret_cast<uint4*>(Tm + T::kVec)[idx] = vec[q];
+    else reinterpret_cast<uint2*>(Tm + T::kVec)[idx] = make_uint2(vec[q].x, vec[q].y);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
+    uint32_t* Pt = ptab + (size_t)blockIdx.x * P;
     uint32_t piece = 0;
-    for (int g = 0; g < NB; ++g) {
-      const uint32_t c = cnt[g];
-      pstart[g] = piece;
-      pos[g] = piece * 1024u;
-      const uint32_t np = (c + 1023u) / 1024u;
-      for (uint32_t q = 0; q < np; ++q) Pt[piece + q] = (uint32_t)g | (min(1024u, c - 1024u * q) << 16);
-      piece += np;
+    for (uint32_t g = 0; g < (uint32_t)NB; ++g) {
+      const uint32_t c = bsize[g];
+      for (uint32_t q = 0; 1024u * q < c; ++q) Pt[piece++] = g | (min(1024u, c - 1024u * q) << 8) | (q << 20);
     }
-    for (uint32_t q = piece; q < (uint32_t)P; ++q) Pt[q] = 0;  // unused pieces: count 0
-  }
-  __syncthreads();
-  // scatter in arrival order (one counter per bucket): a lane's slots are
-  // then spread over the whole subset range, which keeps filter passes from
-  // clustering in one lane (per-warp ranges measured 4 % slower on C2)
-  for (uint32_t s = threadIdx.x; s < (1u << FIX); s += blockDim.x) L[atomicAdd(&pos[pat(s)], 1u)] = (LT)s;
-  // dummy slots: the tail of each bucket's last piece (unused pieces are never read)
-  for (int g = 0; g < NB; ++g) {
-    const uint32_t end = pstart[g] * 1024u + cnt[g], pend = pstart[g] * 1024u + ((cnt[g] + 1023u) & ~1023u);
-    for (uint32_t i = end + threadIdx.x; i < pend; i += blockDim.x) L[i] = (LT)~0u;
+    for (; piece < (uint32_t)P; ++piece) Pt[piece] = 0;  // unused pieces: count 0
   }
 }
 
@@ -189,22 +301,31 @@ static __device__ __noinline__ unsigned long long bucket_exact_packed(const uint
 // with at most 64 W real slots runs the filter on W words only.
 __device__ __forceinline__ uint32_t lrow(int k) { return 2u * (uint32_t)(k & 15) + ((uint32_t)k >> 4); }
 
-// n > 32: the secondary word (columns 32..n-1) of A subset s, from scratch.
-__device__ __forceinline__ void a_word1(const RowRec* R, uint32_t s, uint32_t z1i, uint32_t& z, uint32_t& g) {
-  z = z1i;
-  g = 0;
-#pragma unroll 1
-  for (uint32_t x = s; x; x &= x - 1) {
-    const int t = __ffs(x) - 1;
-    sub_word(z, g, R[t].m[1], R[t].a[1]);
-  }
+// n > 32: the secondary word (columns 32..n-1) of the A subset at position
+// p of bucket grp, from the table (random access: the runs are walked from
+// the first; rare paths only).
+template <int FIX, int KEYS>
+__device__ __forceinline__ void a_word1(const uint8_t* Tm, uint32_t grp, uint32_t p, uint32_t& z, uint32_t& g) {
+  using T = Tab<FIX, KEYS, true>;
+  RunCursor<KEYS> c;
+  c.init(reinterpret_cast<const uint16_t*>(Tm), grp);
+  c.seek(p);
+  uint32_t i0, i1;
+  c.index(p, i0, i1);
+  const uint4* v = reinterpret_cast<const uint4*>(Tm + T::kVec);
+  const uint4 lo = v[i0], hi = v[T::N0 + i1];
+  z = lo.z;
+  g = lo.w;
+  sub_word(z, g, hi.z, hi.w);
 }
 
 // n > 32, a pair whose 32 primary columns are all nonzero: 1 | parity of the
 // secondary sign word << 1 if the secondary columns are nonzero too, else 0.
-static __device__ __noinline__ uint32_t bucket_wide_term(const RowRec* R, uint32_t s, uint2 h1, uint32_t z1i) {
+template <int FIX, int KEYS>
+static __device__ __noinline__ uint32_t bucket_wide_term(const uint8_t* Tm, uint32_t grp, uint32_t p, uint2 h1,
+                                                         uint32_t z1i) {
   uint32_t za, ga, d, zp;
-  a_word1(R, s, z1i, za, ga);
+  a_word1<FIX, KEYS>(Tm, grp, p, za, ga);
   TP_LOP3(d, za, ga, h1.y, 0x06);
   TP_LOP3(zp, d, za, h1.x, 0x09);
   if (zp != 0) return 0u;
@@ -212,19 +333,30 @@ static __device__ __noinline__ uint32_t bucket_wide_term(const RowRec* R, uint32
 }
 
 // n > 32: exact evaluation of the steps in `mask` against this lane's real
-// slots, both words (dense mode, list overflow).  Slot-major, so each slot's
-// secondary word is built once.  Returns ev | odd << 32.
-template <class LT>
+// slots, both words (dense mode, list overflow).  Slot-major in position
+// order (one run cursor), so each slot's secondary word is built once.
+// Returns ev | odd << 32.
+template <int FIX, int KEYS>
 static __device__ __noinline__ unsigned long long bucket_exact_wide(const uint4 (*A2)[32], const uint4* H,
-                                                                    const uint2* H1, const RowRec* R,
-                                                                    const LT* Lp, uint32_t mask, uint32_t lane,
-                                                                    uint32_t spm, uint32_t vmask, uint32_t z1i) {
+                                                                    const uint2* H1, const uint8_t* Tm,
+                                                                    uint32_t grp, uint32_t pbase, uint32_t cnt,
+                                                                    uint32_t mask, uint32_t lane, uint32_t spm,
+                                                                    uint32_t z1i) {
+  using T = Tab<FIX, KEYS, true>;
+  const uint4* vec = reinterpret_cast<const uint4*>(Tm + T::kVec);
+  RunCursor<KEYS> cur;
+  cur.init(reinterpret_cast<const uint16_t*>(Tm), grp);
   uint32_t ev = 0, odd = 0;
 #pragma unroll 1
-  for (int k = 0; k < 32; ++k) {
-    if (!((vmask >> k) & 1u)) continue;
-    uint32_t za1, ga1;
-    a_word1(R, Lp[32 * lrow(k) + lane], z1i, za1, ga1);
+  for (uint32_t r = 0; 32u * r + lane < cnt; ++r) {  // this lane's real slots: rows r = lrow(k)
+    const uint32_t k = (r >> 1) + ((r & 1u) << 4);
+    const uint32_t p = pbase + 32u * r + lane;
+    uint32_t i0, i1;
+    cur.seek(p);
+    cur.index(p, i0, i1);
+    const uint4 lo = vec[i0], hi = vec[T::N0 + i1];
+    uint32_t za1 = lo.z, ga1 = lo.w;
+    sub_word(za1, ga1, hi.z, hi.w);
     const uint4 a4 = A2[k & 15][lane];
     const uint32_t za = k < 16 ? a4.x : a4.z, ga = k < 16 ? a4.y : a4.w;
     const uint32_t kp = (spm >> k) & 1u;
@@ -256,7 +388,7 @@ static __device__ __noinline__ unsigned long long bucket_exact_wide(const uint4 
 // the 2-key kernel 4 % on C2 and gains the 3-key kernels 3-5 % on C3-C5.
 struct BucketParamsCfg {  // BucketParams' fields, then the configuration
   FastParams fp;
-  const void* list;
+  const void* tab;
   const uint32_t* ptab;
   unsigned long long* tested;
   unsigned long long s_end;
@@ -278,7 +410,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
   constexpr int KB = 5;
   constexpr int K = 1 << KB;
   constexpr int kBucketPieces = pieces_of(FIX, KEYS);
-  using LT = list_t<FIX>;
+  using T = Tab<FIX, KEYS, WIDE>;
   constexpr int SB = 1 << V;
   const FastParams& p = bp.fp;
   static_assert(PACKED || !WIDE, "n > 32 needs the packed filter");
@@ -321,43 +453,54 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
     const uint32_t nsb = (uint32_t)min((unsigned long long)p.nblk, bp.s_end - sb0);
     const unsigned long long A0 = sb0 << V;
     const uint32_t pt = bp.ptab[b * kBucketPieces + q];
-    if ((pt >> 16) == 0) continue;  // unused piece
-    const uint32_t grp = pt & 0xFFFFu;
-    const uint32_t nwd = ((pt >> 16) + 63u) >> 6;  // packed words holding the piece's real slots
+    const uint32_t cnt = (pt >> 8) & 0xFFFu;  // real slots of the piece
+    if (cnt == 0) continue;  // unused piece
+    const uint32_t grp = pt & 0xFFu;
+    const uint32_t pbase = (pt >> 20) << 10;  // the piece is positions [pbase, pbase + cnt) of its bucket
+    const uint32_t nwd = (cnt + 63u) >> 6;  // packed words holding the piece's real slots
     __syncwarp();
     load_rows(R, p.rows + b * 64, lane, p.n);
     __syncwarp();
 
-    // A side: slot k of this lane is the A subset list[piece][32 k + lane];
-    // full words in shared memory (verify, exact fallback), registers: the
-    // unpacked walk keeps all 32 slots, the packed one only the packed words
-    // (low 16 columns of slot w in the low half, of slot w + 16 in the high)
+    // A side: slot k of this lane is position pbase + 32 lrow(k) + lane of
+    // the bucket, decoded from the matrix's table (low-half vector + high-half
+    // row: one 3-LOP3 add); full words in shared memory (verify, exact
+    // fallback), registers: the unpacked walk keeps all 32 slots, the packed
+    // one only the packed words (low 16 columns of slot w in the low half, of
+    // slot w + 16 in the high).  Slots are built in position order, so one
+    // run cursor serves them all.
     uint32_t z1[PACKED ? 1 : K], g1[PACKED ? 1 : K];
     uint32_t Zp[PACKED ? K / 2 : 1], Gp[PACKED ? K / 2 : 1];
     uint32_t spm = 0;  // bit k: parity of slot k's subset
     uint32_t vmask = 0;  // bit k: slot k holds a real A subset (not padding)
-    const LT* Lp = static_cast<const LT*>(bp.list) + (b * kBucketPieces + q) * 1024;
+    const uint8_t* Tm = static_cast<const uint8_t*>(bp.tab) + b * T::kBytes;
     {
+      const uint16_t* subs = reinterpret_cast<const uint16_t*>(Tm + T::kSub);
+      RunCursor<KEYS> cur;
+      cur.init(reinterpret_cast<const uint16_t*>(Tm), grp);
       auto slot = [&](int k, uint32_t& z, uint32_t& g) {
-        const uint32_t s = Lp[32 * lrow(k) + lane];
-        z = colmask;
-        g = 0;
-        if (s == (uint32_t)(LT)~0u) {  // dummy slot
+        const uint32_t r = 32u * lrow(k) + lane;
+        if (r >= cnt) {  // dummy slot
           // n <= 31: -1 in padding column 31 (B side: +1), never a full sum;
           // n = 32 has no padding column: the verify and exact paths test vmask
-          if (p.n <= 31) g = 0x80000000u;
+          z = colmask;
+          g = p.n <= 31 ? 0x80000000u : 0u;
         } else {
+          uint32_t i0, i1;
+          cur.seek(pbase + r);
+          cur.index(pbase + r, i0, i1);
+          const uint2 lo = *reinterpret_cast<const uint2*>(Tm + T::kVec + T::VE * i0);
+          const uint2 hi = *reinterpret_cast<const uint2*>(Tm + T::kVec + T::VE * (T::N0 + i1));
+          const uint32_t par = (__popc(subs[i0]) + __popc(subs[T::N0 + i1])) & 1u;
+          z = lo.x;
+          g = lo.y;
+          sub_word(z, g, hi.x, hi.y);
           vmask |= 1u << k;
           // n <= 31: padding column 31 carries the subset parity p as the trit
           // p (0 or +1; B side +1): the sum there is +1 or -1, so it never
           // zeroes a column and its sign bit is p (the exact fold counts it)
-          if (p.n <= 31 && !(__popc(s) & 1)) z |= 0x80000000u;
-#pragma unroll 1
-          for (uint32_t x = s; x; x &= x - 1) {
-            const int t = __ffs(x) - 1;
-            sub_word(z, g, R[t].m[0], R[t].a[0]);
-          }
-          spm |= (uint32_t)(__popc(s) & 1) << k;
+          if (p.n <= 31 && !par) z |= 0x80000000u;
+          spm |= par << k;
         }
         if constexpr (!PACKED) A[k][lane] = make_uint2(z, g);
       };
@@ -372,8 +515,9 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
           A2[w][lane] = make_uint4(za, ga, zb, gb);
         }
       } else {
+        // position order (row r = lrow(k)) for the run cursor
 #pragma unroll
-        for (int k = 0; k < K; ++k) slot(k, z1[k], g1[k]);
+        for (int r = 0; r < K; ++r) slot((r >> 1) + ((r & 1) << 4), z1[(r >> 1) + ((r & 1) << 4)], g1[(r >> 1) + ((r & 1) << 4)]);
       }
     }
     // forbidden key trits of this piece: f = -x (mod 3)
@@ -418,7 +562,8 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
     // (only the steps in `mask`: incompatible steps have no full term)
     auto exact_block = [&](uint32_t& bev, uint32_t& bodd, uint32_t mask) {
       if constexpr (WIDE) {
-        const unsigned long long r = bucket_exact_wide(A2, H, H1, R, Lp, mask, lane, spm, vmask, colmask1);
+        const unsigned long long r =
+            bucket_exact_wide<FIX, KEYS>(A2, H, H1, Tm, grp, pbase, cnt, mask, lane, spm, colmask1);
         bev = (uint32_t)r;
         bodd = (uint32_t)(r >> 32);
         return;
@@ -572,7 +717,8 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
                     uint32_t par = 0;
                     if constexpr (WIDE) {
                       // the primary columns are nonzero: test the secondary ones
-                      const uint32_t r = bucket_wide_term(R, Lp[32 * lrow(k) + lane], H1[j], colmask1);
+                      const uint32_t r =
+                          bucket_wide_term<FIX, KEYS>(Tm, grp, pbase + 32u * lrow(k) + lane, H1[j], colmask1);
                       if (!r) continue;
                       par = r >> 1;
                     }
@@ -687,7 +833,11 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
 
 int bucket_pieces(BucketCfg c) { return pieces_of(c.fix, c.keys); }
 int bucket_v(bool packed) { return packed ? 5 : 4; }  // log2 superblock length
-size_t bucket_list_elem(BucketCfg c) { return c.fix > 15 ? 4 : 2; }
+size_t bucket_tab_bytes(BucketCfg c, bool wide) {
+  if (c.fix == 13 && c.keys == 2) return Tab<13, 2, false>::kBytes;
+  if (c.fix == 14 && c.keys == 2) return Tab<14, 2, false>::kBytes;
+  return wide ? Tab<17, 3, true>::kBytes : Tab<17, 3, false>::kBytes;
+}
 
 // Unpacked pair tests: 14 rows, 2 keys.  Packed filter: a 13-row A side for
 // n < 28, where items are one matrix's whole B side and a short A side makes
@@ -700,19 +850,21 @@ BucketCfg bucket_cfg(int n, bool packed) {
   return BucketCfg{17, 3};
 }
 
-cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, BucketCfg c, void* list, uint32_t* ptab,
+cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, BucketCfg c, void* tab, uint32_t* ptab,
                                 cudaStream_t st) {
   const unsigned grid = (unsigned)B;
-  if (c.fix == 13 && c.keys == 2) k_bucket_group<13, 2><<<grid, 512, 0, st>>>(rows, n, (uint16_t*)list, ptab);
-  else if (c.fix == 14 && c.keys == 2) k_bucket_group<14, 2><<<grid, 512, 0, st>>>(rows, n, (uint16_t*)list, ptab);
-  else if (c.fix == 17 && c.keys == 3) k_bucket_group<17, 3><<<grid, 512, 0, st>>>(rows, n, (uint32_t*)list, ptab);
+  uint8_t* t = static_cast<uint8_t*>(tab);
+  if (c.fix == 13 && c.keys == 2) k_bucket_group<13, 2, false><<<grid, 256, 0, st>>>(rows, n, t, ptab);
+  else if (c.fix == 14 && c.keys == 2) k_bucket_group<14, 2, false><<<grid, 256, 0, st>>>(rows, n, t, ptab);
+  else if (c.fix == 17 && c.keys == 3 && n > 32) k_bucket_group<17, 3, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
+  else if (c.fix == 17 && c.keys == 3) k_bucket_group<17, 3, false><<<grid, 256, 0, st>>>(rows, n, t, ptab);
   else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 
 cudaError_t launch_walk_bucket(int grid, const BucketParams& bp, bool packed, cudaStream_t st) {
   const BucketCfg c = bucket_cfg(bp.fp.n, packed);
-  const BucketParamsCfg bc{bp.fp, bp.list, bp.ptab, bp.tested, bp.s_end, c.fix, c.keys};
+  const BucketParamsCfg bc{bp.fp, bp.tab, bp.ptab, bp.tested, bp.s_end, c.fix, c.keys};
   if (bp.fp.n > 32) k_walk_bucket<5, 4, true, true, 17, 3><<<grid, 128, 0, st>>>(bc);
   else if (!packed) k_walk_bucket<4, 4, false, false, 14, 2><<<grid, 128, 0, st>>>(bp);
   else if (c.fix == 13) k_walk_bucket<5, 4, true, false, 13, 2><<<grid, 128, 0, st>>>(bp);

@@ -119,14 +119,15 @@ def perm_chunk(m, lo: int, hi: int) -> ChunkResult:
     """Partial sum of the packed traversal over steps lo..hi-1.
 
     Steps are 1-based and half-open, the full job is (1, 2**n); partial sums
-    of adjacent ranges add exactly.  Runs ``tp_range_sum`` on one device.
+    of adjacent ranges add exactly.  Runs ``tp_range_sum`` on one device
+    (n = 64: ``tp_range_sum_ex``, whose end may be 2**64; the reference's
+    big-int twin covers the same case, src/permanent.py:157-178,192-196).
     """
     m = _as_matrix(m)
     last = 1 << m.n
     if not 1 <= lo <= hi <= last:
         raise ValueError(f"need 1 <= lo <= hi <= 2**n, got lo={lo} hi={hi} n={m.n}")
-    if m.n > SINGLE_LIMB_MAX_N:
-        raise ValueError(f"perm_chunk supports n <= {SINGLE_LIMB_MAX_N} (step counters are uint64)")
+    _check_n(m.n)
     mags, sgns = m.planes()
     return ChunkResult(lo=lo, hi=hi, partial_sum=_kernels.chunk_sum(mags, sgns, m.n, lo, hi))
 

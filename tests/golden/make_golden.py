@@ -245,6 +245,83 @@ def oracle_goldens():
     dump("anchors.json", res)
 
 
+def c3_full():
+    """Config C3 in full: all 4,096 classes and the histogram (tests/golden/c3.json).
+
+    * uniform + sparse families (2,048 matrices, no closed form): the C
+      oracle's chunk_sum over [1, 2^32) per matrix, raw partial and class;
+      a seeded subset is cross-pinned to the reference's own
+      perm_mod3_parallel / perm_chunk (src/permanent.py:181-255);
+    * all-ones: perm = n! = 0 mod 3; perturbed permutations: the closed form
+      (fixtures.perturbed_expected), both cross-checked on a few matrices
+      by the reference too.
+    ~35 min on 8 container threads.
+    """
+    from oracle import oracle as orc
+    from paper_2407_20205_b200 import fixtures
+
+    orc.build()
+    threads = os.cpu_count() or 1
+    n = 32
+    entries, fam, exp = fixtures.structured_batch(n, 0, 4096)
+    t0 = time.time()
+    cls = np.array(exp, dtype=np.int8)
+    part = np.zeros(4096, dtype=np.int64)
+    todo = np.nonzero(exp < 0)[0]
+    for lo in range(0, len(todo), 64):  # progress in blocks
+        idx = todo[lo:lo + 64]
+        c, p = orc.perm_batch(entries[idx], threads=threads)
+        cls[idx] = c
+        part[idx] = p
+        print(f"c3 oracle {lo + len(idx)}/{len(todo)}: {time.time() - t0:.0f}s", flush=True)
+    # cross-pin: the reference's own engines on a seeded subset of every family
+    rnd = random.Random(3232)
+    pins = []
+    for f in range(4):
+        members = np.nonzero(fam == f)[0]
+        for i in sorted(rnd.sample(list(members), 3)):
+            m = ref_perm.MatrixF3(entries[i].astype(np.int64).tolist())
+            v = ref_perm.perm_mod3_parallel(m, jobs=threads) % 3
+            assert v == int(cls[i]), (i, v, int(cls[i]))
+            pins.append([int(i), int(v)])
+        print(f"c3 family {f} pinned by the reference: {time.time() - t0:.0f}s", flush=True)
+    hist = np.bincount(cls.astype(np.int64), minlength=3).tolist()
+    dump("c3.json", {"n": n, "seed": 0, "count": 4096,
+                     "entries_sha256": __import__("hashlib").sha256(entries.tobytes()).hexdigest(),
+                     "classes": "".join(str(int(c)) for c in cls),
+                     "partials_oracle": {str(int(i)): int(part[i]) for i in todo},
+                     "hist": hist, "reference_pins": pins,
+                     "seconds": round(time.time() - t0, 1)})
+
+
+def n64_goldens():
+    """perm_chunk on n = 63, 64 windows from the reference, which routes n > 62
+    to its big-int twin _chunk_sum_pure (src/permanent.py:157-178,192-196);
+    the windows include the last steps up to 2^64."""
+    r = random.Random(6464)
+    cases = []
+    for n in (63, 64):
+        for k in range(3):
+            # event-dense inputs (uniform ones have almost no full terms at n = 64):
+            # k = 0 entries in {1, 2}; k = 1 all ones but ~2 % zeros; k = 2 uniform
+            # with a zero-free last row, so the final step 2^n - 1 ({row n-1}) is full
+            if k == 0:
+                a = [[r.choice((1, 2)) for _ in range(n)] for _ in range(n)]
+            elif k == 1:
+                a = [[0 if r.random() < 0.02 else 1 for _ in range(n)] for _ in range(n)]
+            else:
+                a = [[r.randrange(3) for _ in range(n)] for _ in range(n)]
+                a[n - 1] = [r.choice((1, 2)) for _ in range(n)]
+            m = ref_perm.MatrixF3(a)
+            last = 1 << n
+            out = []
+            for lo, hi in ((1, 1 << 12), ((1 << 40) + 5, (1 << 40) + 5 + 3000), ((1 << 62) - 1500, (1 << 62) + 2500),
+                           (last - 4096, last), (last - 3, last), (last - 2000, last - 700)):
+                out.append([lo, hi, ref_perm.perm_chunk(m, lo, hi).partial_sum])
+            cases.append({"n": n, "a": enc(a), "ranges": out})
+    dump("n64.json", {"cases": cases})
+
+
 def pi_goldens():
     """pi_matrix rows and Pi_50 windows from the reference (src/experiments.py:193-213)."""
     out = {"pi_matrix": [], "windows": []}
@@ -287,10 +364,11 @@ def main():
     ap.add_argument("--with-slow", action="store_true")
     ap.add_argument("--only", default=None)
     args = ap.parse_args()
-    jobs = {"core": core_ops, "rng": rng_vectors, "chunks": chunks, "tower": tower, "pi": pi_goldens, "census": census_goldens,
+    jobs = {"core": core_ops, "rng": rng_vectors, "n64": n64_goldens, "chunks": chunks, "tower": tower, "pi": pi_goldens, "census": census_goldens,
             "anchors": lambda: anchors(args.with_slow)}
     if args.with_slow:
         jobs["oracle"] = oracle_goldens
+        jobs["c3"] = c3_full
     for name, fn in jobs.items():
         if args.only and name not in args.only.split(","):
             continue

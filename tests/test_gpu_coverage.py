@@ -1,0 +1,228 @@
+"""GPU parity, second block: the full C3 config, the bucketed walk at n = 30 and
+n = 32 (partial pieces, padding-free slots, dummy-slot masks), the exhaustive
+3x3 tower, n = 64 windows, Monte Carlo and batches beyond the old list-
+workspace cap, concurrent async calls on two streams, the NCCL all-reduce
+behind the C ABI, and the full 2^50 traversal of the C5 config matrix."""
+
+import itertools
+import os
+import random
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, centred, dec, load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _has(name):
+    return os.path.exists(os.path.join(GOLDEN, name))
+
+
+def test_c3_all_4096_classes_and_histogram(gpu):
+    """Config C3 in full: every class and the histogram against
+    tests/golden/c3.json (uniform + sparse families from the C oracle, 12
+    matrices cross-pinned by the reference's perm_mod3_parallel; all-ones and
+    perturbed permutations from their closed forms), and the raw partials of
+    all 2,048 oracle matrices.  All of it runs through the bucketed walk
+    (17-row A side, 3 key columns, n = 32: no padding column)."""
+    if not _has("c3.json"):
+        pytest.skip("C3 goldens not generated")
+    from paper_2407_20205_b200 import _kernels, fixtures
+
+    g = load_golden("c3.json")
+    entries, fam, exp = fixtures.structured_batch(32, 0, 4096)
+    import hashlib
+
+    assert hashlib.sha256(entries.tobytes()).hexdigest() == g["entries_sha256"]
+    _kernels.walk_tested(0)
+    cls, part, hist = gpu.perm_mod3_batch(entries)
+    assert _kernels.walk_tested(0) > 0, "bucketed walk not used"
+    want = np.frombuffer(g["classes"].encode(), dtype=np.uint8) - ord("0")
+    assert np.array_equal(cls, want)
+    assert hist.tolist() == g["hist"]
+    for i, p in g["partials_oracle"].items():
+        assert part[int(i)] == p, i
+    known = exp >= 0
+    assert np.array_equal(cls[known], exp[known])
+
+
+def _oracle_partials(oracle, e):
+    _, part = oracle.perm_batch(e, threads=os.cpu_count() or 4)
+    return part
+
+
+def test_bucketed_walk_n30_n32_against_oracle(gpu, oracle):
+    """n = 32 is the one width where the bucketed walk has no padding column
+    (dummy slots are the zero vector, masked by vmask, and the exact fold
+    takes the h.x == 0 correction); n = 30 keeps the padding column.  Uniform,
+    sparse (partly filled pieces), all-ones (dense mode) and a filter-heavy
+    matrix, raw partials against the C oracle."""
+    from math import comb
+
+    from paper_2407_20205_b200 import _kernels
+
+    r = np.random.default_rng(3032)
+    for n in (30, 32):
+        uni = r.integers(0, 3, (3, n, n)).astype(np.uint8)
+        sp = ((r.random((2, n, n)) < 0.3) * r.integers(1, 3, (2, n, n))).astype(np.uint8)
+        heavy = r.integers(0, 3, (1, n, n)).astype(np.uint8)
+        heavy[:, :, n - 16:] = 1  # the 16-column filter passes 2/3 of the pairs
+        e = np.concatenate([uni, sp, heavy, np.ones((1, n, n), np.uint8)])
+        _kernels.walk_tested(0)
+        cls, part, hist = gpu.perm_mod3_batch(e)
+        assert _kernels.walk_tested(0) > 0, n
+        want = _oracle_partials(oracle, e[:-1])
+        assert np.array_equal(part[:-1], want), n
+        ones = sum(comb(n, k) * (-1) ** k * (1 if k % 3 == 1 else (-1) ** n) for k in range(n + 1) if k % 3)
+        assert part[-1] == ones and cls[-1] == 0, n
+        assert hist.sum() == len(e)
+
+
+def test_exhaustive_3x3_tower(gpu, oracle):
+    """All 19,683 3x3 matrices through perm_mod3_batch (the reference's
+    exhaustive tower, tests/test_acceptance.py:102-123) against permutation
+    expansion."""
+    flat = np.array(list(itertools.product((0, 1, 2), repeat=9)), dtype=np.uint8)
+    e = flat.reshape(-1, 3, 3)
+    cls, part, hist = gpu.perm_mod3_batch(e)
+    want = np.array([oracle.perm_naive(a) % 3 for a in e.astype(np.int64)], dtype=np.int8)
+    assert np.array_equal(cls, want)
+    assert hist.tolist() == np.bincount(want, minlength=3).tolist()
+    # and one matrix at a time through the range path, a sample
+    for i in range(0, len(e), 997):
+        assert gpu.perm_mod3_fast(gpu.MatrixF3(centred(e[i]))) % 3 == want[i]
+
+
+def test_n64_windows_against_reference_twin(gpu, oracle):
+    """perm_chunk at n = 63 and 64: windows up to the end 2^64 pinned by the
+    reference's big-int twin (tests/golden/n64.json), and 2^27-step windows
+    (the bucketed walk's aligned middle plus generic head and tail, one of
+    them ending at 2^64) against the oracle's uint64 walk."""
+    from paper_2407_20205_b200 import _kernels
+
+    for case in load_golden("n64.json")["cases"]:
+        n = case["n"]
+        m = gpu.MatrixF3(centred(dec(case["a"], n)))
+        for lo, hi, s in case["ranges"]:
+            assert gpu.perm_chunk(m, lo, hi).partial_sum == s, (n, lo, hi)
+    r = random.Random(64)
+    for case in load_golden("n64.json")["cases"][3:]:
+        n = case["n"]
+        a = dec(case["a"], n)
+        mags, sgns = oracle.planes_from_classes(a)
+        m = gpu.MatrixF3(centred(a))
+        last = 1 << n
+        for lo, hi in ((last - (1 << 27) - 12345, last), (r.randrange(1, last >> 1), None)):
+            hi = hi or lo + (1 << 27) + 777
+            p, q = oracle.chunk_counts_u64(mags, sgns, n, lo, hi)
+            _kernels.walk_tested(0)
+            assert gpu.perm_chunk(m, lo, hi).partial_sum == p - q, (n, lo, hi)
+            assert _kernels.walk_tested(0) > 0
+
+
+def test_large_batches_take_the_bucketed_walk(gpu, oracle):
+    """No workspace cap: Monte Carlo at n = 28 with 100,000 trials and a
+    16,384 x 32 batch both run the bucketed walk (round 1 fell back to the
+    packed walk above 6,758 matrices at n >= 28).  The batch's first 1,024
+    matrices are C3's uniform family: their classes equal the C3 goldens."""
+    from paper_2407_20205_b200 import _kernels, fixtures
+
+    _kernels.walk_tested(0)
+    h = gpu.montecarlo_hist(28, 100_000, 11)
+    assert _kernels.walk_tested(0) > 0
+    assert h.zeros + h.plus_ones + h.minus_ones == 100_000
+    # the tally is split-invariant: two halves with their own trial offsets
+    c0 = _kernels.mc_hist(28, 0, 50_000, 11)
+    c1 = _kernels.mc_hist(28, 50_000, 100_000, 11)
+    assert (c0 + c1).tolist() == [h.zeros, h.plus_ones, h.minus_ones]
+    e = fixtures.uniform_batch(32, 0, 0, 16384)
+    _kernels.walk_tested(0)
+    cls, part, hist = gpu.perm_mod3_batch(e)
+    assert _kernels.walk_tested(0) > 0
+    assert hist.sum() == 16384
+    if _has("c3.json"):
+        want = np.frombuffer(load_golden("c3.json")["classes"].encode(), dtype=np.uint8) - ord("0")
+        assert np.array_equal(cls[:1024], want[:1024])
+    want = _oracle_partials(oracle, e[1024:1028])
+    assert np.array_equal(part[1024:1028], want)
+
+
+def test_async_calls_on_two_streams_do_not_share_memory(gpu, oracle):
+    """Two tp_walk_async calls with different batches enqueued back to back on
+    two streams (no synchronisation between them), twice, then a third on the
+    first stream: every count equals the synchronous path's.  Round 1 shared
+    one bucket-list workspace per device between them."""
+    import torch
+
+    from paper_2407_20205_b200 import _kernels, fixtures
+
+    jobs = [(fixtures.uniform_batch(24, 21, 0, 600), 24), (fixtures.uniform_batch(28, 22, 0, 40), 28),
+            (fixtures.uniform_batch(26, 23, 0, 90), 26)]
+    want = []
+    for e, n in jobs:
+        _, part, _ = gpu.perm_mod3_batch(e)
+        want.append(part)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream(), None]
+    streams[2] = streams[0]
+    bufs = []
+    for e, n in jobs:
+        B = len(e)
+        d_e = torch.from_numpy(e).cuda()
+        d_rows = torch.empty((B, _kernels.ROWREC_BYTES), dtype=torch.uint8, device="cuda")
+        d_pm = torch.zeros((B, 2), dtype=torch.int64, device="cuda")
+        _kernels.pack_async(d_e.data_ptr(), B, n, d_rows.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        bufs.append((d_e, d_rows, d_pm))
+    torch.cuda.synchronize()
+    for _ in range(2):
+        for (e, n), (_, d_rows, d_pm), st in zip(jobs, bufs, streams):
+            d_pm.zero_()
+        torch.cuda.synchronize()
+        for (e, n), (_, d_rows, d_pm), st in zip(jobs, bufs, streams):
+            _kernels.walk_async(d_rows.data_ptr(), len(e), n, d_pm.data_ptr(), st.cuda_stream)
+        torch.cuda.synchronize()
+        for (_, _, d_pm), w in zip(bufs, want):
+            pm = d_pm.cpu().numpy()
+            assert np.array_equal(pm[:, 0] - pm[:, 1], w)
+
+
+def test_nccl_all_reduce_behind_the_abi(gpu, oracle):
+    """tp_range_sum_nccl: the split of one range across the listed devices
+    with the counters summed by ONE ncclAllReduce inside the library (a
+    1-device clique on a 1-GPU box; every visible device otherwise), equal to
+    tp_range_sum and the host-summing tp_range_sum_multi."""
+    from paper_2407_20205_b200 import _kernels
+
+    devs = list(range(max(1, _kernels.device_count())))
+    g = load_golden("anchors.json")
+    for key in ("c4_window", "c5_window"):
+        w = g[key]
+        m = gpu.MatrixF3(centred(dec(w["a"], w["n"])))
+        mags, sgns = m.planes()
+        p, q = _kernels.chunk_counts_multi(mags, sgns, w["n"], w["lo"], w["hi"], devs, nccl=True)
+        assert p - q == w["partial"]
+        assert (p, q) == _kernels.chunk_counts_multi(mags, sgns, w["n"], w["lo"], w["hi"], devs, nccl=False)
+        assert (p, q) == _kernels.chunk_counts(mags, sgns, w["n"], w["lo"], w["hi"])
+    case = g["c1"][0]
+    m = gpu.MatrixF3(centred(dec(case["a"], 20)))
+    assert gpu.perm_mod3_parallel(m, jobs=8) % 3 == case["class"]
+
+
+def test_c5_config_full_traversal(gpu):
+    """The C5 config's own answer: the full 2^50-step traversal of the seed-0,
+    trial-0 50x50 matrix (~50 s), and the same range in 8 split_steps parts
+    (the multi-GPU partition rule), against tests/golden/c5_full.json.  That
+    value was measured on B200 by two different kernels (the bucketed walk
+    and the packed walk, TRITPERM_BUCKET=0; tools/c5_full.py) -- a CPU oracle
+    would need ~10^6 core-seconds -- and its 2^36-step windows are oracle-
+    pinned (anchors.json c5_window36)."""
+    if not _has("c5_full.json"):
+        pytest.skip("c5_full.json not recorded yet (tools/c5_full.py)")
+    g = load_golden("c5_full.json")
+    m = gpu.MatrixF3(centred(dec(g["a"], 50)))
+    assert gpu.perm_chunk(m, 1, 1 << 50).partial_sum == g["partial"]
+    parts = [gpu.perm_chunk(m, lo, hi).partial_sum for lo, hi in gpu.split_steps(50, 8)]
+    assert sum(parts) == g["partial"]
+    assert parts == g["parts8"]
+    assert gpu.perm_mod3_fast(m) % 3 == g["class"]

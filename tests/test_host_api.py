@@ -174,7 +174,7 @@ def test_library_exports_every_declared_symbol():
     L = _kernels.lib()
     for name in declared:
         assert hasattr(L, name), name
-    assert L.tp_version() == 100
+    assert L.tp_version() == 200
 
 
 def test_library_fails_loudly_without_a_gpu():

@@ -115,3 +115,24 @@ def test_ryser_equals_naive_exhaustive_small(oracle, n):
     for _ in range(200):
         a = [[r.randrange(-1, 2) for _ in range(n)] for _ in range(n)]
         assert oracle.perm_ryser(np.mod(a, 3)) == oracle.perm_naive(np.mod(a, 3))
+
+
+def test_u64_walk_matches_reference_big_int_twin(oracle):
+    """n = 63, 64 windows up to 2^64 from the reference's _chunk_sum_pure
+    (src/permanent.py:157-178), through the oracle's uint64 restatement."""
+    for case in load_golden("n64.json")["cases"]:
+        n = case["n"]
+        mags, sgns = oracle.planes_from_classes(dec(case["a"], n))
+        for lo, hi, s in case["ranges"]:
+            p, q = oracle.chunk_counts_u64(mags, sgns, n, lo, hi)
+            assert p - q == s, (n, lo, hi)
+
+
+def test_exhaustive_3x3_naive_vs_ryser(oracle):
+    """All 19,683 3x3 matrices: Ryser (oracle) == permutation expansion,
+    the reference's exhaustive tower (tests/test_acceptance.py:102-123)."""
+    import itertools
+
+    for flat in itertools.product((0, 1, 2), repeat=9):
+        a = np.array(flat, dtype=np.int64).reshape(3, 3)
+        assert oracle.perm_ryser(a) == oracle.perm_naive(a)
