@@ -20,7 +20,8 @@ from typing import Optional, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libtritperm_b200.so")
+# TRITPERM_LIB: another build of the same library (A/B measurements of kernel variants)
+LIB_PATH = os.environ.get("TRITPERM_LIB") or os.path.join(_HERE, "lib", "libtritperm_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "tritperm.h")
 
 TP_OK = 0

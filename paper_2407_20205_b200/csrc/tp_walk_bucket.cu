@@ -32,6 +32,10 @@
 
 #include "tp_walk_common.cuh"
 
+#ifndef TP_BUCKET_MACC
+#define TP_BUCKET_MACC 1
+#endif
+
 namespace tp {
 
 namespace {
@@ -251,7 +255,7 @@ __device__ __forceinline__ void exact_fold_par(uint32_t z1, uint32_t g1, uint32_
 // Exact evaluation of the steps in `mask` against this lane's 32 slots (the
 // packed variant's dense mode and list-overflow path).  Out of line, so its
 // registers do not constrain the filter loop.  Returns ev | odd << 32.
-static __device__ __noinline__ unsigned long long bucket_exact_packed(const uint4 (*A2)[32], const uint4* H,
+static __device__ __noinline__ unsigned long long bucket_exact_packed(const uint4 (*A2)[32], const uint2* H,
                                                                       uint32_t mask, uint32_t lane, uint32_t spm,
                                                                       uint32_t vmask, uint32_t colmask, int n,
                                                                       uint32_t one) {
@@ -260,7 +264,7 @@ static __device__ __noinline__ unsigned long long bucket_exact_packed(const uint
 #pragma unroll 1
   for (; mask; mask &= mask - 1) {
     const int j = __ffs(mask) - 1;
-    const uint4 h = H[j];
+    const uint2 h = H[j];
     const uint32_t gh = pair_g2(h.x, h.y);
     uint32_t n0 = 0, a0 = 0;
     if (n <= 31) {
@@ -294,6 +298,12 @@ static __device__ __noinline__ unsigned long long bucket_exact_packed(const uint
     bodd += (j & 1) ? (n0 - a0) : a0;
   }
   return (unsigned long long)bev | ((unsigned long long)bodd << 32);
+}
+
+// Position of the k-th (0-based) set bit of m (rare paths only).
+__device__ __forceinline__ uint32_t nth_set(uint32_t m, uint32_t k) {
+  for (; k; --k) m &= m - 1;
+  return __ffs(m) - 1;
 }
 
 // List row of physical slot k = w + 16 h (packed word w, half h): 2 w + h.
@@ -337,7 +347,7 @@ static __device__ __noinline__ uint32_t bucket_wide_term(const uint8_t* Tm, uint
 // order (one run cursor), so each slot's secondary word is built once.
 // Returns ev | odd << 32.
 template <int FIX, int KEYS>
-static __device__ __noinline__ unsigned long long bucket_exact_wide(const uint4 (*A2)[32], const uint4* H,
+static __device__ __noinline__ unsigned long long bucket_exact_wide(const uint4 (*A2)[32], const uint2* H,
                                                                     const uint2* H1, const uint8_t* Tm,
                                                                     uint32_t grp, uint32_t pbase, uint32_t cnt,
                                                                     uint32_t mask, uint32_t lane, uint32_t spm,
@@ -363,7 +373,7 @@ static __device__ __noinline__ unsigned long long bucket_exact_wide(const uint4 
 #pragma unroll 1
     for (uint32_t m = mask; m; m &= m - 1) {
       const uint32_t j = __ffs(m) - 1;
-      const uint4 h = H[j];
+      const uint2 h = H[j];
       uint32_t d, zp;
       TP_LOP3(d, za, ga, h.y, 0x06);
       TP_LOP3(zp, d, za, h.x, 0x09);
@@ -415,7 +425,10 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
   const FastParams& p = bp.fp;
   static_assert(PACKED || !WIDE, "n > 32 needs the packed filter");
   __shared__ RowRec Rs[WARPS][WIDE ? 64 : 32];
-  __shared__ uint4 Hs[WARPS][SB];
+  __shared__ uint2 Hs[WARPS][SB];  // the superblock's B states (z, u), by step
+  // packed filter: the compatible steps' doubled low 16 columns (zz, uu),
+  // compacted in step order (a pair of steps = one 16-byte load)
+  __shared__ __align__(16) uint2 Hcs[WARPS][PACKED ? SB : 2];
   __shared__ uint2 H1s[WARPS][WIDE ? SB : 1];  // n > 32: secondary words (z, u) of the superblock's B states
   __shared__ uint2 As[WARPS][K][32];  // full A words; packed: [w][lane] pairs (slot w, slot w + 16) as uint4
   constexpr int ECAP = PACKED ? (WIDE ? 5 : 6) : 1;  // (48 KB of static shared memory)  // per-lane pass-list capacity (overflow: exact superblock)
@@ -424,7 +437,8 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
   uint2 (*E)[32] = Es[threadIdx.x >> 5];
   const uint32_t cneg = 0xfffeffffu * p.one;  // -0x00010001, runtime so ptxas keeps the IMAD
   RowRec* R = Rs[threadIdx.x >> 5];
-  uint4* H = Hs[threadIdx.x >> 5];
+  uint2* H = Hs[threadIdx.x >> 5];
+  uint2* Hc = Hcs[threadIdx.x >> 5];
   uint2* H1 = H1s[threadIdx.x >> 5];
   uint2 (*A)[32] = As[threadIdx.x >> 5];
   uint4 (*A2)[32] = reinterpret_cast<uint4 (*)[32]>(As[threadIdx.x >> 5]);
@@ -452,7 +466,10 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
     const unsigned long long sb0 = p.F0 + c * p.nblk;
     const uint32_t nsb = (uint32_t)min((unsigned long long)p.nblk, bp.s_end - sb0);
     const unsigned long long A0 = sb0 << V;
-    const uint32_t pt = bp.ptab[b * kBucketPieces + q];
+    // (through REDUX: a uniform register, so every branch on the piece --
+    // the filter width, the dummy-slot tests -- is a uniform branch and the
+    // step loop below can live on the uniform datapath)
+    const uint32_t pt = __reduce_or_sync(FULL, lane == 0 ? bp.ptab[b * kBucketPieces + q] : 0u);
     const uint32_t cnt = (pt >> 8) & 0xFFFu;  // real slots of the piece
     if (cnt == 0) continue;  // unused piece
     const uint32_t grp = pt & 0xFFu;
@@ -505,14 +522,23 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
         if constexpr (!PACKED) A[k][lane] = make_uint2(z, g);
       };
       if constexpr (PACKED) {
+        // a rolled loop in position order (one copy of the decode: the
+        // unrolled 32 copies doubled the kernel's code and cost the 3-key
+        // kernels 10 % in instruction fetch), full words to shared memory,
+        // then the packed registers from there
+#pragma unroll 1
+        for (uint32_t r = 0; r < (uint32_t)K; ++r) {
+          const int k = (int)((r >> 1) + ((r & 1u) << 4));
+          uint32_t z, g;
+          slot(k, z, g);
+          reinterpret_cast<uint2*>(&A2[k & 15][lane])[k >> 4] = make_uint2(z, g);
+        }
+        __syncwarp();
 #pragma unroll
         for (int w = 0; w < K / 2; ++w) {
-          uint32_t za, ga, zb, gb;
-          slot(w, za, ga);
-          slot(w + K / 2, zb, gb);
-          Zp[w] = __byte_perm(za, zb, 0x5410);
-          Gp[w] = __byte_perm(ga, gb, 0x5410);
-          A2[w][lane] = make_uint4(za, ga, zb, gb);
+          const uint4 a = A2[w][lane];
+          Zp[w] = __byte_perm(a.x, a.z, 0x5410);
+          Gp[w] = __byte_perm(a.y, a.w, 0x5410);
         }
       } else {
         // position order (row r = lrow(k)) for the run cursor
@@ -577,7 +603,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
 #pragma unroll 1
       for (; mask; mask &= mask - 1) {
         const int j = __ffs(mask) - 1;
-        const uint4 h = H[j];
+        const uint2 h = H[j];
         const uint32_t gh = pair_g2(h.x, h.y);
         uint32_t n0 = 0, a0 = 0, n1 = 0, a1 = 0;
 #pragma unroll
@@ -610,24 +636,29 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
           }
         }
       }
-      __syncwarp();
-      if (lane < (uint32_t)SB) {
-        H[lane] = PACKED ? make_uint4(zj, uj, __byte_perm(zj, zj, 0x1010), __byte_perm(uj, uj, 0x1010))
-                         : make_uint4(zj, uj, 0u, 0u);
-        if (WIDE) H1[lane] = make_uint2(zjw, ujw);
-      }
       // compatible steps: no key column of y equals the forbidden trit
       // (y = 0 <=> z; y = 2 <=> ~z & ~u; y = 1 <=> ~z & u)
       const uint32_t match = (zj & F0) | (~zj & ~uj & F2) | (~zj & uj & F1);
-      const uint32_t cmask = __ballot_sync(FULL, match == 0u) & (SB == 32 ? 0xffffffffu : ((1u << SB) - 1u));
-      tested_steps += __popc(cmask);
+      // (REDUX: a uniform register, so everything derived from it is uniform)
+      const uint32_t cmask = __reduce_or_sync(FULL, (match == 0u && lane < (uint32_t)SB) ? 1u << lane : 0u);
+      const uint32_t ncomp = __popc(cmask);
+      tested_steps += ncomp;
+      __syncwarp();
+      if (lane < (uint32_t)SB) {
+        H[lane] = make_uint2(zj, uj);
+        if (WIDE) H1[lane] = make_uint2(zjw, ujw);
+        // compacted packed states: the filter loop walks positions 0..ncomp-1
+        // with a plain counter (no per-step bit pops)
+        if (PACKED && ((cmask >> lane) & 1u))
+          Hc[__popc(cmask & ((1u << lane) - 1u))] = make_uint2(__byte_perm(zj, zj, 0x1010), __byte_perm(uj, uj, 0x1010));
+      }
       if (dense) {
         __syncwarp();
         uint32_t bev, bodd;
         exact_block(bev, bodd, cmask);
         ev += bev;
         odd += bodd;
-        dense = __any_sync(FULL, bev >= (uint32_t)K / 2);
+        dense = __reduce_or_sync(FULL, bev >= (uint32_t)K / 2 ? 1u : 0u) != 0;
       } else {
         // the compatible steps only: a rolled loop over the set bits of
         // cmask, the next step's B state loaded (uniform shared-memory
@@ -640,42 +671,51 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
           // packed filter over the compatible steps, two per iteration: bit w
           // (step a) / 16 + w (step b) of M = a pass of word w; nonzero masks
           // go to this lane's list E for the exact verify after the loop
-          uint32_t cm = cmask, ne = 0;
+          uint32_t ne = 0;
           // W packed words hold every real slot of the piece (the rest are
           // padding): 15 for most 2-key pieces (<= 960 of 1024 slots)
           auto filter = [&](auto Wc) {
           constexpr int W = decltype(Wc)::value;
-          // two compatible steps per iteration while two remain ...
-          while (cm & (cm - 1)) {
-            const uint32_t ja = __ffs(cm) - 1;
-            cm &= cm - 1;
-            const uint32_t jb = __ffs(cm) - 1;
-            cm &= cm - 1;
-            const uint4 ha = H[ja];
-            const uint4 hb = H[jb];
+          // two compatible steps (compacted positions i, i + 1) per
+          // iteration while two remain ...
+          uint32_t i = 0;
+#pragma unroll 1
+          for (; i + 2 <= ncomp; i += 2) {
+            const uint4 hab = *reinterpret_cast<const uint4*>(Hc + i);
+#if TP_BUCKET_MACC == 2
+            // two pass-mask accumulators (even / odd words): the predicated
+            // IMADs form two dependency chains of 16 instead of one of 32
+            uint32_t M = 0, M1 = 0;
+            static_for<W>([&](auto wc) {
+              constexpr int w = decltype(wc)::value;
+              uint32_t& Mw = (w & 1) ? M1 : M;
+              packed_test<(1u << w)>(Zp[w], Gp[w], hab.x, hab.y, Mw, one, cneg);
+              packed_test<(1u << (16 + w))>(Zp[w], Gp[w], hab.z, hab.w, Mw, one, cneg);
+            });
+            M = M1 * one + M;
+#else
             uint32_t M = 0;
             static_for<W>([&](auto wc) {
               constexpr int w = decltype(wc)::value;
-              packed_test<(1u << w)>(Zp[w], Gp[w], ha.z, ha.w, M, one, cneg);
-              packed_test<(1u << (16 + w))>(Zp[w], Gp[w], hb.z, hb.w, M, one, cneg);
+              packed_test<(1u << w)>(Zp[w], Gp[w], hab.x, hab.y, M, one, cneg);
+              packed_test<(1u << (16 + w))>(Zp[w], Gp[w], hab.z, hab.w, M, one, cneg);
             });
+#endif
             if (M) {
-              if (ne < (uint32_t)ECAP) E[ne][lane] = make_uint2(M, ja | (jb << 8));
+              if (ne < (uint32_t)ECAP) E[ne][lane] = make_uint2(M, i);
               ++ne;
             }
           }
           // ... and an odd last step alone (half the tests)
-          if (cm) {
-            const uint32_t ja = __ffs(cm) - 1;
-            cm = 0;
-            const uint4 ha = H[ja];
+          if (i < ncomp) {
+            const uint2 ha = Hc[i];
             uint32_t M = 0;
             static_for<W>([&](auto wc) {
               constexpr int w = decltype(wc)::value;
-              packed_test<(1u << w)>(Zp[w], Gp[w], ha.z, ha.w, M, one, cneg);
+              packed_test<(1u << w)>(Zp[w], Gp[w], ha.x, ha.y, M, one, cneg);
             });
             if (M) {
-              if (ne < (uint32_t)ECAP) E[ne][lane] = make_uint2(M, ja | (0xFFu << 8));
+              if (ne < (uint32_t)ECAP) E[ne][lane] = make_uint2(M, i);
               ++ne;
             }
           }
@@ -693,7 +733,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
             exact_block(bev, bodd, cmask);
             ev += bev;
             odd += bodd;
-            dense = p.dense_ok != 0 && __any_sync(FULL, bev >= (uint32_t)K / 2);
+            dense = p.dense_ok != 0 && __reduce_or_sync(FULL, bev >= (uint32_t)K / 2 ? 1u : 0u) != 0;
           } else if (__any_sync(FULL, ne != 0)) {
             uint32_t bev = 0, bodd = 0;
             for (uint32_t e = 0; e < ne; ++e) {
@@ -702,8 +742,9 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
               while (M) {
                 const uint32_t bit = __ffs(M) - 1;
                 M &= M - 1;
-                const uint32_t j = (bit < 16) ? (ent.y & 0xFFu) : (ent.y >> 8), w = bit & 15u;
-                const uint4 h = H[j];
+                // compacted position -> step: the (pos)-th set bit of cmask
+                const uint32_t j = nth_set(cmask, ent.y + (bit >> 4)), w = bit & 15u;
+                const uint2 h = H[j];
                 const uint32_t gh = pair_g2(h.x, h.y);
   #pragma unroll
                 for (int hf = 0; hf < 2; ++hf) {
@@ -731,14 +772,14 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
             ev += bev;
             odd += bodd;
             // event-dense (e.g. all-ones rows): exact mode for the next superblocks
-            dense = p.dense_ok != 0 && __any_sync(FULL, bev >= (uint32_t)K / 2);
+            dense = p.dense_ok != 0 && __reduce_or_sync(FULL, bev >= (uint32_t)K / 2 ? 1u : 0u) != 0;
           }
         } else {
           // two compatible steps per iteration (independent tests interleave);
           // the next two states are loaded before the current tests
           uint32_t cm = cmask;
           uint32_t ja = 0, jb = 0, hj = 0;
-          uint4 ha = make_uint4(0, 0, 0, 0), hb = ha;
+          uint2 ha = make_uint2(0, 0), hb = ha;
           auto pop2 = [&]() {
             ja = __ffs(cm) - 1;
             cm &= cm - 1;
@@ -750,7 +791,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
             ha = H[ja];
             hb = H[jb];
             for (;;) {
-              const uint4 ca = ha, cb = hb;
+              const uint2 ca = ha, cb = hb;
               const uint32_t cja = ja, cjb = jb;
               const bool more = __popc(cm) >= 2;
               if (more) {
@@ -774,7 +815,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
           }
           if (cm) {
             const uint32_t jc = __ffs(cm) - 1;
-            const uint4 hc = H[jc];
+            const uint2 hc = H[jc];
             const uint32_t sa = r0 + r1;
             static_for<K>([&](auto kc) {
               constexpr int k = decltype(kc)::value;
@@ -789,12 +830,12 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
             uint32_t bev = 0, bodd = 0;
             if (__any_sync(FULL, cnt > 1)) {
               exact_block(bev, bodd, cmask);
-              dense = p.dense_ok != 0 && __any_sync(FULL, bev >= (uint32_t)K / 2);
+              dense = p.dense_ok != 0 && __reduce_or_sync(FULL, bev >= (uint32_t)K / 2 ? 1u : 0u) != 0;
             } else if (cnt == 1) {
               // one hit: slot k from the record, step hj tracked in the loop
               const uint32_t k = rec >> 16;
               const uint2 a1 = A[k][lane];
-              const uint4 hh = H[hj];
+              const uint2 hh = H[hj];
               uint32_t d;
               TP_LOP3(d, a1.x, a1.y, hh.y, 0x06);
               bev = 1;
