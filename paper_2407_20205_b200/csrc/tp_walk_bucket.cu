@@ -32,8 +32,28 @@
 
 #include "tp_walk_common.cuh"
 
+// Build variants for A/B timing (tools/ab_build.sh ... EXTRA=-D...):
+//   TP_BUCKET_MACC     1 / 2 pass-mask accumulators in the filter
+//   TP_BUCKET_COMPACT  1: the compatible steps' packed states compacted, the
+//                      filter loop on a counter; 0: popped from the mask (ffs)
+//   TP_BUCKET_REDUX    1: piece word and dense flag through REDUX (uniform)
+//   TP_BUCKET_ROLLED   1: the A-slot decode as a rolled loop; 0: unrolled
 #ifndef TP_BUCKET_MACC
 #define TP_BUCKET_MACC 1
+#endif
+#ifndef TP_BUCKET_COMPACT
+#define TP_BUCKET_COMPACT 0
+#endif
+#ifndef TP_BUCKET_REDUX
+#define TP_BUCKET_REDUX 0
+#endif
+#ifndef TP_BUCKET_ROLLED
+#define TP_BUCKET_ROLLED 1
+#endif
+#if TP_BUCKET_REDUX
+#define TP_ANY(x) (__reduce_or_sync(FULL, (x) ? 1u : 0u) != 0)
+#else
+#define TP_ANY(x) __any_sync(FULL, (x))
 #endif
 
 namespace tp {
@@ -70,10 +90,20 @@ __host__ __device__ __forceinline__ uint32_t pat_sub(uint32_t g, uint32_t a) {
 // the union over low patterns a of  low_a x high_(g - a),  and the table only
 // holds each half sorted by pattern:
 //   u16 off[2][NB + 1]     start of each pattern's run in the sorted half
-//   u16 sub[N0 + N1]       the sorted subsets (low half, then high half)
+//   u32 wt[N0 + N1]        the entries' weights: (subsets of even size) |
+//                          (subsets of odd size) << 16 with this vector
 //   vec[N0 + N1]           their vectors: low (z, g) words, high in row form
 //                          (m, a = m ^ s), so slot = one 3-LOP3 add; WIDE
 //                          tables carry both 32-column words (16 bytes)
+// Duplicates.  Two subsets of a half have equal vectors iff the half's rows
+// are linearly dependent over F3 (their difference is a nonzero F3
+// combination of the rows).  Independent halves (every uniform or sparse
+// C2/C3/C4/C5 input) keep all 2^TB entries, each of weight (1, 0) or (0, 1).
+// A dependent half (all-ones rows: 3 distinct vectors; a zero row; repeated
+// rows) keeps one entry per distinct vector with the parity counts of the
+// subsets that share it, and the matrix is "weighted" (ptab bit 31): its
+// items are evaluated exactly with the weights (bucket_exact_weighted).  An
+// all-ones 32x32 matrix then has 9 slots instead of 2^17.
 // Position p of bucket g is decoded by walking the runs a = 0, 1, ..: run a
 // holds |low_a| * |high_(g-a)| subsets, low index fastest.  A piece of 1024
 // slots is positions [1024 q, 1024 q + 1024) of its bucket (ptab).
@@ -86,10 +116,46 @@ struct Tab {
   static constexpr int TB = (FIX + 1) / 2, HB = FIX - TB;
   static constexpr int N0 = 1 << TB, N1 = 1 << HB;
   static constexpr int VE = WIDE ? 16 : 8;  // bytes per vector entry
-  static constexpr int kSub = align16(4 * (NB + 1));
-  static constexpr int kVec = kSub + align16(2 * (N0 + N1));
+  static constexpr int kWt = align16(4 * (NB + 1));
+  static constexpr int kVec = kWt + 4 * (N0 + N1);
   static constexpr int kBytes = kVec + VE * (N0 + N1);
 };
+
+// F3 linear independence of rows r0..r0+cnt-1 (bit planes of all n columns):
+// sequential elimination, each new row reduced by the earlier pivots (whose
+// rows are zero at every earlier pivot column).  The reference's add_reps /
+// sub_reps (src/core_f3.py:123-138) on 64-bit planes.  One thread.
+__device__ __forceinline__ bool f3_rows_independent(const RowRec* R, int r0, int cnt) {
+  uint64_t PM[9], PS[9];
+  int pc[9];
+  int rank = 0;
+  for (int t = 0; t < cnt; ++t) {
+    uint64_t m = (uint64_t)R[r0 + t].m[0] | ((uint64_t)R[r0 + t].m[1] << 32);
+    uint64_t s = (uint64_t)R[r0 + t].s[0] | ((uint64_t)R[r0 + t].s[1] << 32);
+    for (int q = 0; q < rank; ++q) {
+      if (!((m >> pc[q]) & 1ull)) continue;
+      const uint64_t m2 = PM[q], s2 = PS[q];
+      if (((s ^ s2) >> pc[q]) & 1ull) {  // opposite trits: add the pivot row
+        const uint64_t c = m2 & (m ^ s ^ s2);
+        const uint64_t nm = c | (m ^ m2);
+        s = c ^ s;
+        m = nm;
+      } else {  // equal trits: subtract it
+        const uint64_t d = m & (s ^ s2);
+        const uint64_t nm = d | (m ^ m2);
+        s = d ^ m2 ^ s2;
+        m = nm;
+      }
+      s &= m;
+    }
+    if (m == 0) return false;
+    PM[rank] = m;
+    PS[rank] = s;
+    pc[rank] = __ffsll((long long)m) - 1;
+    ++rank;
+  }
+  return true;
+}
 
 // Sequential decoder of bucket positions (monotone p): the current run a,
 // its position range [start, end), the halves' run offsets and the low
@@ -130,11 +196,14 @@ struct RunCursor {
 };
 
 // ----------------------------------------------------------------- grouping
-// One CTA per matrix: every half subset's vector and key pattern, a
+// One CTA per matrix: every half subset's vector and key pattern; for a half
+// whose rows are F3-dependent, one representative per distinct vector (the
+// lowest subset) carrying the parity counts of its duplicates; a
 // deterministic counting sort of each half by pattern (rank = earlier
-// entries with the same half and pattern), the table, then the bucket sizes
-// sum_a |low_a| |high_(g-a)| and the pieces (ptab).
-template <int FIX, int KEYS, bool WIDE>
+// representatives with the same half and pattern), the table, then the
+// bucket sizes sum_a |low_a| |high_(g-a)| and the pieces (ptab).  DEDUP =
+// false (the unpacked pair-test kernel) keeps every subset.
+template <int FIX, int KEYS, bool WIDE, bool DEDUP>
 __global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n, uint8_t* tab, uint32_t* ptab) {
   using T = Tab<FIX, KEYS, WIDE>;
   constexpr int NB = T::NB, N0 = T::N0, NE = T::N0 + T::N1, NT = 256, NW = NT / 32;
@@ -144,6 +213,9 @@ __global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n,
   __shared__ uint32_t kcnt[NK];      // key counts of the earlier rounds, then totals
   __shared__ uint32_t offs[2][NB + 1];
   __shared__ uint32_t bsize[NB];
+  __shared__ uint4 vs[DEDUP ? NE : 1];      // dependent halves: every entry's vector
+  __shared__ uint32_t wts[DEDUP ? NE : 1];  // representatives' weights (even | odd << 16)
+  __shared__ int dep[2];                    // half h has F3-dependent rows
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   {
     const uint4* src = reinterpret_cast<const uint4*>(rows + (size_t)blockIdx.x * 64);
@@ -154,19 +226,19 @@ __global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n,
   const int k1 = (n < 32 ? n : 32) - 1;  // key columns k1, k1-1 (, k1-2): primary word for n > 32
   const uint32_t cm0 = n >= 32 ? 0xffffffffu : (1u << n) - 1u;
   const uint32_t cm1 = n <= 32 ? 0u : n >= 64 ? 0xffffffffu : (1u << (n - 32)) - 1u;
-  uint32_t key[EPT], rank[EPT], sub[EPT];
+  uint32_t key[EPT], rank[EPT], wt[EPT];
   uint4 vec[EPT];
+  __syncthreads();
+  if (tid < 2) dep[tid] = DEDUP && !f3_rows_independent(R, tid ? T::TB : 0, tid ? T::HB : T::TB);
 #pragma unroll
-  for (int q = 0; q < EPT; ++q) {
-    __syncthreads();  // R loaded / the previous round's wcnt consumed
-    for (uint32_t e = tid; e < (uint32_t)(NW * NK); e += NT) wcnt[e / NK][e % NK] = 0;
+  for (int q = 0; q < EPT; ++q) {  // vectors and patterns
     const uint32_t e = (uint32_t)q * NT + tid;
     const bool act = e < (uint32_t)NE;
     const uint32_t h = e >= (uint32_t)N0 ? 1u : 0u;
-    const uint32_t s = h ? e - N0 : e;
+    const uint32_t sub = h ? e - N0 : e;
     uint32_t z0 = cm0, g0 = 0, z1 = cm1, g1 = 0;
     if (act) {
-      for (uint32_t x = s; x; x &= x - 1) {
+      for (uint32_t x = sub; x; x &= x - 1) {
         const int r = __ffs(x) - 1 + (h ? T::TB : 0);
         sub_word(z0, g0, R[r].m[0], R[r].a[0]);
         if (WIDE) sub_word(z1, g1, R[r].m[1], R[r].a[1]);
@@ -175,13 +247,54 @@ __global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n,
     auto trit = [&](int c) -> uint32_t { return ((z0 >> c) & 1u) ? 0u : ((g0 >> c) & 1u) ? 2u : 1u; };
     const uint32_t pat = KEYS == 2 ? 3u * trit(k1) + trit(k1 - 1) : 9u * trit(k1) + 3u * trit(k1 - 1) + trit(k1 - 2);
     key[q] = act ? h * NB + pat : 0xFFFFu;
-    sub[q] = s;
+    wt[q] = (__popc(sub) & 1) ? 1u << 16 : 1u;
+    // canonical sign bits (zero columns carry sgn 0) so equal vectors compare equal
+    g0 &= ~z0;
+    g1 &= ~z1;
     if (h) {  // high half in row form: the slot adds it with one sub_word
       const uint32_t m0 = ~z0 & cm0, m1 = ~z1 & cm1;
       vec[q] = make_uint4(m0, m0 ^ (g0 & m0), m1, m1 ^ (g1 & m1));
     } else {
       vec[q] = make_uint4(z0, g0, z1, g1);
     }
+    if (DEDUP && act) {
+      vs[e] = vec[q];
+      wts[e] = 0;
+    }
+  }
+  __syncthreads();
+  if (DEDUP && (dep[0] || dep[1])) {
+    // duplicates of a dependent half: each entry finds its representative
+    // (the first equal vector of its half) and adds its parity count there
+#pragma unroll
+    for (int q = 0; q < EPT; ++q) {
+      const uint32_t e = (uint32_t)q * NT + tid;
+      if (key[q] == 0xFFFFu) continue;
+      const uint32_t h = e >= (uint32_t)N0 ? 1u : 0u;
+      if (!dep[h]) continue;
+      uint32_t rep = e;
+      for (uint32_t f = h ? N0 : 0; f < e; ++f) {
+        const uint4 o = vs[f];
+        if (o.x == vec[q].x && o.y == vec[q].y && o.z == vec[q].z && o.w == vec[q].w) {
+          rep = f;
+          break;
+        }
+      }
+      atomicAdd(&wts[rep], wt[q]);
+      if (rep != e) key[q] = 0xFFFFu;  // not a representative: not in the table
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < EPT; ++q) {
+      const uint32_t e = (uint32_t)q * NT + tid;
+      if (key[q] != 0xFFFFu && dep[e >= (uint32_t)N0 ? 1 : 0]) wt[q] = wts[e];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < EPT; ++q) {  // deterministic ranks within (half, pattern)
+    __syncthreads();  // the previous round's wcnt consumed
+    for (uint32_t e = tid; e < (uint32_t)(NW * NK); e += NT) wcnt[e / NK][e % NK] = 0;
+    const bool act = key[q] != 0xFFFFu;
     const uint32_t mm = __match_any_sync(FULL, key[q]);
     __syncthreads();  // wcnt cleared
     if (act && lane == (uint32_t)(__ffs(mm) - 1)) wcnt[warp][key[q]] = __popc(mm);
@@ -214,23 +327,25 @@ __global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n,
     for (uint32_t a = 0; a < (uint32_t)NB; ++a) c += kcnt[a] * kcnt[NB + pat_sub<KEYS>(tid, a)];
     bsize[tid] = c;
   }
-  uint16_t* subs = reinterpret_cast<uint16_t*>(Tm + T::kSub);
+  uint32_t* wout = reinterpret_cast<uint32_t*>(Tm + T::kWt);
 #pragma unroll
   for (int q = 0; q < EPT; ++q) {
     if (key[q] == 0xFFFFu) continue;
     const uint32_t h = key[q] >= (uint32_t)NB ? 1u : 0u;
     const uint32_t idx = h * N0 + offs[h][key[q] - h * NB] + rank[q];
-    subs[idx] = (uint16_t)sub[q];
+    wout[idx] = wt[q];
     if (WIDE) reinterpret_cast<uint4*>(Tm + T::kVec)[idx] = vec[q];
     else reinterpret_cast<uint2*>(Tm + T::kVec)[idx] = make_uint2(vec[q].x, vec[q].y);
   }
   __syncthreads();
   if (tid == 0) {
+    const uint32_t weighted = (dep[0] || dep[1]) ? 1u << 31 : 0u;
     uint32_t* Pt = ptab + (size_t)blockIdx.x * P;
     uint32_t piece = 0;
     for (uint32_t g = 0; g < (uint32_t)NB; ++g) {
       const uint32_t c = bsize[g];
-      for (uint32_t q = 0; 1024u * q < c; ++q) Pt[piece++] = g | (min(1024u, c - 1024u * q) << 8) | (q << 20);
+      for (uint32_t q = 0; 1024u * q < c; ++q)
+        Pt[piece++] = g | (min(1024u, c - 1024u * q) << 8) | (q << 20) | weighted;
     }
     for (; piece < (uint32_t)P; ++piece) Pt[piece] = 0;  // unused pieces: count 0
   }
@@ -392,6 +507,76 @@ static __device__ __noinline__ unsigned long long bucket_exact_wide(const uint4 
   return (unsigned long long)ev | ((unsigned long long)odd << 32);
 }
 
+// Weighted matrices (a deduplicated A side, Tab): exact evaluation of the
+// steps in `mask` against this lane's real slots, each slot standing for
+// `we` subsets of even and `wo` of odd size with the same vector.  A term of
+// sign parity s (popcount of the sign word + step parity) counts we times
+// with parity s and wo times with parity s + 1.  Both words for n > 32; the
+// slot's vector is rebuilt from the table without the padding-column parity
+// trick (column 31 is +1 + +1 = -1 for n <= 31, so the sign parity masks it
+// out with colmask).  The superblock's counts (per lane <= 2^17 subsets x 32
+// steps, per warp < 2^27) are flushed into pm[0..1] right away, so the
+// weights' totals never ride in the walk's 32-bit per-lane counters.
+template <int FIX, int KEYS, bool WIDE>
+static __device__ __noinline__ void bucket_exact_weighted(const uint2* H, const uint2* H1, const uint8_t* Tm,
+                                                          uint32_t grp, uint32_t pbase, uint32_t cnt, uint32_t mask,
+                                                          uint32_t lane, uint32_t colmask, uint32_t z1i,
+                                                          unsigned long long* pm) {
+  using T = Tab<FIX, KEYS, WIDE>;
+  const uint32_t* wts = reinterpret_cast<const uint32_t*>(Tm + T::kWt);
+  RunCursor<KEYS> cur;
+  cur.init(reinterpret_cast<const uint16_t*>(Tm), grp);
+  uint32_t ev = 0, odd = 0;
+#pragma unroll 1
+  for (uint32_t r = 0; 32u * r + lane < cnt; ++r) {
+    const uint32_t p = pbase + 32u * r + lane;
+    uint32_t i0, i1;
+    cur.seek(p);
+    cur.index(p, i0, i1);
+    const uint32_t w0 = wts[i0], w1 = wts[T::N0 + i1];
+    const uint32_t e0 = w0 & 0xFFFFu, o0 = w0 >> 16, e1 = w1 & 0xFFFFu, o1 = w1 >> 16;
+    const uint32_t we = e0 * e1 + o0 * o1, wo = e0 * o1 + o0 * e1;
+    uint32_t za, ga, za1 = 0, ga1 = 0;
+    if constexpr (WIDE) {
+      const uint4 lo = reinterpret_cast<const uint4*>(Tm + T::kVec)[i0];
+      const uint4 hi = reinterpret_cast<const uint4*>(Tm + T::kVec)[T::N0 + i1];
+      za = lo.x;
+      ga = lo.y;
+      sub_word(za, ga, hi.x, hi.y);
+      za1 = lo.z;
+      ga1 = lo.w;
+      sub_word(za1, ga1, hi.z, hi.w);
+    } else {
+      const uint2 lo = reinterpret_cast<const uint2*>(Tm + T::kVec)[i0];
+      const uint2 hi = reinterpret_cast<const uint2*>(Tm + T::kVec)[T::N0 + i1];
+      za = lo.x;
+      ga = lo.y;
+      sub_word(za, ga, hi.x, hi.y);
+    }
+#pragma unroll 1
+    for (uint32_t m = mask; m; m &= m - 1) {
+      const uint32_t j = __ffs(m) - 1;
+      const uint2 h = H[j];
+      uint32_t d, zp;
+      TP_LOP3(d, za, ga, h.y, 0x06);
+      TP_LOP3(zp, d, za, h.x, 0x09);
+      if (zp != 0) continue;
+      uint32_t sp = __popc((d ^ pair_g2(h.x, h.y)) & colmask) + j;
+      if constexpr (WIDE) {
+        const uint2 h1 = H1[j];
+        uint32_t d1, zp1;
+        TP_LOP3(d1, za1, ga1, h1.y, 0x06);
+        TP_LOP3(zp1, d1, za1, h1.x, 0x09);
+        if (zp1 != 0) continue;
+        sp += __popc((d1 ^ pair_g2(h1.x, h1.y)) & z1i);
+      }
+      ev += we + wo;
+      odd += (sp & 1u) ? we : wo;
+    }
+  }
+  warp_flush(pm, ev - odd, odd, lane);
+}
+
 // Kernel argument: the 3-key kernels also carry their configuration.  The
 // two parameter layouts are the ones measured fastest for each kernel: with
 // the larger block ptxas schedules the filter loop differently, which costs
@@ -469,11 +654,16 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
     // (through REDUX: a uniform register, so every branch on the piece --
     // the filter width, the dummy-slot tests -- is a uniform branch and the
     // step loop below can live on the uniform datapath)
+#if TP_BUCKET_REDUX
     const uint32_t pt = __reduce_or_sync(FULL, lane == 0 ? bp.ptab[b * kBucketPieces + q] : 0u);
+#else
+    const uint32_t pt = bp.ptab[b * kBucketPieces + q];
+#endif
     const uint32_t cnt = (pt >> 8) & 0xFFFu;  // real slots of the piece
     if (cnt == 0) continue;  // unused piece
     const uint32_t grp = pt & 0xFFu;
-    const uint32_t pbase = (pt >> 20) << 10;  // the piece is positions [pbase, pbase + cnt) of its bucket
+    const uint32_t pbase = ((pt >> 20) & 0x7FFu) << 10;  // the piece is positions [pbase, pbase + cnt) of its bucket
+    const bool weighted = (pt >> 31) != 0;  // deduplicated A side (bucket_exact_weighted)
     const uint32_t nwd = (cnt + 63u) >> 6;  // packed words holding the piece's real slots
     __syncwarp();
     load_rows(R, p.rows + b * 64, lane, p.n);
@@ -492,7 +682,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
     uint32_t vmask = 0;  // bit k: slot k holds a real A subset (not padding)
     const uint8_t* Tm = static_cast<const uint8_t*>(bp.tab) + b * T::kBytes;
     {
-      const uint16_t* subs = reinterpret_cast<const uint16_t*>(Tm + T::kSub);
+      const uint32_t* wts = reinterpret_cast<const uint32_t*>(Tm + T::kWt);
       RunCursor<KEYS> cur;
       cur.init(reinterpret_cast<const uint16_t*>(Tm), grp);
       auto slot = [&](int k, uint32_t& z, uint32_t& g) {
@@ -508,7 +698,8 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
           cur.index(pbase + r, i0, i1);
           const uint2 lo = *reinterpret_cast<const uint2*>(Tm + T::kVec + T::VE * i0);
           const uint2 hi = *reinterpret_cast<const uint2*>(Tm + T::kVec + T::VE * (T::N0 + i1));
-          const uint32_t par = (__popc(subs[i0]) + __popc(subs[T::N0 + i1])) & 1u;
+          // subset parity (unweighted entries: weight (1, 0) or (0, 1))
+          const uint32_t par = ((wts[i0] ^ wts[T::N0 + i1]) >> 16) & 1u;
           z = lo.x;
           g = lo.y;
           sub_word(z, g, hi.x, hi.y);
@@ -521,6 +712,19 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
         }
         if constexpr (!PACKED) A[k][lane] = make_uint2(z, g);
       };
+#if !TP_BUCKET_ROLLED
+      if constexpr (PACKED) {
+#pragma unroll
+        for (int w = 0; w < K / 2; ++w) {
+          uint32_t za, ga, zb, gb;
+          slot(w, za, ga);
+          slot(w + K / 2, zb, gb);
+          Zp[w] = __byte_perm(za, zb, 0x5410);
+          Gp[w] = __byte_perm(ga, gb, 0x5410);
+          A2[w][lane] = make_uint4(za, ga, zb, gb);
+        }
+      } else
+#endif
       if constexpr (PACKED) {
         // a rolled loop in position order (one copy of the decode: the
         // unrolled 32 copies doubled the kernel's code and cost the 3-key
@@ -640,17 +844,36 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
       // (y = 0 <=> z; y = 2 <=> ~z & ~u; y = 1 <=> ~z & u)
       const uint32_t match = (zj & F0) | (~zj & ~uj & F2) | (~zj & uj & F1);
       // (REDUX: a uniform register, so everything derived from it is uniform)
+#if TP_BUCKET_REDUX
       const uint32_t cmask = __reduce_or_sync(FULL, (match == 0u && lane < (uint32_t)SB) ? 1u << lane : 0u);
+#else
+      const uint32_t cmask = __ballot_sync(FULL, match == 0u) & (SB == 32 ? 0xffffffffu : ((1u << SB) - 1u));
+#endif
       const uint32_t ncomp = __popc(cmask);
       tested_steps += ncomp;
+      if (PACKED && weighted) {
+        // deduplicated A side: every compatible step exactly, with weights
+        __syncwarp();
+        if (lane < (uint32_t)SB) {
+          H[lane] = make_uint2(zj, uj);
+          if (WIDE) H1[lane] = make_uint2(zjw, ujw);
+        }
+        __syncwarp();
+        bucket_exact_weighted<FIX, KEYS, WIDE>(H, H1, Tm, grp, pbase, cnt, cmask, lane, colmask, colmask1,
+                                               p.pm + 2 * b);
+      } else {
       __syncwarp();
       if (lane < (uint32_t)SB) {
         H[lane] = make_uint2(zj, uj);
         if (WIDE) H1[lane] = make_uint2(zjw, ujw);
         // compacted packed states: the filter loop walks positions 0..ncomp-1
         // with a plain counter (no per-step bit pops)
+#if TP_BUCKET_COMPACT
         if (PACKED && ((cmask >> lane) & 1u))
           Hc[__popc(cmask & ((1u << lane) - 1u))] = make_uint2(__byte_perm(zj, zj, 0x1010), __byte_perm(uj, uj, 0x1010));
+#else
+        if (PACKED) Hc[lane] = make_uint2(__byte_perm(zj, zj, 0x1010), __byte_perm(uj, uj, 0x1010));
+#endif
       }
       if (dense) {
         __syncwarp();
@@ -658,7 +881,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
         exact_block(bev, bodd, cmask);
         ev += bev;
         odd += bodd;
-        dense = __reduce_or_sync(FULL, bev >= (uint32_t)K / 2 ? 1u : 0u) != 0;
+        dense = TP_ANY(bev >= (uint32_t)K / 2);
       } else {
         // the compatible steps only: a rolled loop over the set bits of
         // cmask, the next step's B state loaded (uniform shared-memory
@@ -678,10 +901,22 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
           constexpr int W = decltype(Wc)::value;
           // two compatible steps (compacted positions i, i + 1) per
           // iteration while two remain ...
+#if TP_BUCKET_COMPACT
           uint32_t i = 0;
 #pragma unroll 1
           for (; i + 2 <= ncomp; i += 2) {
             const uint4 hab = *reinterpret_cast<const uint4*>(Hc + i);
+#else
+          uint32_t cm = cmask;
+          while (cm & (cm - 1)) {
+            const uint32_t ja = __ffs(cm) - 1;
+            cm &= cm - 1;
+            const uint32_t jb = __ffs(cm) - 1;
+            cm &= cm - 1;
+            const uint2 ha2 = Hc[ja], hb2 = Hc[jb];
+            const uint4 hab = make_uint4(ha2.x, ha2.y, hb2.x, hb2.y);
+            const uint32_t i = ja | (jb << 8);  // (the pass entry records the steps)
+#endif
 #if TP_BUCKET_MACC == 2
             // two pass-mask accumulators (even / odd words): the predicated
             // IMADs form two dependency chains of 16 instead of one of 32
@@ -707,8 +942,14 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
             }
           }
           // ... and an odd last step alone (half the tests)
+#if TP_BUCKET_COMPACT
           if (i < ncomp) {
             const uint2 ha = Hc[i];
+#else
+          if (cm) {
+            const uint32_t i = (__ffs(cm) - 1) | (0xFFu << 8);
+            const uint2 ha = Hc[i & 0xFFu];
+#endif
             uint32_t M = 0;
             static_for<W>([&](auto wc) {
               constexpr int w = decltype(wc)::value;
@@ -733,7 +974,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
             exact_block(bev, bodd, cmask);
             ev += bev;
             odd += bodd;
-            dense = p.dense_ok != 0 && __reduce_or_sync(FULL, bev >= (uint32_t)K / 2 ? 1u : 0u) != 0;
+            dense = p.dense_ok != 0 && TP_ANY(bev >= (uint32_t)K / 2);
           } else if (__any_sync(FULL, ne != 0)) {
             uint32_t bev = 0, bodd = 0;
             for (uint32_t e = 0; e < ne; ++e) {
@@ -742,8 +983,12 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
               while (M) {
                 const uint32_t bit = __ffs(M) - 1;
                 M &= M - 1;
+#if TP_BUCKET_COMPACT
                 // compacted position -> step: the (pos)-th set bit of cmask
                 const uint32_t j = nth_set(cmask, ent.y + (bit >> 4)), w = bit & 15u;
+#else
+                const uint32_t j = (bit < 16) ? (ent.y & 0xFFu) : (ent.y >> 8), w = bit & 15u;
+#endif
                 const uint2 h = H[j];
                 const uint32_t gh = pair_g2(h.x, h.y);
   #pragma unroll
@@ -772,7 +1017,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
             ev += bev;
             odd += bodd;
             // event-dense (e.g. all-ones rows): exact mode for the next superblocks
-            dense = p.dense_ok != 0 && __reduce_or_sync(FULL, bev >= (uint32_t)K / 2 ? 1u : 0u) != 0;
+            dense = p.dense_ok != 0 && TP_ANY(bev >= (uint32_t)K / 2);
           }
         } else {
           // two compatible steps per iteration (independent tests interleave);
@@ -830,7 +1075,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
             uint32_t bev = 0, bodd = 0;
             if (__any_sync(FULL, cnt > 1)) {
               exact_block(bev, bodd, cmask);
-              dense = p.dense_ok != 0 && __reduce_or_sync(FULL, bev >= (uint32_t)K / 2 ? 1u : 0u) != 0;
+              dense = p.dense_ok != 0 && TP_ANY(bev >= (uint32_t)K / 2);
             } else if (cnt == 1) {
               // one hit: slot k from the record, step hj tracked in the loop
               const uint32_t k = rec >> 16;
@@ -846,6 +1091,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
           }
         }
       }
+      }  // unweighted
       // (z2, u2) = step SB-1 of this superblock, then the entry step of kb + 1
       z2 = __shfl_sync(FULL, zj, SB - 1);
       u2 = __shfl_sync(FULL, uj, SB - 1);
@@ -895,10 +1141,10 @@ cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, BucketCf
                                 cudaStream_t st) {
   const unsigned grid = (unsigned)B;
   uint8_t* t = static_cast<uint8_t*>(tab);
-  if (c.fix == 13 && c.keys == 2) k_bucket_group<13, 2, false><<<grid, 256, 0, st>>>(rows, n, t, ptab);
-  else if (c.fix == 14 && c.keys == 2) k_bucket_group<14, 2, false><<<grid, 256, 0, st>>>(rows, n, t, ptab);
-  else if (c.fix == 17 && c.keys == 3 && n > 32) k_bucket_group<17, 3, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
-  else if (c.fix == 17 && c.keys == 3) k_bucket_group<17, 3, false><<<grid, 256, 0, st>>>(rows, n, t, ptab);
+  if (c.fix == 13 && c.keys == 2) k_bucket_group<13, 2, false, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
+  else if (c.fix == 14 && c.keys == 2) k_bucket_group<14, 2, false, false><<<grid, 256, 0, st>>>(rows, n, t, ptab);
+  else if (c.fix == 17 && c.keys == 3 && n > 32) k_bucket_group<17, 3, true, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
+  else if (c.fix == 17 && c.keys == 3) k_bucket_group<17, 3, false, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
   else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }

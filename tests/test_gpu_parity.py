@@ -266,6 +266,12 @@ def test_integration_binding_from_markdown(gpu):
             if lo >= 1:
                 assert ns["chunk_sum"](mags, sgns, n, lo, hi) == s
                 assert ns["chunk_sum_devices"](mags, sgns, n, lo, hi, [0]) == s
+                assert ns["chunk_sum_devices"](mags, sgns, n, lo, hi, [0], nccl=False) == s
+    for case in load_golden("n64.json")["cases"]:  # n = 63, 64 through the same binding
+        n = case["n"]
+        mags, sgns = gpu.MatrixF3(centred(dec(case["a"], n))).planes()
+        for lo, hi, s in case["ranges"]:
+            assert ns["chunk_sum"](mags, sgns, n, lo, hi) == s
     for case in load_golden("anchors.json")["montecarlo"][:5]:
         assert ns["mc_zero_count"](case["n"], 0, case["trials"], case["seed"]) == case["zero_count"]
     for case in load_golden("rng.json")["samples"][:8]:
