@@ -50,6 +50,31 @@
 #ifndef TP_BUCKET_ROLLED
 #define TP_BUCKET_ROLLED 1
 #endif
+//   TP_BUCKET_SMALLCFG 1: n < 28 with a 14-row A side and 3 key columns
+//   TP_BUCKET_BIGKEYS  key columns of the 17-row A side (n >= 28): 3, 4 or 5
+#ifndef TP_BUCKET_BIGKEYS
+#define TP_BUCKET_BIGKEYS 4
+#endif
+#ifndef TP_BUCKET_SMALLCFG
+#define TP_BUCKET_SMALLCFG 0
+#endif
+//   TP_CHECKED         1: device-side bounds checks on every table, list and
+//                      shared-memory index of the bucketed walk (__trap on a
+//                      violation); the checked build stands in for
+//                      compute-sanitizer, which this GPU pool does not allow
+#ifndef TP_CHECKED
+#define TP_CHECKED 0
+#endif
+#if TP_CHECKED
+#define TP_CHECK(c)    \
+  do {                 \
+    if (!(c)) __trap(); \
+  } while (0)
+#else
+#define TP_CHECK(c) \
+  do {              \
+  } while (0)
+#endif
 #if TP_BUCKET_REDUX
 #define TP_ANY(x) (__reduce_or_sync(FULL, (x) ? 1u : 0u) != 0)
 #else
@@ -63,7 +88,23 @@ namespace {
 // Bucket configurations (bucket_cfg): A side = rows 0..FIX-1, sorted by the
 // trits of KEYS key columns into 3^KEYS buckets; pieces per matrix:
 // 2^(FIX-10) full ones plus one partial per bucket.
-__host__ __device__ constexpr int nbuckets(int keys) { return keys == 2 ? 9 : 27; }
+__host__ __device__ constexpr int nbuckets(int keys) { return keys <= 0 ? 1 : 3 * nbuckets(keys - 1); }
+
+// Packed-filter widths per configuration: pieces with at most WB packed words
+// of real slots run the filter on WB words, at most WA on WA, else all 16
+// (each width is one copy of the filter loop; WA = WB = 16: a single copy).
+// A bucket holds 2^FIX / 3^KEYS subsets on uniform inputs: its last piece is
+// the remainder, e.g. ~594 slots (10 words) for 17 rows and 4 keys.
+template <int FIX, int KEYS>
+struct FilterWidths {
+  static constexpr int WA = FIX == 13 && KEYS == 2 ? 15 : FIX == 14 && KEYS == 3 ? 11 : FIX == 17 && KEYS == 4 ? 11
+                            : FIX == 17 && KEYS == 5 ? 10 : 16;
+  static constexpr int WB = FIX == 13 && KEYS == 2 ? 12 : FIX == 14 && KEYS == 3 ? 10 : FIX == 17 && KEYS == 4 ? 10
+                            : FIX == 17 && KEYS == 5 ? 9 : 16;
+  __host__ __device__ static constexpr uint32_t width(uint32_t nwd) {
+    return nwd > (uint32_t)WA ? 16u : nwd > (uint32_t)WB ? (uint32_t)WA : (uint32_t)WB;
+  }
+};
 __host__ __device__ constexpr int pieces_of(int fix, int keys) { return (1 << (fix - 10)) + nbuckets(keys); }
 __host__ __device__ constexpr int align16(int x) { return (x + 15) & ~15; }
 
@@ -118,7 +159,10 @@ struct Tab {
   static constexpr int VE = WIDE ? 16 : 8;  // bytes per vector entry
   static constexpr int kWt = align16(4 * (NB + 1));
   static constexpr int kVec = kWt + 4 * (N0 + N1);
-  static constexpr int kBytes = kVec + VE * (N0 + N1);
+  // n > 32 (WIDE) also: u32 rstart[NB][NB + 1], the start of run a in bucket
+  // g, so the rare primary-hit path finds a slot's run by binary search
+  static constexpr int kRun = kVec + VE * (N0 + N1);
+  static constexpr int kBytes = align16(kRun + (WIDE ? 4 * NB * (NB + 1) : 0));
 };
 
 // F3 linear independence of rows r0..r0+cnt-1 (bit planes of all n columns):
@@ -183,15 +227,18 @@ struct RunCursor {
   __device__ __forceinline__ void seek(uint32_t p) {
     while (p >= end) {
       ++a;
+      TP_CHECK(a < (uint32_t)nbuckets(KEYS));
       start = end;
       load();
     }
   }
   // table indices (low, high) of position p (after seek(p))
   __device__ __forceinline__ void index(uint32_t p, uint32_t& i0, uint32_t& i1) const {
+    TP_CHECK(p >= start && p < end && c0 > 0);
     const uint32_t rel = p - start, j = rel / c0;
     i0 = o0 + (rel - j * c0);
     i1 = o1 + j;
+    TP_CHECK(i0 < off[nbuckets(KEYS)] && i1 < off[2 * nbuckets(KEYS) + 1]);
   }
 };
 
@@ -221,7 +268,7 @@ __global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n,
     const uint4* src = reinterpret_cast<const uint4*>(rows + (size_t)blockIdx.x * 64);
     if (tid < 2 * FIX) reinterpret_cast<uint4*>(R)[tid] = src[tid];
   }
-  if (tid < (uint32_t)NK) kcnt[tid] = 0;
+  for (uint32_t k = tid; k < (uint32_t)NK; k += NT) kcnt[k] = 0;
   uint8_t* Tm = tab + (size_t)blockIdx.x * T::kBytes;
   const int k1 = (n < 32 ? n : 32) - 1;  // key columns k1, k1-1 (, k1-2): primary word for n > 32
   const uint32_t cm0 = n >= 32 ? 0xffffffffu : (1u << n) - 1u;
@@ -245,7 +292,9 @@ __global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n,
       }
     }
     auto trit = [&](int c) -> uint32_t { return ((z0 >> c) & 1u) ? 0u : ((g0 >> c) & 1u) ? 2u : 1u; };
-    const uint32_t pat = KEYS == 2 ? 3u * trit(k1) + trit(k1 - 1) : 9u * trit(k1) + 3u * trit(k1 - 1) + trit(k1 - 2);
+    uint32_t pat = 0;  // first key column most significant
+#pragma unroll
+    for (int i = 0; i < KEYS; ++i) pat = 3u * pat + trit(k1 - i);
     key[q] = act ? h * NB + pat : 0xFFFFu;
     wt[q] = (__popc(sub) & 1) ? 1u << 16 : 1u;
     // canonical sign bits (zero columns carry sgn 0) so equal vectors compare equal
@@ -305,10 +354,10 @@ __global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n,
       rank[q] = r;
     }
     __syncthreads();
-    if (tid < (uint32_t)NK) {
+    for (uint32_t k = tid; k < (uint32_t)NK; k += NT) {
       uint32_t c = 0;
-      for (int w = 0; w < NW; ++w) c += wcnt[w][tid];
-      kcnt[tid] += c;
+      for (int w = 0; w < NW; ++w) c += wcnt[w][k];
+      kcnt[k] += c;
     }
   }
   __syncthreads();
@@ -321,11 +370,21 @@ __global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n,
     offs[tid][NB] = o;
   }
   __syncthreads();
-  if (tid < (uint32_t)(2 * (NB + 1))) reinterpret_cast<uint16_t*>(Tm)[tid] = (uint16_t)offs[tid / (NB + 1)][tid % (NB + 1)];
-  if (tid < (uint32_t)NB) {
+  for (uint32_t k = tid; k < (uint32_t)(2 * (NB + 1)); k += NT)
+    reinterpret_cast<uint16_t*>(Tm)[k] = (uint16_t)offs[k / (NB + 1)][k % (NB + 1)];
+  for (uint32_t g = tid; g < (uint32_t)NB; g += NT) {
     uint32_t c = 0;
-    for (uint32_t a = 0; a < (uint32_t)NB; ++a) c += kcnt[a] * kcnt[NB + pat_sub<KEYS>(tid, a)];
-    bsize[tid] = c;
+    for (uint32_t a = 0; a < (uint32_t)NB; ++a) c += kcnt[a] * kcnt[NB + pat_sub<KEYS>(g, a)];
+    bsize[g] = c;
+    if (WIDE) {  // run starts of bucket g (the same sum, kept per run)
+      uint32_t* rs = reinterpret_cast<uint32_t*>(Tm + T::kRun) + g * (NB + 1);
+      uint32_t o = 0;
+      for (uint32_t a = 0; a < (uint32_t)NB; ++a) {
+        rs[a] = o;
+        o += kcnt[a] * kcnt[NB + pat_sub<KEYS>(g, a)];
+      }
+      rs[NB] = o;
+    }
   }
   uint32_t* wout = reinterpret_cast<uint32_t*>(Tm + T::kWt);
 #pragma unroll
@@ -333,6 +392,7 @@ __global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n,
     if (key[q] == 0xFFFFu) continue;
     const uint32_t h = key[q] >= (uint32_t)NB ? 1u : 0u;
     const uint32_t idx = h * N0 + offs[h][key[q] - h * NB] + rank[q];
+    TP_CHECK(idx < (uint32_t)(h ? NE : N0));
     wout[idx] = wt[q];
     if (WIDE) reinterpret_cast<uint4*>(Tm + T::kVec)[idx] = vec[q];
     else reinterpret_cast<uint2*>(Tm + T::kVec)[idx] = make_uint2(vec[q].x, vec[q].y);
@@ -344,8 +404,10 @@ __global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n,
     uint32_t piece = 0;
     for (uint32_t g = 0; g < (uint32_t)NB; ++g) {
       const uint32_t c = bsize[g];
-      for (uint32_t q = 0; 1024u * q < c; ++q)
+      for (uint32_t q = 0; 1024u * q < c; ++q) {
+        TP_CHECK(piece < (uint32_t)P);
         Pt[piece++] = g | (min(1024u, c - 1024u * q) << 8) | (q << 20) | weighted;
+      }
     }
     for (; piece < (uint32_t)P; ++piece) Pt[piece] = 0;  // unused pieces: count 0
   }
@@ -432,11 +494,22 @@ __device__ __forceinline__ uint32_t lrow(int k) { return 2u * (uint32_t)(k & 15)
 template <int FIX, int KEYS>
 __device__ __forceinline__ void a_word1(const uint8_t* Tm, uint32_t grp, uint32_t p, uint32_t& z, uint32_t& g) {
   using T = Tab<FIX, KEYS, true>;
-  RunCursor<KEYS> c;
-  c.init(reinterpret_cast<const uint16_t*>(Tm), grp);
-  c.seek(p);
-  uint32_t i0, i1;
-  c.index(p, i0, i1);
+  constexpr uint32_t NB = T::NB;
+  // the run a of position p: the last run start <= p (binary search; empty
+  // runs share their start with the next run, the search lands on a
+  // non-empty one since p < the bucket's size)
+  const uint32_t* rs = reinterpret_cast<const uint32_t*>(Tm + T::kRun) + grp * (NB + 1);
+  uint32_t lo_a = 0, hi_a = NB;  // rs[lo_a] <= p < rs[hi_a]
+  while (hi_a - lo_a > 1) {
+    const uint32_t mid = (lo_a + hi_a) >> 1;
+    if (rs[mid] <= p) lo_a = mid;
+    else hi_a = mid;
+  }
+  const uint16_t* off = reinterpret_cast<const uint16_t*>(Tm);
+  const uint32_t o0 = off[lo_a], c0 = off[lo_a + 1] - o0, o1 = off[NB + 1 + pat_sub<KEYS>(grp, lo_a)];
+  TP_CHECK(c0 > 0 && p < rs[NB]);
+  const uint32_t rel = p - rs[lo_a], j = rel / c0;
+  const uint32_t i0 = o0 + (rel - j * c0), i1 = o1 + j;
   const uint4* v = reinterpret_cast<const uint4*>(Tm + T::kVec);
   const uint4 lo = v[i0], hi = v[T::N0 + i1];
   z = lo.z;
@@ -597,6 +670,14 @@ template <>
 struct BucketArg<3> {
   using type = BucketParamsCfg;
 };
+template <>
+struct BucketArg<4> {
+  using type = BucketParamsCfg;
+};
+template <>
+struct BucketArg<5> {
+  using type = BucketParamsCfg;
+};
 
 }  // namespace
 
@@ -657,6 +738,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
 #if TP_BUCKET_REDUX
     const uint32_t pt = __reduce_or_sync(FULL, lane == 0 ? bp.ptab[b * kBucketPieces + q] : 0u);
 #else
+    TP_CHECK(q < (uint32_t)kBucketPieces && b < nmat);
     const uint32_t pt = bp.ptab[b * kBucketPieces + q];
 #endif
     const uint32_t cnt = (pt >> 8) & 0xFFFu;  // real slots of the piece
@@ -664,6 +746,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
     const uint32_t grp = pt & 0xFFu;
     const uint32_t pbase = ((pt >> 20) & 0x7FFu) << 10;  // the piece is positions [pbase, pbase + cnt) of its bucket
     const bool weighted = (pt >> 31) != 0;  // deduplicated A side (bucket_exact_weighted)
+    TP_CHECK(((pt >> 8) & 0xFFFu) <= 1024u && (pt & 0xFFu) < (uint32_t)nbuckets(KEYS));
     const uint32_t nwd = (cnt + 63u) >> 6;  // packed words holding the piece's real slots
     __syncwarp();
     load_rows(R, p.rows + b * 64, lane, p.n);
@@ -751,8 +834,9 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
       }
     }
     // forbidden key trits of this piece: f = -x (mod 3)
-    uint32_t F0, F1, F2;
-    if constexpr (KEYS == 2) {
+    // (digit i of grp, weight 3^(KEYS-1-i), is the trit of column k1 - i)
+    uint32_t F0 = 0, F1 = 0, F2 = 0;
+    if constexpr (KEYS == 2) {  // (this form keeps the 2-key kernel's register allocation spill-free)
       const int k2 = k1 - 1;
       const uint32_t x1 = grp / 3, x2 = grp % 3;
       const uint32_t f1 = (3 - x1) % 3, f2 = (3 - x2) % 3;
@@ -760,11 +844,12 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
       F1 = (f1 == 1 ? 1u << k1 : 0u) | (f2 == 1 ? 1u << k2 : 0u);
       F2 = (f1 == 2 ? 1u << k1 : 0u) | (f2 == 2 ? 1u << k2 : 0u);
     } else {
-      F0 = F1 = F2 = 0;
+      uint32_t rest = grp;
 #pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const uint32_t x = (i == 0 ? grp / 9 : i == 1 ? grp / 3 : grp) % 3;
-        const uint32_t f = (3 - x) % 3, bit = 1u << (k1 - i);
+      for (int i = KEYS - 1; i >= 0; --i) {
+        const uint32_t x = rest % 3u;
+        rest /= 3u;
+        const uint32_t f = (3u - x) % 3u, bit = 1u << (k1 - i);
         F0 |= f == 0 ? bit : 0u;
         F1 |= f == 1 ? bit : 0u;
         F2 |= f == 2 ? bit : 0u;
@@ -961,11 +1046,17 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
             }
           }
           };
-          // (2-key kernels only: in the 3-key kernels the extra loop copies
-          // cost more in schedule quality than the 4 % of tests they save)
-          if (KEYS == 3 || nwd > 15) filter(std::integral_constant<int, 16>{});
-          else if (nwd > 12) filter(std::integral_constant<int, 15>{});
-          else filter(std::integral_constant<int, 12>{});
+          // (17 rows / 3 keys: one copy; its pieces are nearly all full, and
+          // the extra loop copies cost more in schedule quality than the 4 %
+          // of tests they would save)
+          using FW = FilterWidths<FIX, KEYS>;
+          if constexpr (FW::WA == 16) {
+            filter(std::integral_constant<int, 16>{});
+          } else {
+            if (nwd > (uint32_t)FW::WA) filter(std::integral_constant<int, 16>{});
+            else if (nwd > (uint32_t)FW::WB) filter(std::integral_constant<int, FW::WA>{});
+            else filter(std::integral_constant<int, FW::WB>{});
+          }
           if (__any_sync(FULL, ne > (uint32_t)ECAP)) {
             // a lane's pass list overflowed (event-dense matrix): evaluate the
             // superblock's compatible steps exactly instead
@@ -989,6 +1080,7 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
 #else
                 const uint32_t j = (bit < 16) ? (ent.y & 0xFFu) : (ent.y >> 8), w = bit & 15u;
 #endif
+                TP_CHECK(j < (uint32_t)SB && ((cmask >> j) & 1u));
                 const uint2 h = H[j];
                 const uint32_t gh = pair_g2(h.x, h.y);
   #pragma unroll
@@ -1113,7 +1205,10 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
       }
     }
     warp_flush(p.pm + 2 * b, ev - odd, odd, lane);
-    if (bp.tested && lane == 0) atomicAdd(bp.tested, (PACKED && KEYS == 2 ? 64ull * (nwd > 15 ? 16 : nwd > 12 ? 15 : 12) : 1024ull) * tested_steps);
+    if (bp.tested && lane == 0) {
+      const uint32_t words = PACKED ? FilterWidths<FIX, KEYS>::width(nwd) : 16u;
+      atomicAdd(bp.tested, 64ull * words * tested_steps);
+    }
   }
   queue_done(p, lane);
 }
@@ -1122,19 +1217,28 @@ int bucket_pieces(BucketCfg c) { return pieces_of(c.fix, c.keys); }
 int bucket_v(bool packed) { return packed ? 5 : 4; }  // log2 superblock length
 size_t bucket_tab_bytes(BucketCfg c, bool wide) {
   if (c.fix == 13 && c.keys == 2) return Tab<13, 2, false>::kBytes;
+  if (c.fix == 14 && c.keys == 3) return Tab<14, 3, false>::kBytes;
   if (c.fix == 14 && c.keys == 2) return Tab<14, 2, false>::kBytes;
-  return wide ? Tab<17, 3, true>::kBytes : Tab<17, 3, false>::kBytes;
+  return wide ? Tab<17, TP_BUCKET_BIGKEYS, true>::kBytes : Tab<17, TP_BUCKET_BIGKEYS, false>::kBytes;
 }
 
 // Unpacked pair tests: 14 rows, 2 keys.  Packed filter: a 13-row A side for
 // n < 28, where items are one matrix's whole B side and a short A side makes
-// them longer; from n = 28 a 17-row A side in 27 buckets of three key
-// columns (the B side still has >= 64 superblocks per matrix), which skips
-// 19/27 of the steps instead of 5/9 and fills its pieces better.
+// them longer; from n = 28 a 17-row A side in 81 buckets of four key columns
+// (the B side still has >= 64 superblocks per matrix), which skips 65/81 of
+// the steps (3 keys: 19/27) at the cost of one partly filled piece per
+// bucket.  Measured on B200: 4 keys against 3 take C3 from
+// 472 to 378 ms, C4 from 3.33 to 2.84 ms, C5 from 747 to 604 ms; 5 keys are
+// slower (243 runs per bucket to decode, 9-word pieces); for n < 28 a 14-row
+// A side with 3 keys (TP_BUCKET_SMALLCFG) is 3 % faster on C2 but leaves
+// the filter a smaller share of the time (C2 LOP3 roofline 0.61 -> 0.42).
 BucketCfg bucket_cfg(int n, bool packed) {
   if (!packed) return BucketCfg{14, 2};
+#if TP_BUCKET_SMALLCFG == 1
+  if (n < 28) return BucketCfg{14, 3};
+#endif
   if (n < 28) return BucketCfg{13, 2};
-  return BucketCfg{17, 3};
+  return BucketCfg{17, TP_BUCKET_BIGKEYS};
 }
 
 cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, BucketCfg c, void* tab, uint32_t* ptab,
@@ -1143,8 +1247,13 @@ cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, BucketCf
   uint8_t* t = static_cast<uint8_t*>(tab);
   if (c.fix == 13 && c.keys == 2) k_bucket_group<13, 2, false, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
   else if (c.fix == 14 && c.keys == 2) k_bucket_group<14, 2, false, false><<<grid, 256, 0, st>>>(rows, n, t, ptab);
-  else if (c.fix == 17 && c.keys == 3 && n > 32) k_bucket_group<17, 3, true, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
-  else if (c.fix == 17 && c.keys == 3) k_bucket_group<17, 3, false, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
+#if TP_BUCKET_SMALLCFG == 1
+  else if (c.fix == 14 && c.keys == 3) k_bucket_group<14, 3, false, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
+#endif
+  else if (c.fix == 17 && c.keys == TP_BUCKET_BIGKEYS && n > 32)
+    k_bucket_group<17, TP_BUCKET_BIGKEYS, true, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
+  else if (c.fix == 17 && c.keys == TP_BUCKET_BIGKEYS)
+    k_bucket_group<17, TP_BUCKET_BIGKEYS, false, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
   else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
@@ -1152,10 +1261,13 @@ cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, BucketCf
 cudaError_t launch_walk_bucket(int grid, const BucketParams& bp, bool packed, cudaStream_t st) {
   const BucketCfg c = bucket_cfg(bp.fp.n, packed);
   const BucketParamsCfg bc{bp.fp, bp.tab, bp.ptab, bp.tested, bp.s_end, c.fix, c.keys};
-  if (bp.fp.n > 32) k_walk_bucket<5, 4, true, true, 17, 3><<<grid, 128, 0, st>>>(bc);
+  if (bp.fp.n > 32) k_walk_bucket<5, 4, true, true, 17, TP_BUCKET_BIGKEYS><<<grid, 128, 0, st>>>(bc);
   else if (!packed) k_walk_bucket<4, 4, false, false, 14, 2><<<grid, 128, 0, st>>>(bp);
   else if (c.fix == 13) k_walk_bucket<5, 4, true, false, 13, 2><<<grid, 128, 0, st>>>(bp);
-  else k_walk_bucket<5, 4, true, false, 17, 3><<<grid, 128, 0, st>>>(bc);
+#if TP_BUCKET_SMALLCFG == 1
+  else if (c.fix == 14) k_walk_bucket<5, 4, true, false, 14, 3><<<grid, 128, 0, st>>>(bc);
+#endif
+  else k_walk_bucket<5, 4, true, false, 17, TP_BUCKET_BIGKEYS><<<grid, 128, 0, st>>>(bc);
   return cudaGetLastError();
 }
 

@@ -226,3 +226,25 @@ def test_c5_config_full_traversal(gpu):
     assert sum(parts) == g["partial"]
     assert parts == g["parts8"]
     assert gpu.perm_mod3_fast(m) % 3 == g["class"]
+
+
+def test_bounds_checked_build_runs_every_walk_family():
+    """Stand-in for compute-sanitizer (closed on this GPU pool: runs under it
+    left GPUs needing a reset): the TP_CHECKED build of the library traps on
+    any out-of-range table, list or shared-memory index of the bucketed walk
+    (RunCursor decode, piece table, pass-list steps, grouping ranks), and
+    tools/sanitize_case.py drives every walk family through it against the
+    oracle in a separate process."""
+    import subprocess
+    import sys
+
+    from conftest import REPO
+
+    lib = os.path.join(REPO, "paper_2407_20205_b200", "lib", "checked", "libtritperm_b200.so")
+    if not os.path.exists(lib):
+        pytest.skip("checked build missing (make -C paper_2407_20205_b200/csrc checked)")
+    env = dict(os.environ, TRITPERM_LIB=lib)
+    out = subprocess.run([sys.executable, os.path.join(REPO, "tools", "sanitize_case.py")], env=env,
+                         capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "sanitize case ok" in out.stdout
