@@ -116,8 +116,8 @@ BucketCfg bucket_cfg(int n, bool packed);
 int bucket_pieces(BucketCfg c);
 size_t bucket_tab_bytes(BucketCfg c, bool wide);  // per matrix
 int bucket_v(bool packed);
-cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, BucketCfg c, void* tab, uint32_t* ptab,
-                                cudaStream_t st);
+cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, BucketCfg c, bool packed, void* tab,
+                                uint32_t* ptab, cudaStream_t st);
 cudaError_t launch_walk_bucket(int grid, const BucketParams& bp, bool packed, cudaStream_t st);
 const void* walk_bucket_symbol(bool packed);
 

@@ -331,7 +331,15 @@ int make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, uns
     const unsigned long long warps = (unsigned long long)d.sm_count * d.bucket_blocks_per_sm * 4;
     unsigned long long nblk = std::min<unsigned long long>(std::max<unsigned long long>(total, 1), 1ull << 16);
     auto items_of = [&](unsigned long long nb) { return B * (unsigned long long)P * ((total + nb - 1) / nb); };
-    while (nblk > 1 && (items_of(nblk) < 4 * warps || (nblk > 1024 && items_of(nblk) < per_warp * warps)))
+    // (TRITPERM_BUCKET_MIN_ITEMS: items per warp at least, default 4.  One
+    // 36x36 matrix ends with a tail of 14.7 of 16 warps active, but 16 or 64
+    // items per warp cost more in per-item setup than the tail: C4 2.81 ms at
+    // 4, 2.91 at 16, 4.14 at 64; C3 and C5 unchanged)
+    static const unsigned long long min_items = [] {
+      const char* e = getenv("TRITPERM_BUCKET_MIN_ITEMS");
+      return (unsigned long long)(e && atoi(e) > 0 ? atoi(e) : 4);
+    }();
+    while (nblk > 1 && (items_of(nblk) < min_items * warps || (nblk > 1024 && items_of(nblk) < per_warp * warps)))
       nblk = (nblk + 1) / 2;
     const unsigned long long chunks = (total + nblk - 1) / nblk;
     if (big) {
@@ -515,8 +523,8 @@ int make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, uns
 int run_plan(const Plan& pl, cudaStream_t st, int* launches) {
   int nl = 0;
   if (pl.bucket) {  // (ranges: plus the generic head and tail below)
-    TP_CUDA(tp::launch_bucket_group(pl.bkp.fp.rows, pl.bucket_B, pl.bkp.fp.n, pl.bucket_cfg, pl.bucket_tab,
-                                    pl.bucket_ptab, st));
+    TP_CUDA(tp::launch_bucket_group(pl.bkp.fp.rows, pl.bucket_B, pl.bkp.fp.n, pl.bucket_cfg, pl.bucket_packed,
+                                    pl.bucket_tab, pl.bucket_ptab, st));
     TP_CUDA(tp::launch_walk_bucket(pl.bucket_grid, pl.bkp, pl.bucket_packed, st));
     nl += 2;
   }

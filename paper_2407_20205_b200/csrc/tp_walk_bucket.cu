@@ -55,6 +55,10 @@
 #ifndef TP_BUCKET_BIGKEYS
 #define TP_BUCKET_BIGKEYS 4
 #endif
+//   TP_BUCKET_VOTE1    1: one REDUX.MAX of the pass-list lengths instead of two votes
+#ifndef TP_BUCKET_VOTE1
+#define TP_BUCKET_VOTE1 1
+#endif
 #ifndef TP_BUCKET_SMALLCFG
 #define TP_BUCKET_SMALLCFG 0
 #endif
@@ -97,9 +101,11 @@ __host__ __device__ constexpr int nbuckets(int keys) { return keys <= 0 ? 1 : 3 
 // the remainder, e.g. ~594 slots (10 words) for 17 rows and 4 keys.
 template <int FIX, int KEYS>
 struct FilterWidths {
-  static constexpr int WA = FIX == 13 && KEYS == 2 ? 15 : FIX == 14 && KEYS == 3 ? 11 : FIX == 17 && KEYS == 4 ? 11
+  static constexpr int WA = FIX == 13 && KEYS == 2 ? 15 : FIX == 14 && KEYS == 3 ? 11 : FIX == 14 && KEYS == 2 ? 14
+                            : FIX == 17 && KEYS == 4 ? 11
                             : FIX == 17 && KEYS == 5 ? 10 : 16;
-  static constexpr int WB = FIX == 13 && KEYS == 2 ? 12 : FIX == 14 && KEYS == 3 ? 10 : FIX == 17 && KEYS == 4 ? 10
+  static constexpr int WB = FIX == 13 && KEYS == 2 ? 12 : FIX == 14 && KEYS == 3 ? 10 : FIX == 14 && KEYS == 2 ? 13
+                            : FIX == 17 && KEYS == 4 ? 10
                             : FIX == 17 && KEYS == 5 ? 9 : 16;
   __host__ __device__ static constexpr uint32_t width(uint32_t nwd) {
     return nwd > (uint32_t)WA ? 16u : nwd > (uint32_t)WB ? (uint32_t)WA : (uint32_t)WB;
@@ -1057,7 +1063,12 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
             else if (nwd > (uint32_t)FW::WB) filter(std::integral_constant<int, FW::WA>{});
             else filter(std::integral_constant<int, FW::WB>{});
           }
+#if TP_BUCKET_VOTE1
+          const uint32_t nemax = __reduce_max_sync(FULL, ne);  // one REDUX for both tests below
+          if (nemax > (uint32_t)ECAP) {
+#else
           if (__any_sync(FULL, ne > (uint32_t)ECAP)) {
+#endif
             // a lane's pass list overflowed (event-dense matrix): evaluate the
             // superblock's compatible steps exactly instead
             __syncwarp();
@@ -1066,7 +1077,11 @@ __global__ void __launch_bounds__(32 * WARPS, 4) k_walk_bucket(const typename Bu
             ev += bev;
             odd += bodd;
             dense = p.dense_ok != 0 && TP_ANY(bev >= (uint32_t)K / 2);
+#if TP_BUCKET_VOTE1
+          } else if (nemax != 0) {
+#else
           } else if (__any_sync(FULL, ne != 0)) {
+#endif
             uint32_t bev = 0, bodd = 0;
             for (uint32_t e = 0; e < ne; ++e) {
               const uint2 ent = E[e][lane];
@@ -1236,17 +1251,22 @@ BucketCfg bucket_cfg(int n, bool packed) {
   if (!packed) return BucketCfg{14, 2};
 #if TP_BUCKET_SMALLCFG == 1
   if (n < 28) return BucketCfg{14, 3};
+#elif TP_BUCKET_SMALLCFG == 2
+  if (n < 28) return BucketCfg{14, 2};
 #endif
   if (n < 28) return BucketCfg{13, 2};
   return BucketCfg{17, TP_BUCKET_BIGKEYS};
 }
 
-cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, BucketCfg c, void* tab, uint32_t* ptab,
-                                cudaStream_t st) {
+cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, BucketCfg c, bool packed, void* tab,
+                                uint32_t* ptab, cudaStream_t st) {
   const unsigned grid = (unsigned)B;
   uint8_t* t = static_cast<uint8_t*>(tab);
   if (c.fix == 13 && c.keys == 2) k_bucket_group<13, 2, false, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
-  else if (c.fix == 14 && c.keys == 2) k_bucket_group<14, 2, false, false><<<grid, 256, 0, st>>>(rows, n, t, ptab);
+  else if (c.fix == 14 && c.keys == 2 && !packed) k_bucket_group<14, 2, false, false><<<grid, 256, 0, st>>>(rows, n, t, ptab);
+#if TP_BUCKET_SMALLCFG == 2
+  else if (c.fix == 14 && c.keys == 2) k_bucket_group<14, 2, false, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
+#endif
 #if TP_BUCKET_SMALLCFG == 1
   else if (c.fix == 14 && c.keys == 3) k_bucket_group<14, 3, false, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
 #endif
@@ -1266,6 +1286,8 @@ cudaError_t launch_walk_bucket(int grid, const BucketParams& bp, bool packed, cu
   else if (c.fix == 13) k_walk_bucket<5, 4, true, false, 13, 2><<<grid, 128, 0, st>>>(bp);
 #if TP_BUCKET_SMALLCFG == 1
   else if (c.fix == 14) k_walk_bucket<5, 4, true, false, 14, 3><<<grid, 128, 0, st>>>(bc);
+#elif TP_BUCKET_SMALLCFG == 2
+  else if (c.fix == 14) k_walk_bucket<5, 4, true, false, 14, 2><<<grid, 128, 0, st>>>(bp);
 #endif
   else k_walk_bucket<5, 4, true, false, 17, TP_BUCKET_BIGKEYS><<<grid, 128, 0, st>>>(bc);
   return cudaGetLastError();

@@ -165,6 +165,35 @@ def test_argument_errors_raise_before_device_work():
         tp.perm_mod3_fast(tp.MatrixF3([[1] * 65] * 65))
 
 
+def test_range_bounds_checked_before_uint64_conversion():
+    """2**64 and beyond never reach ctypes (which would wrap them): the bounds
+    are Python ints checked first; n = 64 ranges ending at 2**64 are legal
+    (tp_range_sum_ex), larger ones and n > 64 are ValueError."""
+    z = np.zeros(64, np.uint64)
+    for n, lo, hi in ((64, 1, (1 << 64) + 1), (64, 5, 4), (65, 1, 2), (63, 1, 1 << 64), (20, -1, 3)):
+        with pytest.raises(ValueError):
+            _kernels.chunk_counts(z[:min(n, 64)] if n <= 64 else np.zeros(n, np.uint64),
+                                  z[:min(n, 64)] if n <= 64 else np.zeros(n, np.uint64), n, lo, hi)
+    with pytest.raises(ValueError):
+        _kernels.chunk_counts_multi(z, z, 64, 1, 1 << 64, [0])
+    m64 = tp.MatrixF3([[1] * 64] * 64)
+    with pytest.raises(ValueError):
+        tp.perm_chunk(m64, 0, 1 << 64)
+    with pytest.raises(ValueError):
+        tp.perm_chunk(m64, 1, (1 << 64) + 1)
+
+
+def test_rank_split_reaches_two_to_the_64():
+    """The rank partition of a 64-row walk (parallel.rank_range) tiles
+    [1, 2**64) with the split_steps edge rule in Python ints."""
+    from paper_2407_20205_b200 import parallel
+
+    parts = [parallel.rank_range(64, r, 8) for r in range(8)]
+    assert parts[0][0] == 1 and parts[-1][1] == 1 << 64
+    assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+    assert parts == tp.split_steps(64, 8)
+
+
 def test_library_exports_every_declared_symbol():
     with open(_kernels.HEADER_PATH) as f:
         header = f.read()
