@@ -626,7 +626,7 @@ def main():
     # tests only the 32 primary columns -- see DESIGN.md)
     kernel_name, ops_per_term = _kernels.walk_info(n, B)
     tested_frac = None
-    if "bucket" in kernel_name:
+    if "bucket" in kernel_name or "batch" in kernel_name:
         # the bucketed walk tests only the pairs its key columns do not prove
         # zero: LOP3 per term = LOP3 per tested pair x the tested fraction,
         # counted by the kernel itself over the timed steps
@@ -714,7 +714,8 @@ def main():
                     "terms_per_step": job_terms},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "LOP3 ops/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": kernel_name + " (csrc/" + ("tp_walk_bucket.cu" if "bucket" in kernel_name
+                         "kernel": kernel_name + " (csrc/" + ("tp_walk_batch.cu" if "batch" in kernel_name
+                                                              else "tp_walk_bucket.cu" if "bucket" in kernel_name
                                                               else "tp_walk_packed.cu" if "packed" in kernel_name
                                                               else "tp_walk_pair.cu" if "pair" in kernel_name
                                                               else "tp_walk_lane.cu" if "lane" in kernel_name

@@ -120,6 +120,8 @@ cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, BucketCf
                                 uint32_t* ptab, cudaStream_t st);
 cudaError_t launch_walk_bucket(int grid, const BucketParams& bp, bool packed, cudaStream_t st);
 const void* walk_bucket_symbol(bool packed);
+cudaError_t launch_walk_batch(int grid, const BucketParams& bp, cudaStream_t st);  // tp_walk_batch.cu
+int walk_batch_blocks_per_sm(bool wide);
 
 const void* walk_fast_symbol(int variant);
 const void* walk_generic_symbol(int nw);

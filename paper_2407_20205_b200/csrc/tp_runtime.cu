@@ -71,6 +71,7 @@ struct Device {
   unsigned long long* tc_err = nullptr;  // tensor-path self-check counter (must stay 0)
   unsigned long long* bucket_tested = nullptr;  // pairs tested by the bucketed walk (tp_walk_tested)
   int bucket_blocks_per_sm = 0;
+  int batch_blocks_per_sm[2] = {0, 0};  // k_walk_batch, n <= 32 / n > 32
   // Pinned staging for the synchronous single-range call (tp_range_sum): the
   // row table and zeroed counters go up in one async copy, the counters come
   // back in one (guarded by mu).
@@ -118,6 +119,10 @@ int ensure_device(int dev, Device** out) {
     TP_CUDA(cudaMalloc(&d.tc_err, sizeof(unsigned long long)));
     TP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.bucket_blocks_per_sm, tp::walk_bucket_symbol(true), 128, 0));
     if (d.bucket_blocks_per_sm < 1) return fail(TP_E_CUDA, "bucket walk cannot be resident on device %d", dev);
+    for (int w = 0; w < 2; ++w) {
+      d.batch_blocks_per_sm[w] = tp::walk_batch_blocks_per_sm(w != 0);
+      if (d.batch_blocks_per_sm[w] < 1) return fail(TP_E_CUDA, "batched walk cannot be resident on device %d", dev);
+    }
     TP_CUDA(cudaMemset(d.tc_err, 0, sizeof(unsigned long long)));
     TP_CUDA(cudaMalloc(&d.bucket_tested, sizeof(unsigned long long)));
     TP_CUDA(cudaMemset(d.bucket_tested, 0, sizeof(unsigned long long)));
@@ -211,6 +216,7 @@ struct Plan {
   int bucket_grid = 0;
   long long bucket_B = 0;
   bool bucket_packed = true;
+  bool bucket_batch = false;  // k_walk_batch instead of k_walk_bucket
   tp::BucketCfg bucket_cfg{14, 2};
   void* bucket_tab = nullptr;
   uint32_t* bucket_ptab = nullptr;
@@ -240,6 +246,14 @@ bool bucket_applies(int n, unsigned long long B) {
   // n >= 32 only with the packed filter (its verify tests the padding-slot
   // mask: there is no padding column); the unpacked pair tests need n <= 31
   return n >= 21 && n <= (m == 2 ? 31 : 64) && B > 0 && (n >= 26 || (B << (n - 15)) >= 2048ull) && m > 0;
+}
+
+// The packed bucketed walk runs as k_walk_batch (tp_walk_batch.cu: the
+// compatible steps of several superblocks batched into one filter loop);
+// TRITPERM_BATCH=0 selects k_walk_bucket (one filter loop per superblock).
+bool batch_mode() {
+  const char* e = getenv("TRITPERM_BATCH");  // read per call: tests switch it at run time
+  return e ? atoi(e) != 0 : true;
 }
 
 int tc_mode() {
@@ -328,7 +342,9 @@ int make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, uns
       const char* e = getenv("TRITPERM_BUCKET_ITEMS");  // tuning knob: the ~128 above
       return (unsigned long long)(e && atoi(e) > 0 ? atoi(e) : 128);
     }();
-    const unsigned long long warps = (unsigned long long)d.sm_count * d.bucket_blocks_per_sm * 4;
+    const bool batch = packed && batch_mode();
+    const int bps = batch ? d.batch_blocks_per_sm[n > 32 ? 1 : 0] : d.bucket_blocks_per_sm;
+    const unsigned long long warps = (unsigned long long)d.sm_count * bps * 4;
     unsigned long long nblk = std::min<unsigned long long>(std::max<unsigned long long>(total, 1), 1ull << 16);
     auto items_of = [&](unsigned long long nb) { return B * (unsigned long long)P * ((total + nb - 1) / nb); };
     // (TRITPERM_BUCKET_MIN_ITEMS: items per warp at least, default 4.  One
@@ -350,6 +366,7 @@ int make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, uns
       if (int rc = sc.take(tb + (size_t)B * P * sizeof(uint32_t), &mem)) return rc;
       pl.bucket = true;
       pl.bucket_packed = packed;
+      pl.bucket_batch = batch;
       pl.bucket_B = (long long)B;
       pl.bucket_cfg = cfg;
       pl.bucket_tab = mem;
@@ -375,7 +392,7 @@ int make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, uns
       pl.bkp.ptab = pl.bucket_ptab;
       pl.bkp.tested = d.bucket_tested;
       pl.bkp.s_end = s1;
-      const unsigned long long ctas = (unsigned long long)d.sm_count * d.bucket_blocks_per_sm;
+      const unsigned long long ctas = (unsigned long long)d.sm_count * bps;
       pl.bucket_grid = (int)std::max<unsigned long long>(1, std::min(ctas, (f.items + 3) / 4));
       if (full) return TP_OK;
       bucket_mid = true;
@@ -525,7 +542,8 @@ int run_plan(const Plan& pl, cudaStream_t st, int* launches) {
   if (pl.bucket) {  // (ranges: plus the generic head and tail below)
     TP_CUDA(tp::launch_bucket_group(pl.bkp.fp.rows, pl.bucket_B, pl.bkp.fp.n, pl.bucket_cfg, pl.bucket_packed,
                                     pl.bucket_tab, pl.bucket_ptab, st));
-    TP_CUDA(tp::launch_walk_bucket(pl.bucket_grid, pl.bkp, pl.bucket_packed, st));
+    if (pl.bucket_batch) TP_CUDA(tp::launch_walk_batch(pl.bucket_grid, pl.bkp, st));
+    else TP_CUDA(tp::launch_walk_bucket(pl.bucket_grid, pl.bkp, pl.bucket_packed, st));
     nl += 2;
   }
   if (pl.tc) {
@@ -1028,8 +1046,10 @@ int tp_walk_info(int n, long long batch, char* name, int name_len, double* lop3_
     // 1.5 LOP3 per TESTED pair: the bucketed walk skips the incompatible
     // steps, so the tested fraction (tp_walk_tested) scales this per term
     const bool packed = bucket_mode() != 2;
-    if (name && name_len > 0)
-      snprintf(name, (size_t)name_len, "k_walk_bucket<%s> V=%d", packed ? "packed" : "pair", tp::bucket_v(packed));
+    if (name && name_len > 0) {
+      if (packed && batch_mode()) snprintf(name, (size_t)name_len, "k_walk_batch<packed> V=%d", tp::bucket_v(packed));
+      else snprintf(name, (size_t)name_len, "k_walk_bucket<%s> V=%d", packed ? "packed" : "pair", tp::bucket_v(packed));
+    }
     if (lop3_per_term) *lop3_per_term = packed ? 1.5 : 2.0;
     return TP_OK;
   }

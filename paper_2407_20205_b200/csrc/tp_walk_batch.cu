@@ -1,0 +1,567 @@
+// tp_walk_batch.cu -- the bucketed pair walk with batched compatible steps:
+// the default walk for 21 <= n <= 64 (full traversals and the superblock-
+// aligned middle of step ranges).
+//
+// Same decomposition as k_walk_bucket (tp_walk_bucket.cu): a warp holds one
+// piece of 1024 A subsets of one key bucket (decoded from the matrix's half
+// tables, tp_bucket.cuh) and walks the B side in superblocks of 32 Gray
+// steps, one B state per lane; a B state is compatible with the piece iff no
+// key column of the sum is forced to zero.  The difference is where the
+// compatible states go.  k_walk_bucket runs the packed filter once per
+// superblock over the ~14 (2 keys) or ~6 (4 keys) compatible steps it finds,
+// so the per-superblock fixed cost (loop set-up, pops of the step mask,
+// pass-list votes, the verify dispatch) is paid for every 7 or 3 filter
+// iterations.  Here each superblock's compatible states are compacted into a
+// per-warp list in shared memory (ballot + prefix popcount), NBAT superblocks
+// fill one list, and the filter then runs one long counted loop over it:
+//
+//   * list entry e: the doubled low 16 columns (Hc, what the filter reads,
+//     two entries = one 16-byte load), the full state (Hf, z and u words;
+//     H1 the secondary word for n > 32) and the step within the batch (Hj,
+//     whose parity is the B subset's size parity: batches start at even
+//     steps);
+//   * the filter is the packed test of tp_walk_bucket.cu (1.5 LOP3 per pair:
+//     two pairs per 32-bit word, zero-field test on the FMA pipe); a lane's
+//     passes (mask of words x the two steps, list index) go to its pass list
+//     E and are verified exactly after the loop;
+//   * a pass list that overflows, and event-dense matrices, take the exact
+//     evaluation of the whole list; deduplicated (weighted) A sides take the
+//     weighted exact walk, as in k_walk_bucket.
+//
+// Only zero terms are skipped, so the raw partials equal chunk_sum
+// (src/_kernels.py:90-128) bit for bit.
+#include "tp_bucket.cuh"
+
+namespace tp {
+
+namespace {
+
+// Per-warp shared-memory layout (dynamic shared memory, 4 warps per block).
+template <int NBAT, int ECAP, bool WIDE, int FIX>
+struct BatchSmem {
+  static constexpr int NR = (WIDE ? 64 : 32) - FIX;  // B-side rows FIX..n-1
+  static constexpr int NS = NBAT * 32;               // list capacity: steps per batch
+  static constexpr int oR = 0;                          // RowRec[NR]: row r at r - FIX
+  static constexpr int oA = align16(oR + 32 * NR);      // uint4[16][32]: full A words (slot w | slot w + 16)
+  static constexpr int oHc = oA + 16 * 32 * 16;         // uint2[NS]: doubled low 16 columns (zz, uu)
+  static constexpr int oHf = oHc + 8 * NS;              // uint2[NS]: full state (z, u)
+  static constexpr int oH1 = oHf + 8 * NS;              // uint2[NS]: n > 32, secondary word (z, u)
+  static constexpr int oHj = oH1 + (WIDE ? 8 * NS : 0);  // uint8[NS]: step within the batch
+  static constexpr int oE = align16(oHj + NS);          // uint2[ECAP][32]: passes (mask, list index)
+  static constexpr int kWarp = align16(oE + 8 * 32 * ECAP);
+};
+
+// Exact evaluation of list entries [0, L) against this lane's 32 slots, n <= 32
+// (dense mode and pass-list overflow).  Returns ev | odd << 32.
+static __device__ __noinline__ unsigned long long batch_exact_packed(const uint4 (*A2)[32], const uint2* Hf,
+                                                                     const uint8_t* Hj, uint32_t L, uint32_t lane,
+                                                                     uint32_t spm, uint32_t vmask, uint32_t colmask,
+                                                                     int n, uint32_t one) {
+  constexpr int K = 32;
+  uint32_t bev = 0, bodd = 0;
+#pragma unroll 1
+  for (uint32_t e = 0; e < L; ++e) {
+    const uint2 h = Hf[e];
+    const uint32_t jp = Hj[e] & 1u;
+    const uint32_t gh = pair_g2(h.x, h.y);
+    uint32_t n0 = 0, a0 = 0;
+    if (n <= 31) {
+      // the subset parity rides in padding column 31 of the sign word
+      const uint32_t cmp = colmask | 0x80000000u;
+#pragma unroll
+      for (int w = 0; w < K / 2; ++w) {
+        const uint4 a = A2[w][lane];
+        exact_fold(a.x, a.y, h.x, h.y, gh, cmp, n0, a0, one);
+        exact_fold(a.z, a.w, h.x, h.y, gh, cmp, n0, a0, one);
+      }
+    } else {
+      // n = 32: the slot parity is a runtime bit folded into the sign parity
+#pragma unroll
+      for (int w = 0; w < K / 2; ++w) {
+        const uint4 a = A2[w][lane];
+        exact_fold_par(a.x, a.y, h.x, h.y, gh, colmask, (spm >> w) & 1u, n0, a0, one);
+        exact_fold_par(a.z, a.w, h.x, h.y, gh, colmask, (spm >> (w + K / 2)) & 1u, n0, a0, one);
+      }
+      // padding slots hold the zero vector: each pairs fully with a full y
+      // with subset parity 0; remove them
+      if (h.x == 0u) {
+        const uint32_t nd = (uint32_t)K - __popc(vmask);
+        n0 -= nd;
+        a0 -= nd * (__popc(gh) & 1u);
+      }
+    }
+    bev += n0;
+    bodd += jp ? (n0 - a0) : a0;
+  }
+  return (unsigned long long)bev | ((unsigned long long)bodd << 32);
+}
+
+// n > 32: exact evaluation of list entries [0, L) against this lane's real
+// slots, both words; slot-major in position order (one run cursor).
+template <int FIX, int KEYS>
+static __device__ __noinline__ unsigned long long batch_exact_wide(const uint4 (*A2)[32], const uint2* Hf,
+                                                                   const uint2* H1, const uint8_t* Hj, uint32_t L,
+                                                                   const uint8_t* Tm, uint32_t grp, uint32_t pbase,
+                                                                   uint32_t cnt, uint32_t lane, uint32_t spm,
+                                                                   uint32_t z1i) {
+  using T = Tab<FIX, KEYS, true>;
+  const uint4* vec = reinterpret_cast<const uint4*>(Tm + T::kVec);
+  RunCursor<KEYS> cur;
+  cur.init(reinterpret_cast<const uint16_t*>(Tm), grp);
+  uint32_t ev = 0, odd = 0;
+#pragma unroll 1
+  for (uint32_t r = 0; 32u * r + lane < cnt; ++r) {  // this lane's real slots: rows r = lrow(k)
+    const uint32_t k = (r >> 1) + ((r & 1u) << 4);
+    const uint32_t p = pbase + 32u * r + lane;
+    uint32_t i0, i1;
+    cur.seek(p);
+    cur.index(p, i0, i1);
+    const uint4 lo = vec[i0], hi = vec[T::N0 + i1];
+    uint32_t za1 = lo.z, ga1 = lo.w;
+    sub_word(za1, ga1, hi.z, hi.w);
+    const uint4 a4 = A2[k & 15][lane];
+    const uint32_t za = k < 16 ? a4.x : a4.z, ga = k < 16 ? a4.y : a4.w;
+    const uint32_t kp = (spm >> k) & 1u;
+#pragma unroll 1
+    for (uint32_t e = 0; e < L; ++e) {
+      const uint2 h = Hf[e];
+      uint32_t d, zp;
+      TP_LOP3(d, za, ga, h.y, 0x06);
+      TP_LOP3(zp, d, za, h.x, 0x09);
+      if (zp == 0) {
+        const uint2 h1 = H1[e];
+        uint32_t d1, zp1;
+        TP_LOP3(d1, za1, ga1, h1.y, 0x06);
+        TP_LOP3(zp1, d1, za1, h1.x, 0x09);
+        if (zp1 == 0) {
+          ev += 1;
+          odd += (__popc(d ^ pair_g2(h.x, h.y)) + __popc((d1 ^ pair_g2(h1.x, h1.y)) & z1i) + Hj[e] + kp) & 1u;
+        }
+      }
+    }
+  }
+  return (unsigned long long)ev | ((unsigned long long)odd << 32);
+}
+
+// Weighted matrices (deduplicated A side): exact evaluation of list entries
+// [0, L) against this lane's real slots, each slot standing for `we` subsets
+// of even and `wo` of odd size with the same vector (k_walk_bucket's
+// bucket_exact_weighted over the list).  Flushed into pm right away: per
+// lane <= 2^17 subsets x NS steps, per warp < 2^(22 + log2 NS) < 2^32.
+template <int FIX, int KEYS, bool WIDE>
+static __device__ __noinline__ void batch_exact_weighted(const uint2* Hf, const uint2* H1, const uint8_t* Hj,
+                                                         uint32_t L, const uint8_t* Tm, uint32_t grp,
+                                                         uint32_t pbase, uint32_t cnt, uint32_t lane,
+                                                         uint32_t colmask, uint32_t z1i, unsigned long long* pm) {
+  using T = Tab<FIX, KEYS, WIDE>;
+  const uint32_t* wts = reinterpret_cast<const uint32_t*>(Tm + T::kWt);
+  RunCursor<KEYS> cur;
+  cur.init(reinterpret_cast<const uint16_t*>(Tm), grp);
+  uint32_t ev = 0, odd = 0;
+#pragma unroll 1
+  for (uint32_t r = 0; 32u * r + lane < cnt; ++r) {
+    const uint32_t p = pbase + 32u * r + lane;
+    uint32_t i0, i1;
+    cur.seek(p);
+    cur.index(p, i0, i1);
+    const uint32_t w0 = wts[i0], w1 = wts[T::N0 + i1];
+    const uint32_t e0 = w0 & 0xFFFFu, o0 = w0 >> 16, e1 = w1 & 0xFFFFu, o1 = w1 >> 16;
+    const uint32_t we = e0 * e1 + o0 * o1, wo = e0 * o1 + o0 * e1;
+    uint32_t za, ga, za1 = 0, ga1 = 0;
+    if constexpr (WIDE) {
+      const uint4 lo = reinterpret_cast<const uint4*>(Tm + T::kVec)[i0];
+      const uint4 hi = reinterpret_cast<const uint4*>(Tm + T::kVec)[T::N0 + i1];
+      za = lo.x;
+      ga = lo.y;
+      sub_word(za, ga, hi.x, hi.y);
+      za1 = lo.z;
+      ga1 = lo.w;
+      sub_word(za1, ga1, hi.z, hi.w);
+    } else {
+      const uint2 lo = reinterpret_cast<const uint2*>(Tm + T::kVec)[i0];
+      const uint2 hi = reinterpret_cast<const uint2*>(Tm + T::kVec)[T::N0 + i1];
+      za = lo.x;
+      ga = lo.y;
+      sub_word(za, ga, hi.x, hi.y);
+    }
+#pragma unroll 1
+    for (uint32_t e = 0; e < L; ++e) {
+      const uint2 h = Hf[e];
+      uint32_t d, zp;
+      TP_LOP3(d, za, ga, h.y, 0x06);
+      TP_LOP3(zp, d, za, h.x, 0x09);
+      if (zp != 0) continue;
+      uint32_t sp = __popc((d ^ pair_g2(h.x, h.y)) & colmask) + Hj[e];
+      if constexpr (WIDE) {
+        const uint2 h1 = H1[e];
+        uint32_t d1, zp1;
+        TP_LOP3(d1, za1, ga1, h1.y, 0x06);
+        TP_LOP3(zp1, d1, za1, h1.x, 0x09);
+        if (zp1 != 0) continue;
+        sp += __popc((d1 ^ pair_g2(h1.x, h1.y)) & z1i);
+      }
+      ev += we + wo;
+      odd += (sp & 1u) ? we : wo;
+    }
+  }
+  warp_flush(pm, ev - odd, odd, lane);
+}
+
+}  // namespace
+
+template <int NBAT, int ECAP, bool WIDE, int FIX, int KEYS>
+__global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp) {
+  constexpr int V = 5, K = 32, SB = 32;
+  constexpr int kBucketPieces = pieces_of(FIX, KEYS);
+  using T = Tab<FIX, KEYS, WIDE>;
+  using S = BatchSmem<NBAT, ECAP, WIDE, FIX>;
+  const FastParams& p = bp.fp;
+  extern __shared__ __align__(16) uint8_t batch_smem[];
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint8_t* ws = batch_smem + warp * S::kWarp;
+  RowRec* R = reinterpret_cast<RowRec*>(ws + S::oR);  // row r at R[r - FIX]
+  uint4 (*A2)[32] = reinterpret_cast<uint4 (*)[32]>(ws + S::oA);
+  uint2* Hc = reinterpret_cast<uint2*>(ws + S::oHc);
+  uint2* Hf = reinterpret_cast<uint2*>(ws + S::oHf);
+  uint2* H1 = reinterpret_cast<uint2*>(ws + S::oH1);
+  uint8_t* Hj = ws + S::oHj;
+  uint2 (*E)[32] = reinterpret_cast<uint2 (*)[32]>(ws + S::oE);
+  const uint32_t cneg = 0xfffeffffu * p.one;  // -0x00010001, runtime so ptxas keeps the IMAD
+  const uint32_t one = p.one;
+  const uint32_t colmask = p.z0_init;   // real columns (n <= 31: bit 31 is padding)
+  const uint32_t colmask1 = p.z1_init;  // n > 32: real columns of the secondary word
+  const int k1 = (WIDE ? 32 : p.n) - 1;  // key columns k1, k1-1, ..
+  const uint32_t lanemask_lt = (1u << lane) - 1u;
+  unsigned long long n_items = 0;
+
+  for (;;) {
+    const unsigned long long item = next_item(p, lane, n_items, blockIdx.x * 4 + warp);
+    if (item >= p.items) break;
+    ++n_items;
+    // item = (piece * chunks + chunk) * B + matrix (k_walk_bucket's order)
+    const unsigned long long nmat = p.items / ((unsigned long long)kBucketPieces * p.chunks);
+    const unsigned long long rest = item / nmat;
+    const unsigned long long b = item - rest * nmat;
+    const uint32_t q = (uint32_t)(rest / p.chunks);
+    const unsigned long long c = rest - (unsigned long long)q * p.chunks;
+    const unsigned long long sb0 = p.F0 + c * p.nblk;
+    const uint32_t nsb = (uint32_t)min((unsigned long long)p.nblk, bp.s_end - sb0);
+    const unsigned long long A0 = sb0 << V;
+    TP_CHECK(q < (uint32_t)kBucketPieces && b < nmat);
+    const uint32_t pt = bp.ptab[b * kBucketPieces + q];
+    const uint32_t cnt = (pt >> 8) & 0xFFFu;  // real slots of the piece
+    if (cnt == 0) continue;                   // unused piece
+    const uint32_t grp = pt & 0xFFu;
+    const uint32_t pbase = ((pt >> 20) & 0x7FFu) << 10;  // positions [pbase, pbase + cnt) of the bucket
+    const bool weighted = (pt >> 31) != 0;
+    TP_CHECK(cnt <= 1024u && grp < (uint32_t)nbuckets(KEYS));
+    const uint32_t nwd = (cnt + 63u) >> 6;  // packed words holding the piece's real slots
+    __syncwarp();
+    {  // B-side rows FIX..n-1
+      const uint4* s = reinterpret_cast<const uint4*>(p.rows + b * 64 + FIX);
+      uint4* d = reinterpret_cast<uint4*>(R);
+      TP_CHECK(p.n - FIX <= S::NR);
+      for (int x = (int)lane; x < 2 * (p.n - FIX); x += 32) d[x] = s[x];
+    }
+
+    // A side: slot k of this lane is position pbase + 32 lrow(k) + lane of
+    // the bucket (tp_bucket.cuh); full words to shared memory, the packed
+    // words (low 16 columns of slots w and w + 16) to registers.
+    uint32_t Zp[K / 2], Gp[K / 2];
+    uint32_t spm = 0;    // bit k: parity of slot k's subset
+    uint32_t vmask = 0;  // bit k: slot k holds a real A subset
+    const uint8_t* Tm = static_cast<const uint8_t*>(bp.tab) + b * T::kBytes;
+    {
+      const uint32_t* wts = reinterpret_cast<const uint32_t*>(Tm + T::kWt);
+      RunCursor<KEYS> cur;
+      cur.init(reinterpret_cast<const uint16_t*>(Tm), grp);
+#pragma unroll 1
+      for (uint32_t r = 0; r < (uint32_t)K; ++r) {
+        const int k = (int)((r >> 1) + ((r & 1u) << 4));
+        const uint32_t rr = 32u * r + lane;
+        uint32_t z, g;
+        if (rr >= cnt) {  // dummy slot: n <= 31 -1 in padding column 31; n = 32: vmask
+          z = colmask;
+          g = p.n <= 31 ? 0x80000000u : 0u;
+        } else {
+          uint32_t i0, i1;
+          cur.seek(pbase + rr);
+          cur.index(pbase + rr, i0, i1);
+          const uint2 lo = *reinterpret_cast<const uint2*>(Tm + T::kVec + T::VE * i0);
+          const uint2 hi = *reinterpret_cast<const uint2*>(Tm + T::kVec + T::VE * (T::N0 + i1));
+          const uint32_t par = ((wts[i0] ^ wts[T::N0 + i1]) >> 16) & 1u;
+          z = lo.x;
+          g = lo.y;
+          sub_word(z, g, hi.x, hi.y);
+          vmask |= 1u << k;
+          // n <= 31: padding column 31 carries the subset parity as the trit p
+          if (p.n <= 31 && !par) z |= 0x80000000u;
+          spm |= par << k;
+        }
+        reinterpret_cast<uint2*>(&A2[k & 15][lane])[k >> 4] = make_uint2(z, g);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int w = 0; w < K / 2; ++w) {
+        const uint4 a = A2[w][lane];
+        Zp[w] = __byte_perm(a.x, a.z, 0x5410);
+        Gp[w] = __byte_perm(a.y, a.w, 0x5410);
+      }
+    }
+    // forbidden key trits of this piece: f = -x (mod 3)
+    uint32_t F0 = 0, F1 = 0, F2 = 0;
+    {
+      uint32_t rest_g = grp;
+#pragma unroll
+      for (int i = KEYS - 1; i >= 0; --i) {
+        const uint32_t x = rest_g % 3u;
+        rest_g /= 3u;
+        const uint32_t f = (3u - x) % 3u, bit = 1u << (k1 - i);
+        F0 |= f == 0 ? bit : 0u;
+        F1 |= f == 1 ? bit : 0u;
+        F2 |= f == 2 ? bit : 0u;
+      }
+    }
+    // B side: v2 for S2 = gray(A0) on rows >= FIX
+    uint32_t z2, u2, z2w = 0, u2w = 0;
+    {
+      uint32_t z = colmask, g = 0, zw = colmask1, gw = 0;
+      const unsigned long long hs = A0 ^ (A0 >> 1);
+      for (int r = FIX; r < p.n; ++r)
+        if ((hs >> (r - FIX)) & 1ull) {
+          sub_word(z, g, R[r - FIX].m[0], R[r - FIX].a[0]);
+          if (WIDE) sub_word(zw, gw, R[r - FIX].m[1], R[r - FIX].a[1]);
+        }
+      z2 = z;
+      u2 = pair_u2(z, g);
+      z2w = zw;
+      u2w = pair_u2(zw, gw);
+    }
+    uint32_t ev = 0, odd = 0;
+    uint32_t tested_steps = 0;
+    bool dense = false;
+    for (uint32_t kb0 = 0; kb0 < nsb; kb0 += NBAT) {
+      const uint32_t nbt = min((uint32_t)NBAT, nsb - kb0);
+      uint32_t L = 0;  // list length
+      __syncwarp();    // the previous batch's list is consumed
+#pragma unroll 1
+      for (uint32_t t = 0; t < nbt; ++t) {
+        const uint32_t kb = kb0 + t;
+        // this lane's B state: step j = lane of superblock kb (the top row's
+        // direction follows the parity of the global superblock index)
+        const bool godd = ((sb0 + kb) & 1ull) != 0;
+        uint32_t zj = z2, uj = u2, zjw = z2w, ujw = u2w;
+        {
+          const uint32_t gj = lane ^ (lane >> 1);
+#pragma unroll
+          for (int r = 0; r < V; ++r) {
+            if ((gj >> r) & 1u) {
+              const bool lv = (r == V - 1) && godd;
+              const RowRec& row = R[r];
+              sub_word_u(zj, uj, row.m[0], lv ? row.s[0] : row.a[0], lv ? row.a[0] : row.s[0]);
+              if (WIDE) sub_word_u(zjw, ujw, row.m[1], lv ? row.s[1] : row.a[1], lv ? row.a[1] : row.s[1]);
+            }
+          }
+        }
+        // compatible: no key column of y equals the forbidden trit
+        const uint32_t match = (zj & F0) | (~zj & ~uj & F2) | (~zj & uj & F1);
+        const uint32_t cmask = __ballot_sync(FULL, match == 0u);
+        if (match == 0u) {
+          const uint32_t pos = L + __popc(cmask & lanemask_lt);
+          TP_CHECK(pos < (uint32_t)S::NS);
+          Hc[pos] = make_uint2(__byte_perm(zj, zj, 0x1010), __byte_perm(uj, uj, 0x1010));
+          Hf[pos] = make_uint2(zj, uj);
+          if (WIDE) H1[pos] = make_uint2(zjw, ujw);
+          Hj[pos] = (uint8_t)(32u * t + lane);
+        }
+        L += __popc(cmask);
+        // (z2, u2) = step SB-1 of this superblock, then the entry of kb + 1
+        z2 = __shfl_sync(FULL, zj, SB - 1);
+        u2 = __shfl_sync(FULL, uj, SB - 1);
+        if (WIDE) {
+          z2w = __shfl_sync(FULL, zjw, SB - 1);
+          u2w = __shfl_sync(FULL, ujw, SB - 1);
+        }
+        if (kb + 1 < nsb) {
+          // entry of global superblock G flips row FIX + V + tz(G); it leaves
+          // iff bit tz(G) + 1 of G is set
+          const unsigned long long G = sb0 + kb + 1;
+          const int tzg = tz64(G);
+          const RowRec& row = R[V + tzg];
+          const bool lv = ((G >> (tzg + 1)) & 1ull) != 0;
+          sub_word_u(z2, u2, row.m[0], lv ? row.s[0] : row.a[0], lv ? row.a[0] : row.s[0]);
+          if (WIDE) sub_word_u(z2w, u2w, row.m[1], lv ? row.s[1] : row.a[1], lv ? row.a[1] : row.s[1]);
+        }
+      }
+      tested_steps += L;
+      __syncwarp();
+      if (L == 0) continue;
+      if (weighted) {  // deduplicated A side: every listed step exactly, with weights
+        batch_exact_weighted<FIX, KEYS, WIDE>(Hf, H1, Hj, L, Tm, grp, pbase, cnt, lane, colmask, colmask1,
+                                              p.pm + 2 * b);
+        continue;
+      }
+      auto exact_list = [&](uint32_t& bev, uint32_t& bodd) {
+        unsigned long long r;
+        if constexpr (WIDE) r = batch_exact_wide<FIX, KEYS>(A2, Hf, H1, Hj, L, Tm, grp, pbase, cnt, lane, spm, colmask1);
+        else r = batch_exact_packed(A2, Hf, Hj, L, lane, spm, vmask, colmask, p.n, one);
+        bev = (uint32_t)r;
+        bodd = (uint32_t)(r >> 32);
+      };
+      if (dense) {
+        uint32_t bev, bodd;
+        exact_list(bev, bodd);
+        ev += bev;
+        odd += bodd;
+        dense = __any_sync(FULL, bev >= (uint32_t)(K / 2) * nbt);
+        continue;
+      }
+      // the packed filter over the list, two entries per iteration: bit w
+      // (entry i) / 16 + w (entry i + 1) of M = a pass of word w
+      uint32_t ne = 0;
+      auto filter = [&](auto Wc) {
+        constexpr int W = decltype(Wc)::value;
+        uint32_t i = 0;
+#pragma unroll 1
+        for (; i + 2 <= L; i += 2) {
+          const uint4 hab = *reinterpret_cast<const uint4*>(Hc + i);
+          uint32_t M = 0;
+          static_for<W>([&](auto wc) {
+            constexpr int w = decltype(wc)::value;
+            packed_test<(1u << w)>(Zp[w], Gp[w], hab.x, hab.y, M, one, cneg);
+            packed_test<(1u << (16 + w))>(Zp[w], Gp[w], hab.z, hab.w, M, one, cneg);
+          });
+          if (M) {
+            if (ne < (uint32_t)ECAP) E[ne][lane] = make_uint2(M, i);
+            ++ne;
+          }
+        }
+        if (i < L) {  // an odd last entry alone
+          const uint2 ha = Hc[i];
+          uint32_t M = 0;
+          static_for<W>([&](auto wc) {
+            constexpr int w = decltype(wc)::value;
+            packed_test<(1u << w)>(Zp[w], Gp[w], ha.x, ha.y, M, one, cneg);
+          });
+          if (M) {
+            if (ne < (uint32_t)ECAP) E[ne][lane] = make_uint2(M, i);
+            ++ne;
+          }
+        }
+      };
+      using FW = FilterWidths<FIX, KEYS>;
+      if constexpr (FW::WA == 16) {
+        filter(std::integral_constant<int, 16>{});
+      } else {
+        if (nwd > (uint32_t)FW::WA) filter(std::integral_constant<int, 16>{});
+        else if (nwd > (uint32_t)FW::WB) filter(std::integral_constant<int, FW::WA>{});
+        else filter(std::integral_constant<int, FW::WB>{});
+      }
+      const uint32_t nemax = __reduce_max_sync(FULL, ne);
+      if (nemax > (uint32_t)ECAP) {
+        // a lane's pass list overflowed (event-dense matrix): the whole list exactly
+        __syncwarp();
+        uint32_t bev, bodd;
+        exact_list(bev, bodd);
+        ev += bev;
+        odd += bodd;
+        dense = p.dense_ok != 0 && __any_sync(FULL, bev >= (uint32_t)(K / 2) * nbt);
+      } else if (nemax != 0) {
+        uint32_t bev = 0, bodd = 0;
+        for (uint32_t e = 0; e < ne; ++e) {
+          const uint2 ent = E[e][lane];
+          uint32_t M = ent.x;
+          while (M) {
+            const uint32_t bit = __ffs(M) - 1;
+            M &= M - 1;
+            const uint32_t j = ent.y + (bit >> 4), w = bit & 15u;
+            TP_CHECK(j < L);
+            const uint2 h = Hf[j];
+            const uint32_t gh = pair_g2(h.x, h.y);
+            const uint32_t jp = Hj[j] & 1u;
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              const uint32_t k = w + 16 * hf;
+              const uint4 a4 = A2[w][lane];
+              const uint2 a = hf ? make_uint2(a4.z, a4.w) : make_uint2(a4.x, a4.y);
+              uint32_t d, zp;
+              TP_LOP3(d, a.x, a.y, h.y, 0x06);
+              TP_LOP3(zp, d, a.x, h.x, 0x09);
+              if (zp == 0 && ((vmask >> k) & 1u)) {
+                uint32_t par = 0;
+                if constexpr (WIDE) {
+                  // the primary columns are nonzero: test the secondary ones
+                  const uint32_t rr =
+                      bucket_wide_term<FIX, KEYS>(Tm, grp, pbase + 32u * lrow(k) + lane, H1[j], colmask1);
+                  if (!rr) continue;
+                  par = rr >> 1;
+                }
+                bev += 1;
+                bodd += (__popc((d ^ gh) & colmask) + par + jp + ((spm >> k) & 1u)) & 1u;
+              }
+            }
+          }
+        }
+        ev += bev;
+        odd += bodd;
+        // event-dense (e.g. all-ones rows): exact mode for the next batches
+        dense = p.dense_ok != 0 && __any_sync(FULL, bev >= (uint32_t)(K / 2) * nbt);
+      }
+    }
+    warp_flush(p.pm + 2 * b, ev - odd, odd, lane);
+    if (bp.tested && lane == 0) {
+      const uint32_t words = FilterWidths<FIX, KEYS>::width(nwd);
+      atomicAdd(bp.tested, 64ull * words * tested_steps);
+    }
+  }
+  queue_done(p, lane);
+}
+
+// Batch shapes: NBAT superblocks per list, ECAP pass-list entries per lane.
+// Sized so that four 4-warp blocks fit an SM (228 KB of shared memory).
+template <bool WIDE>
+struct BatchShape {
+  static constexpr int NBAT = WIDE ? 2 : 4;
+  static constexpr int ECAP = WIDE ? 8 : 10;
+};
+
+template <bool WIDE, int FIX, int KEYS>
+static cudaError_t launch_batch_k(int grid, const BucketParamsCfg& bc, cudaStream_t st) {
+  using Sh = BatchShape<WIDE>;
+  constexpr int bytes = 4 * BatchSmem<Sh::NBAT, Sh::ECAP, WIDE, FIX>::kWarp;
+  auto* k = &k_walk_batch<Sh::NBAT, Sh::ECAP, WIDE, FIX, KEYS>;
+  static const cudaError_t attr = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (attr != cudaSuccess) return attr;
+  k<<<grid, 128, bytes, st>>>(bc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_walk_batch(int grid, const BucketParams& bp, cudaStream_t st) {
+  const BucketCfg c = bucket_cfg(bp.fp.n, true);
+  const BucketParamsCfg bc{bp.fp, bp.tab, bp.ptab, bp.tested, bp.s_end, c.fix, c.keys};
+  if (bp.fp.n > 32) return launch_batch_k<true, 17, TP_BUCKET_BIGKEYS>(grid, bc, st);
+  if (c.fix == 13 && c.keys == 2) return launch_batch_k<false, 13, 2>(grid, bc, st);
+  if (c.fix == 17 && c.keys == TP_BUCKET_BIGKEYS) return launch_batch_k<false, 17, TP_BUCKET_BIGKEYS>(grid, bc, st);
+  return cudaErrorInvalidValue;
+}
+
+// blocks of the batched walk resident per SM (the plan sizes its grid with it)
+int walk_batch_blocks_per_sm(bool wide) {
+  int nb = 0;
+  if (wide) {
+    using Sh = BatchShape<true>;
+    constexpr int bytes = 4 * BatchSmem<Sh::NBAT, Sh::ECAP, true, 17>::kWarp;
+    auto* k = &k_walk_batch<Sh::NBAT, Sh::ECAP, true, 17, TP_BUCKET_BIGKEYS>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 128, bytes) != cudaSuccess) return 0;
+  } else {
+    using Sh = BatchShape<false>;
+    constexpr int bytes = 4 * BatchSmem<Sh::NBAT, Sh::ECAP, false, 13>::kWarp;
+    auto* k = &k_walk_batch<Sh::NBAT, Sh::ECAP, false, 13, 2>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 128, bytes) != cudaSuccess) return 0;
+  }
+  return nb;
+}
+
+}  // namespace tp
