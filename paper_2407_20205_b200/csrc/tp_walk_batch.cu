@@ -48,7 +48,10 @@ struct BatchSmem {
   static constexpr int oH1 = oHf + 8 * NS;              // uint2[NS]: n > 32, secondary word (z, u)
   static constexpr int oHj = oH1 + (WIDE ? 8 * NS : 0);  // uint8[NS]: step within the batch
   static constexpr int oE = align16(oHj + NS);          // uint2[ECAP][32]: passes (mask, list index)
-  static constexpr int kWarp = align16(oE + 8 * 32 * ECAP);
+  // per lane the low-row part of its B state in row form, for superblocks
+  // of even / odd index: uint2 (m, s) [2][32], n > 32 uint4 (m0, s0, m1, s1)
+  static constexpr int oL = oE + 8 * 32 * ECAP;
+  static constexpr int kWarp = align16(oL + 2 * 32 * (WIDE ? 16 : 8));
 };
 
 // Exact evaluation of list entries [0, L) against this lane's 32 slots, n <= 32
@@ -226,6 +229,8 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
   uint2* H1 = reinterpret_cast<uint2*>(ws + S::oH1);
   uint8_t* Hj = ws + S::oHj;
   uint2 (*E)[32] = reinterpret_cast<uint2 (*)[32]>(ws + S::oE);
+  uint2* L2 = reinterpret_cast<uint2*>(ws + S::oL);  // [parity][lane] (m, s), n <= 32
+  uint4* L4 = reinterpret_cast<uint4*>(ws + S::oL);  // [parity][lane] (m0, s0, m1, s1), n > 32
   const uint32_t cneg = 0xfffeffffu * p.one;  // -0x00010001, runtime so ptxas keeps the IMAD
   const uint32_t one = p.one;
   const uint32_t colmask = p.z0_init;   // real columns (n <= 31: bit 31 is padding)
@@ -322,20 +327,39 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
         F2 |= f == 2 ? bit : 0u;
       }
     }
-    // B side: v2 for S2 = gray(A0) on rows >= FIX
-    uint32_t z2, u2, z2w = 0, u2w = 0;
+    // B side.  Step j of superblock G is the subset gray(32 G + j) of rows
+    // FIX.. : rows FIX+5.. from gray(G) (the "high" state H, the same for
+    // every lane) and rows FIX..FIX+4 from gray(j) ^ (G odd ? 16 : 0) (this
+    // lane's low part, two vectors per item, L[G & 1][lane]).  So a lane's
+    // state is one add, H + L, and H changes by one row per superblock.
+    uint32_t zh, uh, zhw = 0, uhw = 0;
     {
       uint32_t z = colmask, g = 0, zw = colmask1, gw = 0;
-      const unsigned long long hs = A0 ^ (A0 >> 1);
-      for (int r = FIX; r < p.n; ++r)
-        if ((hs >> (r - FIX)) & 1ull) {
+      const unsigned long long hs = sb0 ^ (sb0 >> 1);
+      for (int r = FIX + V; r < p.n; ++r)
+        if ((hs >> (r - FIX - V)) & 1ull) {
           sub_word(z, g, R[r - FIX].m[0], R[r - FIX].a[0]);
           if (WIDE) sub_word(zw, gw, R[r - FIX].m[1], R[r - FIX].a[1]);
         }
-      z2 = z;
-      u2 = pair_u2(z, g);
-      z2w = zw;
-      u2w = pair_u2(zw, gw);
+      zh = z;
+      uh = pair_u2(z, g);
+      zhw = zw;
+      uhw = pair_u2(zw, gw);
+#pragma unroll
+      for (uint32_t par = 0; par < 2; ++par) {
+        const uint32_t gl = (lane ^ (lane >> 1)) ^ (par << 4);
+        uint32_t zl = colmask, gll = 0, zlw = colmask1, glw = 0;
+#pragma unroll
+        for (int r = 0; r < V; ++r)
+          if ((gl >> r) & 1u) {
+            sub_word(zl, gll, R[r].m[0], R[r].a[0]);
+            if (WIDE) sub_word(zlw, glw, R[r].m[1], R[r].a[1]);
+          }
+        // row form on the real columns (padding columns stay H's +1)
+        const uint32_t m0 = ~zl & colmask, m1 = ~zlw & colmask1;
+        if (WIDE) L4[32 * par + lane] = make_uint4(m0, gll & m0, m1, glw & m1);
+        else L2[32 * par + lane] = make_uint2(m0, gll & m0);
+      }
     }
     uint32_t ev = 0, odd = 0;
     uint32_t tested_steps = 0;
@@ -347,21 +371,17 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
 #pragma unroll 1
       for (uint32_t t = 0; t < nbt; ++t) {
         const uint32_t kb = kb0 + t;
-        // this lane's B state: step j = lane of superblock kb (the top row's
-        // direction follows the parity of the global superblock index)
-        const bool godd = ((sb0 + kb) & 1ull) != 0;
-        uint32_t zj = z2, uj = u2, zjw = z2w, ujw = u2w;
-        {
-          const uint32_t gj = lane ^ (lane >> 1);
-#pragma unroll
-          for (int r = 0; r < V; ++r) {
-            if ((gj >> r) & 1u) {
-              const bool lv = (r == V - 1) && godd;
-              const RowRec& row = R[r];
-              sub_word_u(zj, uj, row.m[0], lv ? row.s[0] : row.a[0], lv ? row.a[0] : row.s[0]);
-              if (WIDE) sub_word_u(zjw, ujw, row.m[1], lv ? row.s[1] : row.a[1], lv ? row.a[1] : row.s[1]);
-            }
-          }
+        // this lane's B state: H + L[G & 1][lane] (L in row form: add = sub of
+        // the negated row, sign m ^ s)
+        const uint32_t gp = (uint32_t)((sb0 + kb) & 1ull);
+        uint32_t zj = zh, uj = uh, zjw = zhw, ujw = uhw;
+        if constexpr (WIDE) {
+          const uint4 l = L4[32 * gp + lane];
+          sub_word_u(zj, uj, l.x, l.x ^ l.y, l.y);
+          sub_word_u(zjw, ujw, l.z, l.z ^ l.w, l.w);
+        } else {
+          const uint2 l = L2[32 * gp + lane];
+          sub_word_u(zj, uj, l.x, l.x ^ l.y, l.y);
         }
         // compatible: no key column of y equals the forbidden trit
         const uint32_t match = (zj & F0) | (~zj & ~uj & F2) | (~zj & uj & F1);
@@ -375,22 +395,15 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
           Hj[pos] = (uint8_t)(32u * t + lane);
         }
         L += __popc(cmask);
-        // (z2, u2) = step SB-1 of this superblock, then the entry of kb + 1
-        z2 = __shfl_sync(FULL, zj, SB - 1);
-        u2 = __shfl_sync(FULL, uj, SB - 1);
-        if (WIDE) {
-          z2w = __shfl_sync(FULL, zjw, SB - 1);
-          u2w = __shfl_sync(FULL, ujw, SB - 1);
-        }
         if (kb + 1 < nsb) {
-          // entry of global superblock G flips row FIX + V + tz(G); it leaves
+          // H of global superblock G flips row FIX + V + tz(G); it leaves
           // iff bit tz(G) + 1 of G is set
           const unsigned long long G = sb0 + kb + 1;
           const int tzg = tz64(G);
           const RowRec& row = R[V + tzg];
           const bool lv = ((G >> (tzg + 1)) & 1ull) != 0;
-          sub_word_u(z2, u2, row.m[0], lv ? row.s[0] : row.a[0], lv ? row.a[0] : row.s[0]);
-          if (WIDE) sub_word_u(z2w, u2w, row.m[1], lv ? row.s[1] : row.a[1], lv ? row.a[1] : row.s[1]);
+          sub_word_u(zh, uh, row.m[0], lv ? row.s[0] : row.a[0], lv ? row.a[0] : row.s[0]);
+          if (WIDE) sub_word_u(zhw, uhw, row.m[1], lv ? row.s[1] : row.a[1], lv ? row.a[1] : row.s[1]);
         }
       }
       tested_steps += L;
@@ -522,7 +535,10 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
 template <bool WIDE>
 struct BatchShape {
   static constexpr int NBAT = WIDE ? 2 : 4;
-  static constexpr int ECAP = WIDE ? 8 : 10;
+  static constexpr int ECAP = WIDE ? 7 : 10;
+  // four blocks per SM: 228 KB of shared memory, 1 KB reserved per block
+  static_assert(4 * (4 * BatchSmem<NBAT, ECAP, WIDE, WIDE ? 17 : 13>::kWarp + 1024) <= 228 * 1024,
+                "k_walk_batch: four blocks must fit an SM");
 };
 
 template <bool WIDE, int FIX, int KEYS>
