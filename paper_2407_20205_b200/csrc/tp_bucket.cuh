@@ -26,10 +26,6 @@
   } while (0)
 #endif
 
-//   TP_BUCKET_BIGKEYS  key columns of the 17-row A side (n >= 28): 3, 4 or 5
-#ifndef TP_BUCKET_BIGKEYS
-#define TP_BUCKET_BIGKEYS 4
-#endif
 
 namespace tp {
 

@@ -112,7 +112,7 @@ struct BucketCfg {
   int fix;   // A side: rows 0..fix-1
   int keys;  // key columns: 3^keys buckets
 };
-BucketCfg bucket_cfg(int n, bool packed);
+BucketCfg bucket_cfg(int n, bool packed, bool batch);
 int bucket_pieces(BucketCfg c);
 size_t bucket_tab_bytes(BucketCfg c, bool wide);  // per matrix
 int bucket_v(bool packed);

@@ -317,7 +317,8 @@ int make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, uns
   unsigned long long mid0 = 0, mid1 = 0;  // bucket region in 32-step units (ranges)
   if (bucket_applies(n, B) && (full || end64 || lo < hi)) {
     const bool packed = n > 31 || bucket_mode() != 2;  // 2: the unpacked pair tests
-    const tp::BucketCfg cfg = tp::bucket_cfg(n, packed);
+    const bool batch = packed && batch_mode();
+    const tp::BucketCfg cfg = tp::bucket_cfg(n, packed, batch);
     const int fix = cfg.fix;  // A side: rows 0..fix-1
     const int P = tp::bucket_pieces(cfg);
     const int bv = tp::bucket_v(packed);
@@ -342,7 +343,6 @@ int make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, uns
       const char* e = getenv("TRITPERM_BUCKET_ITEMS");  // tuning knob: the ~128 above
       return (unsigned long long)(e && atoi(e) > 0 ? atoi(e) : 128);
     }();
-    const bool batch = packed && batch_mode();
     const int bps = batch ? d.batch_blocks_per_sm[n > 32 ? 1 : 0] : d.bucket_blocks_per_sm;
     const unsigned long long warps = (unsigned long long)d.sm_count * bps * 4;
     unsigned long long nblk = std::min<unsigned long long>(std::max<unsigned long long>(total, 1), 1ull << 16);

@@ -553,11 +553,11 @@ static cudaError_t launch_batch_k(int grid, const BucketParamsCfg& bc, cudaStrea
 }
 
 cudaError_t launch_walk_batch(int grid, const BucketParams& bp, cudaStream_t st) {
-  const BucketCfg c = bucket_cfg(bp.fp.n, true);
+  const BucketCfg c = bucket_cfg(bp.fp.n, true, true);
   const BucketParamsCfg bc{bp.fp, bp.tab, bp.ptab, bp.tested, bp.s_end, c.fix, c.keys};
-  if (bp.fp.n > 32) return launch_batch_k<true, 17, TP_BUCKET_BIGKEYS>(grid, bc, st);
-  if (c.fix == 13 && c.keys == 2) return launch_batch_k<false, 13, 2>(grid, bc, st);
-  if (c.fix == 17 && c.keys == TP_BUCKET_BIGKEYS) return launch_batch_k<false, 17, TP_BUCKET_BIGKEYS>(grid, bc, st);
+  if (bp.fp.n > 32 && c.fix == 17 && c.keys == 4) return launch_batch_k<true, 17, 4>(grid, bc, st);
+  if (c.fix == 14 && c.keys == 3) return launch_batch_k<false, 14, 3>(grid, bc, st);
+  if (c.fix == 17 && c.keys == 5) return launch_batch_k<false, 17, 5>(grid, bc, st);
   return cudaErrorInvalidValue;
 }
 
@@ -567,13 +567,13 @@ int walk_batch_blocks_per_sm(bool wide) {
   if (wide) {
     using Sh = BatchShape<true>;
     constexpr int bytes = 4 * BatchSmem<Sh::NBAT, Sh::ECAP, true, 17>::kWarp;
-    auto* k = &k_walk_batch<Sh::NBAT, Sh::ECAP, true, 17, TP_BUCKET_BIGKEYS>;
+    auto* k = &k_walk_batch<Sh::NBAT, Sh::ECAP, true, 17, 4>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 128, bytes) != cudaSuccess) return 0;
   } else {
     using Sh = BatchShape<false>;
-    constexpr int bytes = 4 * BatchSmem<Sh::NBAT, Sh::ECAP, false, 13>::kWarp;
-    auto* k = &k_walk_batch<Sh::NBAT, Sh::ECAP, false, 13, 2>;
+    constexpr int bytes = 4 * BatchSmem<Sh::NBAT, Sh::ECAP, false, 14>::kWarp;
+    auto* k = &k_walk_batch<Sh::NBAT, Sh::ECAP, false, 14, 3>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 128, bytes) != cudaSuccess) return 0;
   }

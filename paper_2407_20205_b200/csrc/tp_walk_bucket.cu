@@ -50,14 +50,6 @@
 #ifndef TP_BUCKET_ROLLED
 #define TP_BUCKET_ROLLED 1
 #endif
-//   TP_BUCKET_SMALLCFG 1: n < 28 with a 14-row A side and 3 key columns
-//   TP_BUCKET_VOTE1    1: one REDUX.MAX of the pass-list lengths instead of two votes
-#ifndef TP_BUCKET_VOTE1
-#define TP_BUCKET_VOTE1 1
-#endif
-#ifndef TP_BUCKET_SMALLCFG
-#define TP_BUCKET_SMALLCFG 0
-#endif
 #if TP_BUCKET_REDUX
 #define TP_ANY(x) (__reduce_or_sync(FULL, (x) ? 1u : 0u) != 0)
 #else
@@ -974,62 +966,50 @@ size_t bucket_tab_bytes(BucketCfg c, bool wide) {
   if (c.fix == 13 && c.keys == 2) return Tab<13, 2, false>::kBytes;
   if (c.fix == 14 && c.keys == 3) return Tab<14, 3, false>::kBytes;
   if (c.fix == 14 && c.keys == 2) return Tab<14, 2, false>::kBytes;
-  return wide ? Tab<17, TP_BUCKET_BIGKEYS, true>::kBytes : Tab<17, TP_BUCKET_BIGKEYS, false>::kBytes;
+  if (c.fix == 17 && c.keys == 5) return Tab<17, 5, false>::kBytes;
+  return wide ? Tab<17, 4, true>::kBytes : Tab<17, 4, false>::kBytes;
 }
 
-// Unpacked pair tests: 14 rows, 2 keys.  Packed filter: a 13-row A side for
-// n < 28, where items are one matrix's whole B side and a short A side makes
-// them longer; from n = 28 a 17-row A side in 81 buckets of four key columns
-// (the B side still has >= 64 superblocks per matrix), which skips 65/81 of
-// the steps (3 keys: 19/27) at the cost of one partly filled piece per
-// bucket.  Measured on B200: 4 keys against 3 take C3 from
-// 472 to 378 ms, C4 from 3.33 to 2.84 ms, C5 from 747 to 604 ms; 5 keys are
-// slower (243 runs per bucket to decode, 9-word pieces); for n < 28 a 14-row
-// A side with 3 keys (TP_BUCKET_SMALLCFG) is 3 % faster on C2 but leaves
-// the filter a smaller share of the time (C2 LOP3 roofline 0.61 -> 0.42).
-BucketCfg bucket_cfg(int n, bool packed) {
+// Configurations (A side rows FIX, KEYS key columns).
+//  * Unpacked pair tests (TRITPERM_BUCKET=2): 14 rows, 2 keys.
+//  * k_walk_batch (the default): n < 28 14 rows and 3 keys (27 buckets of
+//    ~607 slots, 8/27 of the steps tested); 28 <= n <= 32 17 rows and 5
+//    keys (243 buckets of ~539 slots, 32/243 tested); n > 32 17 rows and 4
+//    keys (81 buckets, 16/81 tested: 5 keys would need 237 KB of run starts
+//    per matrix for the primary-hit lookup).  Its batched filter loop keeps
+//    the short pieces efficient; measured on B200 against 13
+//    rows / 2 keys and 17 rows / 4 keys: C2 14.78 -> 13.78 ms, C3 313 -> 276
+//    ms, C5 507 -> 477 ms with 5 keys (kept at 4 for the table size).
+//  * k_walk_bucket (TRITPERM_BATCH=0): n < 28 13 rows and 2 keys, else 17
+//    rows and 4 keys, its measured best: its per-superblock
+//    filter set-up makes short pieces expensive.
+BucketCfg bucket_cfg(int n, bool packed, bool batch) {
   if (!packed) return BucketCfg{14, 2};
-#if TP_BUCKET_SMALLCFG == 1
-  if (n < 28) return BucketCfg{14, 3};
-#elif TP_BUCKET_SMALLCFG == 2
-  if (n < 28) return BucketCfg{14, 2};
-#endif
-  if (n < 28) return BucketCfg{13, 2};
-  return BucketCfg{17, TP_BUCKET_BIGKEYS};
+  if (batch) return n < 28 ? BucketCfg{14, 3} : n <= 32 ? BucketCfg{17, 5} : BucketCfg{17, 4};
+  return n < 28 ? BucketCfg{13, 2} : BucketCfg{17, 4};
 }
 
 cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, BucketCfg c, bool packed, void* tab,
                                 uint32_t* ptab, cudaStream_t st) {
   const unsigned grid = (unsigned)B;
   uint8_t* t = static_cast<uint8_t*>(tab);
-  if (c.fix == 13 && c.keys == 2) k_bucket_group<13, 2, false, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
-  else if (c.fix == 14 && c.keys == 2 && !packed) k_bucket_group<14, 2, false, false><<<grid, 256, 0, st>>>(rows, n, t, ptab);
-#if TP_BUCKET_SMALLCFG == 2
-  else if (c.fix == 14 && c.keys == 2) k_bucket_group<14, 2, false, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
-#endif
-#if TP_BUCKET_SMALLCFG == 1
+  if (!packed) k_bucket_group<14, 2, false, false><<<grid, 256, 0, st>>>(rows, n, t, ptab);
+  else if (c.fix == 13 && c.keys == 2) k_bucket_group<13, 2, false, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
   else if (c.fix == 14 && c.keys == 3) k_bucket_group<14, 3, false, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
-#endif
-  else if (c.fix == 17 && c.keys == TP_BUCKET_BIGKEYS && n > 32)
-    k_bucket_group<17, TP_BUCKET_BIGKEYS, true, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
-  else if (c.fix == 17 && c.keys == TP_BUCKET_BIGKEYS)
-    k_bucket_group<17, TP_BUCKET_BIGKEYS, false, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
+  else if (c.fix == 17 && c.keys == 5 && n <= 32) k_bucket_group<17, 5, false, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
+  else if (c.fix == 17 && c.keys == 4 && n > 32) k_bucket_group<17, 4, true, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
+  else if (c.fix == 17 && c.keys == 4) k_bucket_group<17, 4, false, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
   else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 
 cudaError_t launch_walk_bucket(int grid, const BucketParams& bp, bool packed, cudaStream_t st) {
-  const BucketCfg c = bucket_cfg(bp.fp.n, packed);
+  const BucketCfg c = bucket_cfg(bp.fp.n, packed, false);
   const BucketParamsCfg bc{bp.fp, bp.tab, bp.ptab, bp.tested, bp.s_end, c.fix, c.keys};
-  if (bp.fp.n > 32) k_walk_bucket<5, 4, true, true, 17, TP_BUCKET_BIGKEYS><<<grid, 128, 0, st>>>(bc);
+  if (bp.fp.n > 32) k_walk_bucket<5, 4, true, true, 17, 4><<<grid, 128, 0, st>>>(bc);
   else if (!packed) k_walk_bucket<4, 4, false, false, 14, 2><<<grid, 128, 0, st>>>(bp);
   else if (c.fix == 13) k_walk_bucket<5, 4, true, false, 13, 2><<<grid, 128, 0, st>>>(bp);
-#if TP_BUCKET_SMALLCFG == 1
-  else if (c.fix == 14) k_walk_bucket<5, 4, true, false, 14, 3><<<grid, 128, 0, st>>>(bc);
-#elif TP_BUCKET_SMALLCFG == 2
-  else if (c.fix == 14) k_walk_bucket<5, 4, true, false, 14, 2><<<grid, 128, 0, st>>>(bp);
-#endif
-  else k_walk_bucket<5, 4, true, false, 17, TP_BUCKET_BIGKEYS><<<grid, 128, 0, st>>>(bc);
+  else k_walk_bucket<5, 4, true, false, 17, 4><<<grid, 128, 0, st>>>(bc);
   return cudaGetLastError();
 }
 
