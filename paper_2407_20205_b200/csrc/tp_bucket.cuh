@@ -244,6 +244,54 @@ static __device__ __noinline__ uint32_t bucket_wide_term(const uint8_t* Tm, uint
   return 1u | ((__popc((d ^ pair_g2(h1.x, h1.y)) & z1i) & 1u) << 1);
 }
 
+// Cooperative decode table of bucket g's runs (k_walk_batch): one uint4 per
+// run a = (start, o0 | c0 << 16, o1, 1/c0 as float) plus a sentinel whose
+// start is the bucket size, built by the 32 lanes in parallel (the runs'
+// sizes |low_a| |high_(g-a)| prefix-summed with a warp scan).  A lane then
+// finds the run of each of its (increasing) positions with a linear walk
+// over the starts and splits rel = p - start into rel / c0, rel % c0 with a
+// float reciprocal: rel < 2^17 and c0 < 2^10, so (rel + 1/2) / c0 lies at
+// least 1/(2 c0) from an integer and the product's 2^-23 relative error
+// (< 2^-6 / c0 absolute) cannot move the truncation.  Replaces the per-lane
+// RunCursor (a base-3 digit subtraction and a runtime division per slot).
+template <int KEYS>
+__device__ __forceinline__ void run_table(const uint16_t* off, uint32_t grp, uint4* RT, uint32_t lane) {
+  constexpr uint32_t NB = nbuckets(KEYS);
+  uint32_t carry = 0;
+#pragma unroll 1
+  for (uint32_t a0 = 0; a0 < NB; a0 += 32) {
+    const uint32_t a = a0 + lane;
+    uint32_t sz = 0, o0 = 0, c0 = 0, o1 = 0;
+    if (a < NB) {
+      const uint32_t ga = pat_sub<KEYS>(grp, a);
+      o0 = off[a];
+      c0 = off[a + 1] - o0;
+      o1 = off[NB + 1 + ga];
+      sz = c0 * (uint32_t)(off[NB + 2 + ga] - o1);
+    }
+    uint32_t incl = sz;
+#pragma unroll
+    for (uint32_t d = 1; d < 32; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(FULL, incl, d);
+      if (lane >= d) incl += t;
+    }
+    if (a < NB) RT[a] = make_uint4(carry + incl - sz, o0 | (c0 << 16), o1, __float_as_uint(c0 ? __frcp_rn((float)c0) : 0.f));
+    carry += __shfl_sync(FULL, incl, 31);
+  }
+  if (lane == 0) RT[NB] = make_uint4(carry, 0, 0, 0);
+  __syncwarp();
+}
+
+// Table indices (low i0, high i1) of bucket position p in run record rec.
+__device__ __forceinline__ void run_index(uint4 rec, uint32_t p, uint32_t& i0, uint32_t& i1) {
+  const uint32_t rel = p - rec.x, c0 = rec.y >> 16;
+  const float rc = __uint_as_float(rec.w);
+  const uint32_t j = __float2uint_rz(__fmaf_rn((float)rel, rc, 0.5f * rc));
+  TP_CHECK(c0 > 0 && j * c0 <= rel && rel - j * c0 < c0);
+  i0 = (rec.y & 0xFFFFu) + rel - j * c0;
+  i1 = rec.z + j;
+}
+
 // Exact fold of one pair with the A subset's parity bit sp: n += full,
 // a += full & (parity(popc(sign word)) ^ sp).
 __device__ __forceinline__ void exact_fold_par(uint32_t z1, uint32_t g1, uint32_t z2, uint32_t u2, uint32_t g2,

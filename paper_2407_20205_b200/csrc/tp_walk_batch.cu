@@ -52,6 +52,9 @@ struct BatchSmem {
   // of even / odd index: uint2 (m, s) [2][32], n > 32 uint4 (m0, s0, m1, s1)
   static constexpr int oL = oE + 8 * 32 * ECAP;
   static constexpr int kWarp = align16(oL + 2 * 32 * (WIDE ? 16 : 8));
+  // the A decode's run table (run_table) borrows [oHc, oL)
+  template <int KEYS>
+  __host__ __device__ static constexpr bool run_table_fits() { return 16 * (nbuckets(KEYS) + 1) <= oL - oHc; }
 };
 
 // Exact evaluation of list entries [0, L) against this lane's 32 slots, n <= 32
@@ -218,6 +221,7 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
   constexpr int kBucketPieces = pieces_of(FIX, KEYS);
   using T = Tab<FIX, KEYS, WIDE>;
   using S = BatchSmem<NBAT, ECAP, WIDE, FIX>;
+  static_assert(S::template run_table_fits<KEYS>(), "k_walk_batch: the run table must fit the list area");
   const FastParams& p = bp.fp;
   extern __shared__ __align__(16) uint8_t batch_smem[];
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -278,8 +282,10 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
     const uint8_t* Tm = static_cast<const uint8_t*>(bp.tab) + b * T::kBytes;
     {
       const uint32_t* wts = reinterpret_cast<const uint32_t*>(Tm + T::kWt);
-      RunCursor<KEYS> cur;
-      cur.init(reinterpret_cast<const uint16_t*>(Tm), grp);
+      // the bucket's run table in the (still unused) list / pass-list area
+      uint4* RT = reinterpret_cast<uint4*>(ws + S::oHc);
+      run_table<KEYS>(reinterpret_cast<const uint16_t*>(Tm), grp, RT, lane);
+      uint32_t ra = 0;  // this lane's current run
 #pragma unroll 1
       for (uint32_t r = 0; r < (uint32_t)K; ++r) {
         const int k = (int)((r >> 1) + ((r & 1u) << 4));
@@ -289,9 +295,11 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
           z = colmask;
           g = p.n <= 31 ? 0x80000000u : 0u;
         } else {
+          const uint32_t pp = pbase + rr;
+          while (RT[ra + 1].x <= pp) ++ra;
+          TP_CHECK(ra < (uint32_t)nbuckets(KEYS));
           uint32_t i0, i1;
-          cur.seek(pbase + rr);
-          cur.index(pbase + rr, i0, i1);
+          run_index(RT[ra], pp, i0, i1);
           const uint2 lo = *reinterpret_cast<const uint2*>(Tm + T::kVec + T::VE * i0);
           const uint2 hi = *reinterpret_cast<const uint2*>(Tm + T::kVec + T::VE * (T::N0 + i1));
           const uint32_t par = ((wts[i0] ^ wts[T::N0 + i1]) >> 16) & 1u;
