@@ -47,14 +47,19 @@ struct BatchSmem {
   static constexpr int oHf = oHc + 8 * NS;              // uint2[NS]: full state (z, u)
   static constexpr int oH1 = oHf + 8 * NS;              // uint2[NS]: n > 32, secondary word (z, u)
   static constexpr int oHj = oH1 + (WIDE ? 8 * NS : 0);  // uint8[NS]: step within the batch
-  static constexpr int oE = align16(oHj + NS);          // uint2[ECAP][32]: passes (mask, list index)
+  static constexpr int oE = align16(oHj + NS);          // uint2[ECAP + 1][32]: passes (mask, list index)
   // per lane the low-row part of its B state in row form, for superblocks
   // of even / odd index: uint2 (m, s) [2][32], n > 32 uint4 (m0, s0, m1, s1)
-  static constexpr int oL = oE + 8 * 32 * ECAP;
+  static constexpr int oL = oE + 8 * 32 * (ECAP + 1);
   static constexpr int kWarp = align16(oL + 2 * 32 * (WIDE ? 16 : 8));
   // the A decode's run table (run_table) borrows [oHc, oL)
   template <int KEYS>
   __host__ __device__ static constexpr bool run_table_fits() { return 16 * (nbuckets(KEYS) + 1) <= oL - oHc; }
+  // ... and behind it a copy of the matrix's half table, when that fits too
+  template <int KEYS, int TBYTES>
+  __host__ __device__ static constexpr bool tab_fits() {
+    return align16(16 * (nbuckets(KEYS) + 1)) + TBYTES <= oL - oHc;
+  }
 };
 
 // Exact evaluation of list entries [0, L) against this lane's 32 slots, n <= 32
@@ -281,10 +286,22 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
     uint32_t vmask = 0;  // bit k: slot k holds a real A subset
     const uint8_t* Tm = static_cast<const uint8_t*>(bp.tab) + b * T::kBytes;
     {
-      const uint32_t* wts = reinterpret_cast<const uint32_t*>(Tm + T::kWt);
-      // the bucket's run table in the (still unused) list / pass-list area
+      // the bucket's run table in the (still unused) list / pass-list area,
+      // and (short items, n < 28) a copy of the half table behind it: one
+      // coalesced read instead of a dependent L2 round trip per slot
       uint4* RT = reinterpret_cast<uint4*>(ws + S::oHc);
-      run_table<KEYS>(reinterpret_cast<const uint16_t*>(Tm), grp, RT, lane);
+      const uint8_t* Td = Tm;
+      if constexpr (S::template tab_fits<KEYS, T::kBytes>()) {
+        uint4* dst = reinterpret_cast<uint4*>(ws + S::oHc + align16(16 * (nbuckets(KEYS) + 1)));
+        const uint4* src = reinterpret_cast<const uint4*>(Tm);
+#pragma unroll
+        for (int x = 0; x < T::kBytes / 16; x += 32)
+          if (x + (int)lane < T::kBytes / 16) dst[x + lane] = src[x + lane];
+        __syncwarp();
+        Td = reinterpret_cast<const uint8_t*>(dst);
+      }
+      const uint32_t* wts = reinterpret_cast<const uint32_t*>(Td + T::kWt);
+      run_table<KEYS>(reinterpret_cast<const uint16_t*>(Td), grp, RT, lane);
       uint32_t ra = 0;  // this lane's current run
 #pragma unroll 1
       for (uint32_t r = 0; r < (uint32_t)K; ++r) {
@@ -300,8 +317,8 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
           TP_CHECK(ra < (uint32_t)nbuckets(KEYS));
           uint32_t i0, i1;
           run_index(RT[ra], pp, i0, i1);
-          const uint2 lo = *reinterpret_cast<const uint2*>(Tm + T::kVec + T::VE * i0);
-          const uint2 hi = *reinterpret_cast<const uint2*>(Tm + T::kVec + T::VE * (T::N0 + i1));
+          const uint2 lo = *reinterpret_cast<const uint2*>(Td + T::kVec + T::VE * i0);
+          const uint2 hi = *reinterpret_cast<const uint2*>(Td + T::kVec + T::VE * (T::N0 + i1));
           const uint32_t par = ((wts[i0] ^ wts[T::N0 + i1]) >> 16) & 1u;
           z = lo.x;
           g = lo.y;
@@ -438,24 +455,49 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
         continue;
       }
       // the packed filter over the list, two entries per iteration: bit w
-      // (entry i) / 16 + w (entry i + 1) of M = a pass of word w
+      // (entry i) / 16 + w (entry i + 1) of M = a pass of word w; pieces of
+      // at most 10 words three entries per iteration: bit W e + w (entry
+      // i + e), the record's list index tagged with W << 16
       uint32_t ne = 0;
+      auto record = [&](uint32_t M, uint32_t tag) {
+        // unconditional store (slot ECAP takes the overflow), no branch
+        E[min(ne, (uint32_t)ECAP)][lane] = make_uint2(M, tag);
+        ne += M != 0u ? 1u : 0u;
+      };
       auto filter = [&](auto Wc) {
         constexpr int W = decltype(Wc)::value;
         uint32_t i = 0;
+        if constexpr (W <= 10) {
+#pragma unroll 1
+          for (; i + 3 <= L; i += 3) {
+            const uint2 ha = Hc[i], hb = Hc[i + 1], hc = Hc[i + 2];
+            uint32_t M = 0;
+            static_for<W>([&](auto wc) {
+              constexpr int w = decltype(wc)::value;
+              packed_test<(1u << w)>(Zp[w], Gp[w], ha.x, ha.y, M, one, cneg);
+              packed_test<(1u << (W + w))>(Zp[w], Gp[w], hb.x, hb.y, M, one, cneg);
+              packed_test<(1u << (2 * W + w))>(Zp[w], Gp[w], hc.x, hc.y, M, one, cneg);
+            });
+            record(M, i | ((uint32_t)W << 16));
+          }
+        }
 #pragma unroll 1
         for (; i + 2 <= L; i += 2) {
-          const uint4 hab = *reinterpret_cast<const uint4*>(Hc + i);
+          // (after the three-entry loop i may be odd: two 8-byte loads)
+          uint4 hab;
+          if constexpr (W <= 10) {
+            const uint2 ha = Hc[i], hb = Hc[i + 1];
+            hab = make_uint4(ha.x, ha.y, hb.x, hb.y);
+          } else {
+            hab = *reinterpret_cast<const uint4*>(Hc + i);
+          }
           uint32_t M = 0;
           static_for<W>([&](auto wc) {
             constexpr int w = decltype(wc)::value;
             packed_test<(1u << w)>(Zp[w], Gp[w], hab.x, hab.y, M, one, cneg);
             packed_test<(1u << (16 + w))>(Zp[w], Gp[w], hab.z, hab.w, M, one, cneg);
           });
-          if (M) {
-            if (ne < (uint32_t)ECAP) E[ne][lane] = make_uint2(M, i);
-            ++ne;
-          }
+          record(M, i);
         }
         if (i < L) {  // an odd last entry alone
           const uint2 ha = Hc[i];
@@ -464,10 +506,7 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
             constexpr int w = decltype(wc)::value;
             packed_test<(1u << w)>(Zp[w], Gp[w], ha.x, ha.y, M, one, cneg);
           });
-          if (M) {
-            if (ne < (uint32_t)ECAP) E[ne][lane] = make_uint2(M, i);
-            ++ne;
-          }
+          record(M, i);
         }
       };
       using FW = FilterWidths<FIX, KEYS>;
@@ -495,7 +534,11 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
           while (M) {
             const uint32_t bit = __ffs(M) - 1;
             M &= M - 1;
-            const uint32_t j = ent.y + (bit >> 4), w = bit & 15u;
+            // entry and word of the pass: tag W: three entries of W words,
+            // else two of 16
+            const uint32_t tw = ent.y >> 16;
+            const uint32_t eo = tw ? (bit >= 2u * tw ? 2u : bit >= tw ? 1u : 0u) : bit >> 4;
+            const uint32_t j = (ent.y & 0xFFFFu) + eo, w = tw ? bit - eo * tw : bit & 15u;
             TP_CHECK(j < L);
             const uint2 h = Hf[j];
             const uint32_t gh = pair_g2(h.x, h.y);
@@ -543,7 +586,7 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
 template <bool WIDE>
 struct BatchShape {
   static constexpr int NBAT = WIDE ? 2 : 4;
-  static constexpr int ECAP = WIDE ? 7 : 10;
+  static constexpr int ECAP = WIDE ? 6 : 10;
   // four blocks per SM: 228 KB of shared memory, 1 KB reserved per block
   static_assert(4 * (4 * BatchSmem<NBAT, ECAP, WIDE, WIDE ? 17 : 13>::kWarp + 1024) <= 228 * 1024,
                 "k_walk_batch: four blocks must fit an SM");
