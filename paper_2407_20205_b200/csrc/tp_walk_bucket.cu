@@ -216,18 +216,42 @@ __global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n,
     else reinterpret_cast<uint2*>(Tm + T::kVec)[idx] = make_uint2(vec[q].x, vec[q].y);
   }
   __syncthreads();
-  if (tid == 0) {
-    const uint32_t weighted = (dep[0] || dep[1]) ? 1u << 31 : 0u;
-    uint32_t* Pt = ptab + (size_t)blockIdx.x * P;
-    uint32_t piece = 0;
+  // Piece order (longest first, so the dynamic queue ends on the shortest
+  // items): every full piece of 1024 slots, bucket by bucket, then the
+  // partial pieces by decreasing slot count (ties by bucket).  Thread g
+  // places bucket g's pieces.
+  const uint32_t weighted = (dep[0] || dep[1]) ? 1u << 31 : 0u;
+  uint32_t* Pt = ptab + (size_t)blockIdx.x * P;
+  __shared__ uint32_t nfull;
+  if (tid == 0) {  // full pieces before bucket g, in offs[0][g] (free now)
+    uint32_t f = 0;
     for (uint32_t g = 0; g < (uint32_t)NB; ++g) {
-      const uint32_t c = bsize[g];
-      for (uint32_t q = 0; 1024u * q < c; ++q) {
-        TP_CHECK(piece < (uint32_t)P);
-        Pt[piece++] = g | (min(1024u, c - 1024u * q) << 8) | (q << 20) | weighted;
-      }
+      offs[0][g] = f;
+      f += bsize[g] >> 10;
     }
-    for (; piece < (uint32_t)P; ++piece) Pt[piece] = 0;  // unused pieces: count 0
+    nfull = f;
+  }
+  __syncthreads();
+  for (uint32_t g = tid; g < (uint32_t)NB; g += NT) {
+    const uint32_t c = bsize[g], nf = c >> 10, part = c & 1023u;
+    for (uint32_t q = 0; q < nf; ++q) {
+      TP_CHECK(offs[0][g] + q < (uint32_t)P);
+      Pt[offs[0][g] + q] = g | (1024u << 8) | (q << 20) | weighted;
+    }
+    if (part) {
+      uint32_t rank = 0;
+      for (uint32_t h = 0; h < (uint32_t)NB; ++h) {
+        const uint32_t ph = bsize[h] & 1023u;
+        rank += (ph > part || (ph == part && h < g)) ? 1u : 0u;
+      }
+      TP_CHECK(nfull + rank < (uint32_t)P);
+      Pt[nfull + rank] = g | (part << 8) | (nf << 20) | weighted;
+    }
+  }
+  if (tid == 0) {  // unused pieces: count 0
+    uint32_t used = nfull;
+    for (uint32_t g = 0; g < (uint32_t)NB; ++g) used += (bsize[g] & 1023u) ? 1u : 0u;
+    for (uint32_t piece = used; piece < (uint32_t)P; ++piece) Pt[piece] = 0;
   }
 }
 
