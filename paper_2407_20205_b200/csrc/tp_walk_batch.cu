@@ -157,24 +157,21 @@ static __device__ __noinline__ unsigned long long batch_exact_wide(const uint4 (
 // Weighted matrices (deduplicated A side): exact evaluation of list entries
 // [0, L) against this lane's real slots, each slot standing for `we` subsets
 // of even and `wo` of odd size with the same vector (k_walk_bucket's
-// bucket_exact_weighted over the list).  Flushed into pm right away: per
+// bucket_exact_weighted over the list; the slots' table indices IX[r][lane]
+// come from the item's A decode).  Flushed into pm right away: per
 // lane <= 2^17 subsets x NS steps, per warp < 2^(22 + log2 NS) < 2^32.
 template <int FIX, int KEYS, bool WIDE>
 static __device__ __noinline__ void batch_exact_weighted(const uint2* Hf, const uint2* H1, const uint8_t* Hj,
-                                                         uint32_t L, const uint8_t* Tm, uint32_t grp,
-                                                         uint32_t pbase, uint32_t cnt, uint32_t lane,
-                                                         uint32_t colmask, uint32_t z1i, unsigned long long* pm) {
+                                                         uint32_t L, const uint8_t* Tm, const uint32_t* IX,
+                                                         uint32_t cnt, uint32_t lane, uint32_t colmask, uint32_t z1i,
+                                                         unsigned long long* pm) {
   using T = Tab<FIX, KEYS, WIDE>;
   const uint32_t* wts = reinterpret_cast<const uint32_t*>(Tm + T::kWt);
-  RunCursor<KEYS> cur;
-  cur.init(reinterpret_cast<const uint16_t*>(Tm), grp);
   uint32_t ev = 0, odd = 0;
 #pragma unroll 1
   for (uint32_t r = 0; 32u * r + lane < cnt; ++r) {
-    const uint32_t p = pbase + 32u * r + lane;
-    uint32_t i0, i1;
-    cur.seek(p);
-    cur.index(p, i0, i1);
+    // the slot's half-table indices, decoded once per item (IX)
+    const uint32_t i0 = IX[32u * r + lane] & 0xFFFFu, i1 = IX[32u * r + lane] >> 16;
     const uint32_t w0 = wts[i0], w1 = wts[T::N0 + i1];
     const uint32_t e0 = w0 & 0xFFFFu, o0 = w0 >> 16, e1 = w1 & 0xFFFFu, o1 = w1 >> 16;
     const uint32_t we = e0 * e1 + o0 * o1, wo = e0 * o1 + o0 * e1;
@@ -233,6 +230,7 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
   uint8_t* ws = batch_smem + warp * S::kWarp;
   RowRec* R = reinterpret_cast<RowRec*>(ws + S::oR);  // row r at R[r - FIX]
   uint4 (*A2)[32] = reinterpret_cast<uint4 (*)[32]>(ws + S::oA);
+  uint32_t* IX = reinterpret_cast<uint32_t*>(ws + S::oA);  // weighted items: slot r's table indices [r][lane]
   uint2* Hc = reinterpret_cast<uint2*>(ws + S::oHc);
   uint2* Hf = reinterpret_cast<uint2*>(ws + S::oHf);
   uint2* H1 = reinterpret_cast<uint2*>(ws + S::oH1);
@@ -303,6 +301,19 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
       const uint32_t* wts = reinterpret_cast<const uint32_t*>(Td + T::kWt);
       run_table<KEYS>(reinterpret_cast<const uint16_t*>(Td), grp, RT, lane);
       uint32_t ra = 0;  // this lane's current run
+      if (weighted) {
+        // the weighted walk rebuilds its slots from their table indices:
+        // IX[r][lane] (in the A2 area, which weighted items do not use)
+#pragma unroll 1
+        for (uint32_t r = 0; 32u * r + lane < cnt; ++r) {
+          const uint32_t pp = pbase + 32u * r + lane;
+          while (RT[ra + 1].x <= pp) ++ra;
+          TP_CHECK(ra < (uint32_t)nbuckets(KEYS));
+          uint32_t i0, i1;
+          run_index(RT[ra], pp, i0, i1);
+          IX[32u * r + lane] = i0 | (i1 << 16);
+        }
+      } else
 #pragma unroll 1
       for (uint32_t r = 0; r < (uint32_t)K; ++r) {
         const int k = (int)((r >> 1) + ((r & 1u) << 4));
@@ -435,7 +446,7 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
       __syncwarp();
       if (L == 0) continue;
       if (weighted) {  // deduplicated A side: every listed step exactly, with weights
-        batch_exact_weighted<FIX, KEYS, WIDE>(Hf, H1, Hj, L, Tm, grp, pbase, cnt, lane, colmask, colmask1,
+        batch_exact_weighted<FIX, KEYS, WIDE>(Hf, H1, Hj, L, Tm, IX, cnt, lane, colmask, colmask1,
                                               p.pm + 2 * b);
         continue;
       }
