@@ -404,12 +404,10 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
       const uint32_t nbt = min((uint32_t)NBAT, nsb - kb0);
       uint32_t L = 0;  // list length
       __syncwarp();    // the previous batch's list is consumed
-#pragma unroll 1
-      for (uint32_t t = 0; t < nbt; ++t) {
-        const uint32_t kb = kb0 + t;
-        // this lane's B state: H + L[G & 1][lane] (L in row form: add = sub of
-        // the negated row, sign m ^ s)
-        const uint32_t gp = (uint32_t)((sb0 + kb) & 1ull);
+      // superblock kb0 + t of the batch: this lane's B state H + L[G & 1][lane]
+      // (L in row form: add = sub of the negated row, sign m ^ s), its
+      // compatibility, and the compacted list entry
+      auto superblock = [&](uint32_t t, uint32_t gp) {
         uint32_t zj = zh, uj = uh, zjw = zhw, ujw = uhw;
         if constexpr (WIDE) {
           const uint4 l = L4[32 * gp + lane];
@@ -431,15 +429,45 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
           Hj[pos] = (uint8_t)(32u * t + lane);
         }
         L += __popc(cmask);
-        if (kb + 1 < nsb) {
-          // H of global superblock G flips row FIX + V + tz(G); it leaves
-          // iff bit tz(G) + 1 of G is set
-          const unsigned long long G = sb0 + kb + 1;
+      };
+      // H of global superblock G flips row FIX + V + tz(G); it leaves iff
+      // bit tz(G) + 1 of G is set
+      auto h_flip = [&](const RowRec& row, bool lv) {
+        sub_word_u(zh, uh, row.m[0], lv ? row.s[0] : row.a[0], lv ? row.a[0] : row.s[0]);
+        if (WIDE) sub_word_u(zhw, uhw, row.m[1], lv ? row.s[1] : row.a[1], lv ? row.a[1] : row.s[1]);
+      };
+      const unsigned long long G0 = sb0 + kb0;
+      if (nbt == (uint32_t)NBAT && (G0 & (unsigned long long)(NBAT - 1)) == 0) {
+        // an aligned full batch: G = G0 + t has parity t & 1 and, inside the
+        // batch, flips row FIX + V + tz(t) (compile-time); only the next
+        // batch's entry needs the runtime tz of G0 + NBAT
+        constexpr int LNB = NBAT == 2 ? 1 : NBAT == 4 ? 2 : 3;
+        static_assert(NBAT == (1 << LNB), "NBAT: a power of two <= 8");
+        static_for<NBAT>([&](auto tc) {
+          constexpr uint32_t t = decltype(tc)::value;
+          superblock(t, t & 1u);
+          if constexpr (t + 1 < (uint32_t)NBAT) {
+            constexpr int tzt = __builtin_ctz(t + 1);
+            // bit tz + 1 of G0 + t + 1: inside the batch offset unless it is bit LNB (of G0)
+            const bool lv = tzt + 1 < LNB ? (((t + 1) >> (tzt + 1)) & 1u) != 0 : ((G0 >> LNB) & 1ull) != 0;
+            h_flip(R[V + tzt], lv);
+          }
+        });
+        if (kb0 + NBAT < nsb) {
+          const unsigned long long G = G0 + NBAT;
           const int tzg = tz64(G);
-          const RowRec& row = R[V + tzg];
-          const bool lv = ((G >> (tzg + 1)) & 1ull) != 0;
-          sub_word_u(zh, uh, row.m[0], lv ? row.s[0] : row.a[0], lv ? row.a[0] : row.s[0]);
-          if (WIDE) sub_word_u(zhw, uhw, row.m[1], lv ? row.s[1] : row.a[1], lv ? row.a[1] : row.s[1]);
+          h_flip(R[V + tzg], ((G >> (tzg + 1)) & 1ull) != 0);
+        }
+      } else {
+#pragma unroll 1
+        for (uint32_t t = 0; t < nbt; ++t) {
+          const uint32_t kb = kb0 + t;
+          superblock(t, (uint32_t)((sb0 + kb) & 1ull));
+          if (kb + 1 < nsb) {
+            const unsigned long long G = sb0 + kb + 1;
+            const int tzg = tz64(G);
+            h_flip(R[V + tzg], ((G >> (tzg + 1)) & 1ull) != 0);
+          }
         }
       }
       tested_steps += L;
