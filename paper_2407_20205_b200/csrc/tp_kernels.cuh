@@ -112,7 +112,7 @@ struct BucketCfg {
   int fix;   // A side: rows 0..fix-1
   int keys;  // key columns: 3^keys buckets
 };
-BucketCfg bucket_cfg(int n, bool packed, bool batch);
+BucketCfg bucket_cfg(int n, bool packed, bool batch, unsigned long long B = 1);
 int bucket_pieces(BucketCfg c);
 size_t bucket_tab_bytes(BucketCfg c, bool wide);  // per matrix
 int bucket_v(bool packed);
@@ -120,7 +120,7 @@ cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, BucketCf
                                 uint32_t* ptab, cudaStream_t st);
 cudaError_t launch_walk_bucket(int grid, const BucketParams& bp, bool packed, cudaStream_t st);
 const void* walk_bucket_symbol(bool packed);
-cudaError_t launch_walk_batch(int grid, const BucketParams& bp, cudaStream_t st);  // tp_walk_batch.cu
+cudaError_t launch_walk_batch(int grid, const BucketParams& bp, BucketCfg c, cudaStream_t st);  // tp_walk_batch.cu
 int walk_batch_blocks_per_sm(bool wide);
 
 const void* walk_fast_symbol(int variant);

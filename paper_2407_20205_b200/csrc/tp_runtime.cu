@@ -318,7 +318,7 @@ int make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, uns
   if (bucket_applies(n, B) && (full || end64 || lo < hi)) {
     const bool packed = n > 31 || bucket_mode() != 2;  // 2: the unpacked pair tests
     const bool batch = packed && batch_mode();
-    const tp::BucketCfg cfg = tp::bucket_cfg(n, packed, batch);
+    const tp::BucketCfg cfg = tp::bucket_cfg(n, packed, batch, B);
     const int fix = cfg.fix;  // A side: rows 0..fix-1
     const int P = tp::bucket_pieces(cfg);
     const int bv = tp::bucket_v(packed);
@@ -542,7 +542,7 @@ int run_plan(const Plan& pl, cudaStream_t st, int* launches) {
   if (pl.bucket) {  // (ranges: plus the generic head and tail below)
     TP_CUDA(tp::launch_bucket_group(pl.bkp.fp.rows, pl.bucket_B, pl.bkp.fp.n, pl.bucket_cfg, pl.bucket_packed,
                                     pl.bucket_tab, pl.bucket_ptab, st));
-    if (pl.bucket_batch) TP_CUDA(tp::launch_walk_batch(pl.bucket_grid, pl.bkp, st));
+    if (pl.bucket_batch) TP_CUDA(tp::launch_walk_batch(pl.bucket_grid, pl.bkp, pl.bucket_cfg, st));
     else TP_CUDA(tp::launch_walk_bucket(pl.bucket_grid, pl.bkp, pl.bucket_packed, st));
     nl += 2;
   }

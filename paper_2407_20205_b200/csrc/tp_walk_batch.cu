@@ -52,13 +52,14 @@ struct BatchSmem {
   // of even / odd index: uint2 (m, s) [2][32], n > 32 uint4 (m0, s0, m1, s1)
   static constexpr int oL = oE + 8 * 32 * (ECAP + 1);
   static constexpr int kWarp = align16(oL + 2 * 32 * (WIDE ? 16 : 8));
-  // the A decode's run table (run_table) borrows [oHc, oL)
+  // the A decode's run table (run_table) borrows [oHc, kWarp): the lists,
+  // the pass list and the L tables are all written after the decode
   template <int KEYS>
-  __host__ __device__ static constexpr bool run_table_fits() { return 16 * (nbuckets(KEYS) + 1) <= oL - oHc; }
+  __host__ __device__ static constexpr bool run_table_fits() { return 16 * (nbuckets(KEYS) + 1) <= kWarp - oHc; }
   // ... and behind it a copy of the matrix's half table, when that fits too
   template <int KEYS, int TBYTES>
   __host__ __device__ static constexpr bool tab_fits() {
-    return align16(16 * (nbuckets(KEYS) + 1)) + TBYTES <= oL - oHc;
+    return align16(16 * (nbuckets(KEYS) + 1)) + TBYTES <= kWarp - oHc;
   }
 };
 
@@ -642,32 +643,31 @@ static cudaError_t launch_batch_k(int grid, const BucketParamsCfg& bc, cudaStrea
   return cudaGetLastError();
 }
 
-cudaError_t launch_walk_batch(int grid, const BucketParams& bp, cudaStream_t st) {
-  const BucketCfg c = bucket_cfg(bp.fp.n, true, true);
+cudaError_t launch_walk_batch(int grid, const BucketParams& bp, BucketCfg c, cudaStream_t st) {
   const BucketParamsCfg bc{bp.fp, bp.tab, bp.ptab, bp.tested, bp.s_end, c.fix, c.keys};
   if (bp.fp.n > 32 && c.fix == 17 && c.keys == 4) return launch_batch_k<true, 17, 4>(grid, bc, st);
+  if (bp.fp.n > 32 && c.fix == 17 && c.keys == 5) return launch_batch_k<true, 17, 5>(grid, bc, st);
   if (c.fix == 14 && c.keys == 3) return launch_batch_k<false, 14, 3>(grid, bc, st);
   if (c.fix == 17 && c.keys == 5) return launch_batch_k<false, 17, 5>(grid, bc, st);
   return cudaErrorInvalidValue;
 }
 
 // blocks of the batched walk resident per SM (the plan sizes its grid with it)
-int walk_batch_blocks_per_sm(bool wide) {
+template <bool WIDE, int FIX, int KEYS>
+static int batch_occupancy() {
+  using Sh = BatchShape<WIDE>;
+  constexpr int bytes = 4 * BatchSmem<Sh::NBAT, Sh::ECAP, WIDE, FIX>::kWarp;
+  auto* k = &k_walk_batch<Sh::NBAT, Sh::ECAP, WIDE, FIX, KEYS>;
   int nb = 0;
-  if (wide) {
-    using Sh = BatchShape<true>;
-    constexpr int bytes = 4 * BatchSmem<Sh::NBAT, Sh::ECAP, true, 17>::kWarp;
-    auto* k = &k_walk_batch<Sh::NBAT, Sh::ECAP, true, 17, 4>;
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 128, bytes) != cudaSuccess) return 0;
-  } else {
-    using Sh = BatchShape<false>;
-    constexpr int bytes = 4 * BatchSmem<Sh::NBAT, Sh::ECAP, false, 14>::kWarp;
-    auto* k = &k_walk_batch<Sh::NBAT, Sh::ECAP, false, 14, 3>;
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 128, bytes) != cudaSuccess) return 0;
-  }
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 128, bytes) != cudaSuccess) return 0;
   return nb;
+}
+
+// the least over the kernels of that width
+int walk_batch_blocks_per_sm(bool wide) {
+  if (wide) return std::min(batch_occupancy<true, 17, 4>(), batch_occupancy<true, 17, 5>());
+  return std::min(batch_occupancy<false, 14, 3>(), batch_occupancy<false, 17, 5>());
 }
 
 }  // namespace tp

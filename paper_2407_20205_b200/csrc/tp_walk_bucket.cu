@@ -990,7 +990,7 @@ size_t bucket_tab_bytes(BucketCfg c, bool wide) {
   if (c.fix == 13 && c.keys == 2) return Tab<13, 2, false>::kBytes;
   if (c.fix == 14 && c.keys == 3) return Tab<14, 3, false>::kBytes;
   if (c.fix == 14 && c.keys == 2) return Tab<14, 2, false>::kBytes;
-  if (c.fix == 17 && c.keys == 5) return Tab<17, 5, false>::kBytes;
+  if (c.fix == 17 && c.keys == 5) return wide ? Tab<17, 5, true>::kBytes : Tab<17, 5, false>::kBytes;
   return wide ? Tab<17, 4, true>::kBytes : Tab<17, 4, false>::kBytes;
 }
 
@@ -1007,9 +1007,11 @@ size_t bucket_tab_bytes(BucketCfg c, bool wide) {
 //  * k_walk_bucket (TRITPERM_BATCH=0): n < 28 13 rows and 2 keys, else 17
 //    rows and 4 keys, its measured best: its per-superblock
 //    filter set-up makes short pieces expensive.
-BucketCfg bucket_cfg(int n, bool packed, bool batch) {
+BucketCfg bucket_cfg(int n, bool packed, bool batch, unsigned long long B) {
   if (!packed) return BucketCfg{14, 2};
-  if (batch) return n < 28 ? BucketCfg{14, 3} : n <= 32 ? BucketCfg{17, 5} : BucketCfg{17, 4};
+  // n > 32: 5 keys while the run-start tables (237 KB per matrix) stay
+  // under ~1 GB, i.e. single matrices and small batches (C4, C5, ranges)
+  if (batch) return n < 28 ? BucketCfg{14, 3} : n <= 32 || B <= 4096 ? BucketCfg{17, 5} : BucketCfg{17, 4};
   return n < 28 ? BucketCfg{13, 2} : BucketCfg{17, 4};
 }
 
@@ -1021,6 +1023,7 @@ cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, BucketCf
   else if (c.fix == 13 && c.keys == 2) k_bucket_group<13, 2, false, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
   else if (c.fix == 14 && c.keys == 3) k_bucket_group<14, 3, false, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
   else if (c.fix == 17 && c.keys == 5 && n <= 32) k_bucket_group<17, 5, false, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
+  else if (c.fix == 17 && c.keys == 5) k_bucket_group<17, 5, true, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
   else if (c.fix == 17 && c.keys == 4 && n > 32) k_bucket_group<17, 4, true, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
   else if (c.fix == 17 && c.keys == 4) k_bucket_group<17, 4, false, true><<<grid, 256, 0, st>>>(rows, n, t, ptab);
   else return cudaErrorInvalidValue;

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -x -q --timeout 900 -p no:cacheprovider > gpurun_out/r3g_pytest.log 2>&1; echo pytest=$?
+tail -3 gpurun_out/r3g_pytest.log
+bash tools/gpu_ab.sh r3g -
