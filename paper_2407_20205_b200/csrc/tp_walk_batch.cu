@@ -44,14 +44,20 @@ struct BatchSmem {
   static constexpr int oR = 0;                          // RowRec[NR]: row r at r - FIX
   static constexpr int oA = align16(oR + 32 * NR);      // uint4[16][32]: full A words (slot w | slot w + 16)
   static constexpr int oHc = oA + 16 * 32 * 16;         // uint2[NS]: doubled low 16 columns (zz, uu)
-  static constexpr int oHf = oHc + 8 * NS;              // uint2[NS]: full state (z, u)
-  static constexpr int oH1 = oHf + 8 * NS;              // uint2[NS]: n > 32, secondary word (z, u)
-  static constexpr int oHj = oH1 + (WIDE ? 8 * NS : 0);  // uint8[NS]: step within the batch
+  static constexpr int oHs = oHc + 8 * NS;              // n > 32: uint4[NBAT] H of each superblock (z, u, zw, uw)
+  // n <= 32: uint2[NS] the entries' full states (z, u); n > 32 recomputes
+  // them from Hs and the L tables (entry_state) and keeps the room for a
+  // batch of 4 superblocks
+  static constexpr int oHf = oHs + (WIDE ? 16 * NBAT : 0);
+  static constexpr int oHj = oHf + (WIDE ? 0 : 8 * NS);  // uint8[NS]: step within the batch (32 t + lane)
   static constexpr int oE = align16(oHj + NS);          // uint2[ECAP + 1][32]: passes (mask, list index)
   // per lane the low-row part of its B state in row form, for superblocks
   // of even / odd index: uint2 (m, s) [2][32], n > 32 uint4 (m0, s0, m1, s1)
   static constexpr int oL = oE + 8 * 32 * (ECAP + 1);
   static constexpr int kWarp = align16(oL + 2 * 32 * (WIDE ? 16 : 8));
+  // n > 32: the exact paths materialise the entries' full states (Hf, H1)
+  // in the pass-list area, which they do not use
+  __host__ __device__ static constexpr bool states_fit() { return !WIDE || 16 * NS <= oL - oE; }
   // the A decode's run table (run_table) borrows [oHc, kWarp): the lists,
   // the pass list and the L tables are all written after the decode
   template <int KEYS>
@@ -225,6 +231,7 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
   using T = Tab<FIX, KEYS, WIDE>;
   using S = BatchSmem<NBAT, ECAP, WIDE, FIX>;
   static_assert(S::template run_table_fits<KEYS>(), "k_walk_batch: the run table must fit the list area");
+  static_assert(S::states_fit(), "k_walk_batch: the exact paths' states must fit the pass-list area");
   const FastParams& p = bp.fp;
   extern __shared__ __align__(16) uint8_t batch_smem[];
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -233,8 +240,11 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
   uint4 (*A2)[32] = reinterpret_cast<uint4 (*)[32]>(ws + S::oA);
   uint32_t* IX = reinterpret_cast<uint32_t*>(ws + S::oA);  // weighted items: slot r's table indices [r][lane]
   uint2* Hc = reinterpret_cast<uint2*>(ws + S::oHc);
-  uint2* Hf = reinterpret_cast<uint2*>(ws + S::oHf);
-  uint2* H1 = reinterpret_cast<uint2*>(ws + S::oH1);
+  uint4* Hs = reinterpret_cast<uint4*>(ws + S::oHs);
+  // the entries' full states: stored (n <= 32) or materialised for the
+  // exact paths in the pass-list area (n > 32)
+  uint2* Hf = reinterpret_cast<uint2*>(ws + (WIDE ? S::oE : S::oHf));
+  uint2* H1 = reinterpret_cast<uint2*>(ws + S::oE + 8 * S::NS);
   uint8_t* Hj = ws + S::oHj;
   uint2 (*E)[32] = reinterpret_cast<uint2 (*)[32]>(ws + S::oE);
   uint2* L2 = reinterpret_cast<uint2*>(ws + S::oL);  // [parity][lane] (m, s), n <= 32
@@ -409,6 +419,7 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
       // (L in row form: add = sub of the negated row, sign m ^ s), its
       // compatibility, and the compacted list entry
       auto superblock = [&](uint32_t t, uint32_t gp) {
+        if (WIDE && lane == 0) Hs[t] = make_uint4(zh, uh, zhw, uhw);
         uint32_t zj = zh, uj = uh, zjw = zhw, ujw = uhw;
         if constexpr (WIDE) {
           const uint4 l = L4[32 * gp + lane];
@@ -425,8 +436,7 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
           const uint32_t pos = L + __popc(cmask & lanemask_lt);
           TP_CHECK(pos < (uint32_t)S::NS);
           Hc[pos] = make_uint2(__byte_perm(zj, zj, 0x1010), __byte_perm(uj, uj, 0x1010));
-          Hf[pos] = make_uint2(zj, uj);
-          if (WIDE) H1[pos] = make_uint2(zjw, ujw);
+          if (!WIDE) Hf[pos] = make_uint2(zj, uj);
           Hj[pos] = (uint8_t)(32u * t + lane);
         }
         L += __popc(cmask);
@@ -474,12 +484,52 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
       tested_steps += L;
       __syncwarp();
       if (L == 0) continue;
+      // the full state of list entry j (step 32 t + l of the batch): H of
+      // superblock t plus L[parity][l], as in the compaction
+      auto entry_state = [&](uint32_t j, uint32_t& z, uint32_t& u, uint32_t& zw, uint32_t& uw) {
+        if constexpr (!WIDE) {
+          const uint2 h = Hf[j];
+          z = h.x;
+          u = h.y;
+          return;
+        }
+        const uint32_t hj = Hj[j], t = hj >> 5;
+        const uint4 h = Hs[t];
+        const uint32_t gp = (uint32_t)((G0 + t) & 1ull);
+        z = h.x;
+        u = h.y;
+        if constexpr (WIDE) {
+          const uint4 l = L4[32 * gp + (hj & 31u)];
+          sub_word_u(z, u, l.x, l.x ^ l.y, l.y);
+          zw = h.z;
+          uw = h.w;
+          sub_word_u(zw, uw, l.z, l.z ^ l.w, l.w);
+        } else {
+          const uint2 l = L2[32 * gp + (hj & 31u)];
+          sub_word_u(z, u, l.x, l.x ^ l.y, l.y);
+        }
+      };
+      // the exact paths read every entry's state: materialise them (Hf, H1)
+      // in the pass-list area
+      auto materialise = [&]() {
+        if constexpr (!WIDE) return;
+        __syncwarp();
+        for (uint32_t e = lane; e < L; e += 32) {
+          uint32_t z, u, zw = 0, uw = 0;
+          entry_state(e, z, u, zw, uw);
+          Hf[e] = make_uint2(z, u);
+          if (WIDE) H1[e] = make_uint2(zw, uw);
+        }
+        __syncwarp();
+      };
       if (weighted) {  // deduplicated A side: every listed step exactly, with weights
+        materialise();
         batch_exact_weighted<FIX, KEYS, WIDE>(Hf, H1, Hj, L, Tm, IX, cnt, lane, colmask, colmask1,
                                               p.pm + 2 * b);
         continue;
       }
       auto exact_list = [&](uint32_t& bev, uint32_t& bodd) {
+        materialise();
         unsigned long long r;
         if constexpr (WIDE) r = batch_exact_wide<FIX, KEYS>(A2, Hf, H1, Hj, L, Tm, grp, pbase, cnt, lane, spm, colmask1);
         else r = batch_exact_packed(A2, Hf, Hj, L, lane, spm, vmask, colmask, p.n, one);
@@ -580,7 +630,8 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
             const uint32_t eo = tw ? (bit >= 2u * tw ? 2u : bit >= tw ? 1u : 0u) : bit >> 4;
             const uint32_t j = (ent.y & 0xFFFFu) + eo, w = tw ? bit - eo * tw : bit & 15u;
             TP_CHECK(j < L);
-            const uint2 h = Hf[j];
+            uint2 h, hw;
+            entry_state(j, h.x, h.y, hw.x, hw.y);
             const uint32_t gh = pair_g2(h.x, h.y);
             const uint32_t jp = Hj[j] & 1u;
 #pragma unroll
@@ -596,7 +647,7 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
                 if constexpr (WIDE) {
                   // the primary columns are nonzero: test the secondary ones
                   const uint32_t rr =
-                      bucket_wide_term<FIX, KEYS>(Tm, grp, pbase + 32u * lrow(k) + lane, H1[j], colmask1);
+                      bucket_wide_term<FIX, KEYS>(Tm, grp, pbase + 32u * lrow(k) + lane, hw, colmask1);
                   if (!rr) continue;
                   par = rr >> 1;
                 }
@@ -625,10 +676,15 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
 // Sized so that four 4-warp blocks fit an SM (228 KB of shared memory).
 template <bool WIDE>
 struct BatchShape {
-  static constexpr int NBAT = WIDE ? 2 : 4;
-  static constexpr int ECAP = WIDE ? 6 : 10;
+#ifndef TP_BATCH_NB_NARROW
+#define TP_BATCH_NB_NARROW 4
+#define TP_BATCH_EC_NARROW 10
+#endif
+  static constexpr int NBAT = WIDE ? 4 : TP_BATCH_NB_NARROW;
+  static constexpr int ECAP = WIDE ? 8 : TP_BATCH_EC_NARROW;
   // four blocks per SM: 228 KB of shared memory, 1 KB reserved per block
-  static_assert(4 * (4 * BatchSmem<NBAT, ECAP, WIDE, WIDE ? 17 : 13>::kWarp + 1024) <= 228 * 1024,
+  // (the smallest A side in use: 14 rows for n <= 32, 17 for n > 32)
+  static_assert(4 * (4 * BatchSmem<NBAT, ECAP, WIDE, WIDE ? 17 : 14>::kWarp + 1024) <= 228 * 1024,
                 "k_walk_batch: four blocks must fit an SM");
 };
 
