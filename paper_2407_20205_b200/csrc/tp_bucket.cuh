@@ -319,6 +319,8 @@ struct BucketParamsCfg {  // BucketParams' fields, then the configuration
   unsigned long long* tested;
   unsigned long long s_end;
   int fix, keys;
+  unsigned int* chunk_ctr;  // (BucketParams' sticky-piece fields)
+  unsigned long long npieces;
 };
 }  // namespace
 

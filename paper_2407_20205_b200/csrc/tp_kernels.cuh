@@ -107,6 +107,11 @@ struct BucketParams {
   const uint32_t* ptab;         // [B][pieces] bucket | count << 8 | piece-in-bucket << 20 (count 0 = unused)
   unsigned long long* tested;   // += pairs actually tested (compatible steps x 1024), or nullptr
   unsigned long long s_end;     // end of the superblock region
+  // k_walk_batch, n > 32 ("sticky" pieces): a chunk counter per piece; items
+  // are tickets t, piece t % npieces (matrix fastest), and a warp that joins
+  // a piece takes its chunks from the counter until they run out
+  unsigned int* chunk_ctr = nullptr;
+  unsigned long long npieces = 0;
 };
 struct BucketCfg {
   int fix;   // A side: rows 0..fix-1

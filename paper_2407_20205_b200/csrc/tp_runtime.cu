@@ -357,13 +357,31 @@ int make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, uns
     }();
     while (nblk > 1 && (items_of(nblk) < min_items * warps || (nblk > 1024 && items_of(nblk) < per_warp * warps)))
       nblk = (nblk + 1) / 2;
+    // k_walk_batch, n > 32: sticky pieces (a warp keeps its decoded piece and
+    // takes chunk after chunk of it from the piece's counter), so chunks can
+    // be short without paying the per-piece set-up for each: at least 16
+    // chunks per warp, of at least 16 superblocks.  Only where the items
+    // above are few per warp (their tail shows: C4 1.90 -> 1.76 ms); long
+    // jobs with many items (C5) measured 2 % slower with it.
+    // TRITPERM_STICKY: 0 off, 1 this rule, 2 always (n > 32)
+    static const int sticky_mode = [] {
+      const char* e = getenv("TRITPERM_STICKY");
+      return e ? atoi(e) : 1;
+    }();
+    const bool sticky = batch && n > 32 &&
+                        (sticky_mode == 2 || (sticky_mode == 1 && items_of(nblk) < 64 * warps));
+    if (sticky) {
+      nblk = std::min<unsigned long long>(std::max<unsigned long long>(total, 1), 1024);
+      while (nblk > 16 && items_of(nblk) < 16 * warps) nblk /= 2;
+    }
     const unsigned long long chunks = (total + nblk - 1) / nblk;
     if (big) {
       // per matrix: the half table (2-14 KB) and the piece table; no cap,
       // any batch fits (C2: 33 MB; a 65,536-trial n >= 33 slab: 0.9 GB)
       const size_t tb = align_up(tp::bucket_tab_bytes(cfg, n > 32) * (size_t)B, 256);
       void* mem = nullptr;
-      if (int rc = sc.take(tb + (size_t)B * P * sizeof(uint32_t), &mem)) return rc;
+      const size_t pb = align_up((size_t)B * P * sizeof(uint32_t), 256);
+      if (int rc = sc.take(tb + pb + (sticky ? (size_t)B * P * sizeof(unsigned int) : 0), &mem)) return rc;
       pl.bucket = true;
       pl.bucket_packed = packed;
       pl.bucket_batch = batch;
@@ -371,6 +389,10 @@ int make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, uns
       pl.bucket_cfg = cfg;
       pl.bucket_tab = mem;
       pl.bucket_ptab = reinterpret_cast<uint32_t*>(static_cast<char*>(mem) + tb);
+      if (sticky) {
+        pl.bkp.chunk_ctr = reinterpret_cast<unsigned int*>(static_cast<char*>(mem) + tb + pb);
+        pl.bkp.npieces = B * (unsigned long long)P;
+      }
       tp::FastParams& f = pl.bkp.fp;
       f.rows = rows;
       f.pm = pm;
@@ -379,6 +401,10 @@ int make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, uns
       f.L = nblk << bv;
       f.chunks = chunks;
       f.items = B * (unsigned long long)P * chunks;
+      if (sticky) {  // tickets: every piece at least twice, about 4 per warp
+        const unsigned long long np = B * (unsigned long long)P;
+        f.items = np * std::max<unsigned long long>(2, (4 * warps + np - 1) / np);
+      }
       f.nblk = (uint32_t)nblk;  // superblocks of 2^bv B steps
       f.lognblk = 0;
       f.n = n;
@@ -542,6 +568,7 @@ int run_plan(const Plan& pl, cudaStream_t st, int* launches) {
   if (pl.bucket) {  // (ranges: plus the generic head and tail below)
     TP_CUDA(tp::launch_bucket_group(pl.bkp.fp.rows, pl.bucket_B, pl.bkp.fp.n, pl.bucket_cfg, pl.bucket_packed,
                                     pl.bucket_tab, pl.bucket_ptab, st));
+    if (pl.bkp.chunk_ctr) TP_CUDA(cudaMemsetAsync(pl.bkp.chunk_ctr, 0, pl.bkp.npieces * sizeof(unsigned int), st));
     if (pl.bucket_batch) TP_CUDA(tp::launch_walk_batch(pl.bucket_grid, pl.bkp, pl.bucket_cfg, st));
     else TP_CUDA(tp::launch_walk_bucket(pl.bucket_grid, pl.bkp, pl.bucket_packed, st));
     nl += 2;

@@ -261,19 +261,38 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
     const unsigned long long item = next_item(p, lane, n_items, blockIdx.x * 4 + warp);
     if (item >= p.items) break;
     ++n_items;
-    // item = (piece * chunks + chunk) * B + matrix (k_walk_bucket's order)
-    const unsigned long long nmat = p.items / ((unsigned long long)kBucketPieces * p.chunks);
-    const unsigned long long rest = item / nmat;
-    const unsigned long long b = item - rest * nmat;
-    const uint32_t q = (uint32_t)(rest / p.chunks);
-    const unsigned long long c = rest - (unsigned long long)q * p.chunks;
-    const unsigned long long sb0 = p.F0 + c * p.nblk;
-    const uint32_t nsb = (uint32_t)min((unsigned long long)p.nblk, bp.s_end - sb0);
-    const unsigned long long A0 = sb0 << V;
-    TP_CHECK(q < (uint32_t)kBucketPieces && b < nmat);
+    // item = (piece * chunks + chunk) * B + matrix (k_walk_bucket's order);
+    // sticky pieces (n > 32): item = ticket, piece (t % npieces) = q * B + b,
+    // the chunks come from the piece's counter
+    const bool sticky = WIDE && bp.chunk_ctr != nullptr;
+    unsigned long long b, c, pid = 0;
+    uint32_t q;
+    auto grab = [&]() -> unsigned long long {  // the piece's next chunk
+      unsigned int v = 0;
+      if (lane == 0) v = atomicAdd(bp.chunk_ctr + pid, 1u);
+      return (unsigned long long)__shfl_sync(FULL, v, 0);
+    };
+    if (sticky) {
+      const unsigned long long nmat = bp.npieces / kBucketPieces;
+      pid = item % bp.npieces;
+      q = (uint32_t)(pid / nmat);
+      b = pid - (unsigned long long)q * nmat;
+      TP_CHECK(q < (uint32_t)kBucketPieces && b < nmat);
+    } else {
+      const unsigned long long nmat = p.items / ((unsigned long long)kBucketPieces * p.chunks);
+      const unsigned long long rest = item / nmat;
+      b = item - rest * nmat;
+      q = (uint32_t)(rest / p.chunks);
+      c = rest - (unsigned long long)q * p.chunks;
+      TP_CHECK(q < (uint32_t)kBucketPieces && b < nmat);
+    }
     const uint32_t pt = bp.ptab[b * kBucketPieces + q];
     const uint32_t cnt = (pt >> 8) & 0xFFFu;  // real slots of the piece
     if (cnt == 0) continue;                   // unused piece
+    if (sticky) {
+      c = grab();
+      if (c >= p.chunks) continue;  // the piece is done
+    }
     const uint32_t grp = pt & 0xFFu;
     const uint32_t pbase = ((pt >> 20) & 0x7FFu) << 10;  // positions [pbase, pbase + cnt) of the bucket
     const bool weighted = (pt >> 31) != 0;
@@ -379,19 +398,7 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
     // every lane) and rows FIX..FIX+4 from gray(j) ^ (G odd ? 16 : 0) (this
     // lane's low part, two vectors per item, L[G & 1][lane]).  So a lane's
     // state is one add, H + L, and H changes by one row per superblock.
-    uint32_t zh, uh, zhw = 0, uhw = 0;
     {
-      uint32_t z = colmask, g = 0, zw = colmask1, gw = 0;
-      const unsigned long long hs = sb0 ^ (sb0 >> 1);
-      for (int r = FIX + V; r < p.n; ++r)
-        if ((hs >> (r - FIX - V)) & 1ull) {
-          sub_word(z, g, R[r - FIX].m[0], R[r - FIX].a[0]);
-          if (WIDE) sub_word(zw, gw, R[r - FIX].m[1], R[r - FIX].a[1]);
-        }
-      zh = z;
-      uh = pair_u2(z, g);
-      zhw = zw;
-      uhw = pair_u2(zw, gw);
 #pragma unroll
       for (uint32_t par = 0; par < 2; ++par) {
         const uint32_t gl = (lane ^ (lane >> 1)) ^ (par << 4);
@@ -407,6 +414,23 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
         if (WIDE) L4[32 * par + lane] = make_uint4(m0, gll & m0, m1, glw & m1);
         else L2[32 * par + lane] = make_uint2(m0, gll & m0);
       }
+    }
+    for (;;) {  // the item's chunk; sticky pieces: every chunk this warp can take
+    const unsigned long long sb0 = p.F0 + c * p.nblk;
+    const uint32_t nsb = (uint32_t)min((unsigned long long)p.nblk, bp.s_end - sb0);
+    uint32_t zh, uh, zhw = 0, uhw = 0;
+    {
+      uint32_t z = colmask, g = 0, zw = colmask1, gw = 0;
+      const unsigned long long hs = sb0 ^ (sb0 >> 1);
+      for (int r = FIX + V; r < p.n; ++r)
+        if ((hs >> (r - FIX - V)) & 1ull) {
+          sub_word(z, g, R[r - FIX].m[0], R[r - FIX].a[0]);
+          if (WIDE) sub_word(zw, gw, R[r - FIX].m[1], R[r - FIX].a[1]);
+        }
+      zh = z;
+      uh = pair_u2(z, g);
+      zhw = zw;
+      uhw = pair_u2(zw, gw);
     }
     uint32_t ev = 0, odd = 0;
     uint32_t tested_steps = 0;
@@ -668,6 +692,10 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
       const uint32_t words = FilterWidths<FIX, KEYS>::width(nwd);
       atomicAdd(bp.tested, 64ull * words * tested_steps);
     }
+    if (!sticky) break;
+    c = grab();
+    if (c >= p.chunks) break;
+    }  // chunks
   }
   queue_done(p, lane);
 }
@@ -700,7 +728,7 @@ static cudaError_t launch_batch_k(int grid, const BucketParamsCfg& bc, cudaStrea
 }
 
 cudaError_t launch_walk_batch(int grid, const BucketParams& bp, BucketCfg c, cudaStream_t st) {
-  const BucketParamsCfg bc{bp.fp, bp.tab, bp.ptab, bp.tested, bp.s_end, c.fix, c.keys};
+  const BucketParamsCfg bc{bp.fp, bp.tab, bp.ptab, bp.tested, bp.s_end, c.fix, c.keys, bp.chunk_ctr, bp.npieces};
   if (bp.fp.n > 32 && c.fix == 17 && c.keys == 4) return launch_batch_k<true, 17, 4>(grid, bc, st);
   if (bp.fp.n > 32 && c.fix == 17 && c.keys == 5) return launch_batch_k<true, 17, 5>(grid, bc, st);
   if (c.fix == 14 && c.keys == 3) return launch_batch_k<false, 14, 3>(grid, bc, st);

@@ -1032,7 +1032,7 @@ cudaError_t launch_bucket_group(const RowRec* rows, long long B, int n, BucketCf
 
 cudaError_t launch_walk_bucket(int grid, const BucketParams& bp, bool packed, cudaStream_t st) {
   const BucketCfg c = bucket_cfg(bp.fp.n, packed, false);
-  const BucketParamsCfg bc{bp.fp, bp.tab, bp.ptab, bp.tested, bp.s_end, c.fix, c.keys};
+  const BucketParamsCfg bc{bp.fp, bp.tab, bp.ptab, bp.tested, bp.s_end, c.fix, c.keys, nullptr, 0};
   if (bp.fp.n > 32) k_walk_bucket<5, 4, true, true, 17, 4><<<grid, 128, 0, st>>>(bc);
   else if (!packed) k_walk_bucket<4, 4, false, false, 14, 2><<<grid, 128, 0, st>>>(bp);
   else if (c.fix == 13) k_walk_bucket<5, 4, true, false, 13, 2><<<grid, 128, 0, st>>>(bp);
