@@ -364,10 +364,8 @@ int make_plan(Device& d, int n, unsigned long long B, unsigned long long lo, uns
     // above are few per warp (their tail shows: C4 1.90 -> 1.76 ms); long
     // jobs with many items (C5) measured 2 % slower with it.
     // TRITPERM_STICKY: 0 off, 1 this rule, 2 always (n > 32)
-    static const int sticky_mode = [] {
-      const char* e = getenv("TRITPERM_STICKY");
-      return e ? atoi(e) : 1;
-    }();
+    const char* se = getenv("TRITPERM_STICKY");  // read per call: tests switch it at run time
+    const int sticky_mode = se ? atoi(se) : 1;
     const bool sticky = batch && n > 32 &&
                         (sticky_mode == 2 || (sticky_mode == 1 && items_of(nblk) < 64 * warps));
     if (sticky) {

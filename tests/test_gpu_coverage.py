@@ -248,3 +248,30 @@ def test_bounds_checked_build_runs_every_walk_family():
                          capture_output=True, text=True, timeout=900)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
     assert "sanitize case ok" in out.stdout
+
+
+def test_walk_options_agree(gpu, oracle, monkeypatch):
+    """The scheduling and kernel options give the same raw partials: sticky
+    pieces off / by the rule / always (n > 32), and the round-2 k_walk_bucket
+    (TRITPERM_BATCH=0) against k_walk_batch, on the C4 config's full 2^36
+    traversal, the C5 matrix's 2^36-step window, and the C2 batch's first 64
+    matrices (all pinned to the reference: anchors.json)."""
+    from paper_2407_20205_b200 import _kernels, fixtures
+
+    g = load_golden("anchors.json")
+    w4, w5 = g["c4_full"], g["c5_window36"]
+    m4 = gpu.MatrixF3(centred(dec(w4["a"], 36)))
+    m5 = gpu.MatrixF3(centred(dec(w5["a"], 50)))
+    c2 = fixtures.uniform_batch(24, 0, 0, 64)
+    for env in ({"TRITPERM_STICKY": "0"}, {"TRITPERM_STICKY": "1"}, {"TRITPERM_STICKY": "2"},
+                {"TRITPERM_BATCH": "0"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        _kernels.walk_tested(0)
+        assert gpu.perm_chunk(m4, 1, 1 << 36).partial_sum == w4["partial"], env
+        assert gpu.perm_chunk(m5, w5["lo"], w5["hi"]).partial_sum == w5["partial"], env
+        _, part, _ = gpu.perm_mod3_batch(c2)
+        assert part.tolist() == g["c2_partials_head"], env
+        assert _kernels.walk_tested(0) > 0, env  # the bucketed walks ran
+        for k in env:
+            monkeypatch.delenv(k)
