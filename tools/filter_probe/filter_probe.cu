@@ -106,8 +106,8 @@ __device__ __forceinline__ uint32_t v1_mask(uint32_t a0, uint32_t a1, uint32_t a
 
 struct Out { unsigned long long hits, sum; };
 
-template <int V>
-__global__ void __launch_bounds__(128, 4) k_probe(const uint32_t* A, const uint2* B, int nB, int reps, uint32_t* masks, int record, unsigned long long* res) {
+template <int V, int MINB = 4>
+__global__ void __launch_bounds__(128, MINB) k_probe(const uint32_t* A, const uint2* B, int nB, int reps, uint32_t* masks, int record, unsigned long long* res) {
   __shared__ __align__(16) uint2 Hc[4][1024];
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = lane; i < nB; i += 32) {
@@ -222,5 +222,25 @@ int main() {
     const double cyc = ms * 1e-3 * clk * 1e3;
     printf("V%d: %.3f ms, %.2f tests/clk/SM (at %d MHz nominal)\n", v, ms, tests / cyc / nsm, clk / 1000);
   }
+  // occupancy sweep of V0: k blocks of 4 warps per SM (grid nsm * k)
+  auto sweep = [&](auto kc) {
+    constexpr int KB = decltype(kc)::value;
+    const int g2 = nsm * KB;
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    CK(cudaMemset(dR, 0, 16));
+    k_probe<0, KB><<<g2, 128>>>(dA, dB, nB, reps, dM[0], 0, dR);
+    cudaEventRecord(a);
+    k_probe<0, KB><<<g2, 128>>>(dA, dB, nB, reps, dM[0], 0, dR);
+    cudaEventRecord(b); CK(cudaEventSynchronize(b)); CK(cudaGetLastError());
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    const double tests = (double)g2 * 128 * reps * (nB / 2) * 32;
+    printf("V0 with %d warps/SM: %.2f tests/clk/SM\n", 4 * KB, tests / (ms * 1e-3 * clk * 1e3) / nsm);
+  };
+  sweep(std::integral_constant<int, 2>{});
+  sweep(std::integral_constant<int, 3>{});
+  sweep(std::integral_constant<int, 4>{});
+  sweep(std::integral_constant<int, 5>{});
+  sweep(std::integral_constant<int, 6>{});
+  sweep(std::integral_constant<int, 8>{});
   return 0;
 }
