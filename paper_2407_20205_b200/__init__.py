@@ -18,6 +18,7 @@ from .core_f3 import (
     sign_parity,
     sub_reps,
 )
+from .checkpoint import RangeJournal, perm_mod3_resumable, resumable_counts
 from .experiments import (
     ExactCountResult,
     McHistogram,
@@ -51,6 +52,7 @@ __all__ = [
     "McHistogram",
     "McResult",
     "PackedF3Vec",
+    "RangeJournal",
     "add_reps",
     "cmod3",
     "decode",
@@ -64,10 +66,12 @@ __all__ = [
     "perm_mod3_batch",
     "perm_mod3_fast",
     "perm_mod3_parallel",
+    "perm_mod3_resumable",
     "pi_digit",
     "pi_matrix",
     "resolve_gpus",
     "resolve_jobs",
+    "resumable_counts",
     "sample_trial_matrix",
     "sign_parity",
     "split_steps",

@@ -74,12 +74,25 @@ def _cmd_perm(args) -> int:
         m = parse_matrix_text(fh.read())
     gpus = resolve_gpus(args.jobs)
     t0 = time.perf_counter()
-    value = perm_mod3_parallel(m, len(gpus))
+    extra = {}
+    if args.checkpoint:
+        # journalled traversal: finished parts are kept in the file and a rerun resumes from it
+        from .checkpoint import perm_mod3_resumable
+
+        value = perm_mod3_resumable(m, args.checkpoint, parts=args.parts, jobs=len(gpus), max_parts=args.max_parts)
+        extra = {"checkpoint": args.checkpoint, "parts": args.parts}
+        if value is None:
+            print(json.dumps({"schema": PERM_SCHEMA, "n": m.n, "method": "mod3", "jobs": len(gpus), "value": None,
+                              "complete": False, "elapsed_seconds": time.perf_counter() - t0, "device": "b200",
+                              **extra}))
+            return 0
+    else:
+        value = perm_mod3_parallel(m, len(gpus))
     elapsed = time.perf_counter() - t0
     shown = _shown(value, args.mod3_classes)
     print(shown)
     print(json.dumps({"schema": PERM_SCHEMA, "n": m.n, "method": "mod3", "jobs": len(gpus), "value": shown,
-                      "elapsed_seconds": elapsed, "device": "b200"}))
+                      "elapsed_seconds": elapsed, "device": "b200", **extra}))
     return 0
 
 
@@ -155,6 +168,9 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--method", default="mod3")
     p.add_argument("--jobs", type=int, default=None, help="GPUs to split the traversal over")
     p.add_argument("--mod3-classes", action="store_true", help="print {0,1,2} instead of {-1,0,1}")
+    p.add_argument("--checkpoint", default=None, help="journal of finished step ranges; a rerun resumes from it")
+    p.add_argument("--parts", type=int, default=64, help="parts the traversal is journalled in")
+    p.add_argument("--max-parts", type=int, default=None, help="stop after computing this many parts")
     p.set_defaults(func=_cmd_perm)
 
     p = sub.add_parser("perm-batch", help="classes and histogram of a .npy stack [B, n, n]")
