@@ -21,7 +21,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, tmpdir):
     import sys
 
     sys.path.insert(0, REPO)
@@ -61,17 +61,32 @@ def _worker(rank, world, port, q):
             local[oracle.perm_centered(oracle.sample_classes(8, 5, t)) % 3] += 1
         out["hist"] = parallel.distributed_hist(local.tolist(), device="cpu").tolist()
         out["rank_range"] = parallel.rank_range(20, rank, world)
+        # journalled traversal: every part split over the ranks, rank 0 keeps the journal
+        from paper_2407_20205_b200 import checkpoint
+
+        def dcounts(mm, lo, hi):
+            return parallel.distributed_counts(mm, lo, hi, counts_fn=counts, device="cpu")
+
+        path = os.path.join(tmpdir, "c1.journal")
+        first = checkpoint.resumable_counts(m, path, parts=6, max_parts=2, counts_fn=dcounts)
+        dist.barrier()
+        out["journal_first"] = (first, len(open(path).read().splitlines()))
+        dist.barrier()
+        out["journal"] = checkpoint.resumable_counts(m, path, parts=6, counts_fn=dcounts)
+        dist.barrier()
+        out["journal_lines"] = len(open(path).read().splitlines())
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
 
 
 @pytest.fixture(scope="module")
-def results(oracle):
+def results(oracle, tmp_path_factory):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    tmpdir = str(tmp_path_factory.mktemp("journal"))
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, tmpdir)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in procs)
@@ -107,3 +122,16 @@ def test_histogram_allreduce(results, oracle):
     for t in range(37):
         want[oracle.perm_centered(oracle.sample_classes(8, 5, t)) % 3] += 1
     assert results[0]["hist"] == results[1]["hist"] == want.tolist()
+
+
+def test_journalled_traversal_over_ranks(results, oracle):
+    """checkpoint.resumable_counts under world_size 2: parts are split over the
+    ranks, only rank 0 writes, and a resumed run finishes the missing parts."""
+    a = dec(load_golden("anchors.json")["c1"][0]["a"], 20)
+    mags, sgns = oracle.planes_from_classes(a)
+    want = oracle.chunk_counts(mags, sgns, 20, 1, 1 << 20)
+    for r in (0, 1):
+        (p, q, complete), lines = results[r]["journal_first"]
+        assert not complete and lines == 3  # header + 2 parts, written once
+        assert results[r]["journal"] == (want[0], want[1], True)
+        assert results[r]["journal_lines"] == 7
