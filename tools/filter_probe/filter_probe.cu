@@ -92,6 +92,29 @@ __device__ __forceinline__ void t_v3(uint32_t z1, uint32_t g1, uint32_t za, uint
       : "+r"(m) : "r"(z1), "r"(g1), "r"(za), "r"(ua), "r"(zb), "r"(ub), "r"(one), "r"(cneg), "n"(BIT));
 }
 
+// V4: three B entries against word w share one zero-field test: the
+// halfword-wise minimum of the three zp words (VIMNMX3.U16x2) has a zero
+// field iff one of them has; bit w of m = a pass of word w by any of the three
+template <uint32_t BIT>
+__device__ __forceinline__ void t_v4(uint32_t z1, uint32_t g1, uint32_t za, uint32_t ua, uint32_t zb, uint32_t ub,
+                                     uint32_t zc, uint32_t uc, uint32_t& m, uint32_t one, uint32_t cneg) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 da, zpa, db, zpb, dc, zpc, mn, t, h;\n\t"
+      "lop3.b32 da, %1, %2, %4, 0x06;\n\t"
+      "lop3.b32 zpa, da, %1, %3, 0x09;\n\t"
+      "lop3.b32 db, %1, %2, %6, 0x06;\n\t"
+      "lop3.b32 zpb, db, %1, %5, 0x09;\n\t"
+      "lop3.b32 dc, %1, %2, %8, 0x06;\n\t"
+      "lop3.b32 zpc, dc, %1, %7, 0x09;\n\t"
+      "min.u16x2 mn, zpa, zpb;\n\t"
+      "min.u16x2 mn, mn, zpc;\n\t"
+      "mad.lo.u32 t, mn, %9, %10;\n\t"
+      "lop3.b32 h, t, 0x80008000, mn, 0x40;\n\t"
+      "setp.ne.u32 p, h, 0;\n\t"
+      "@p mad.lo.u32 %0, %9, %11, %0;\n\t}"
+      : "+r"(m) : "r"(z1), "r"(g1), "r"(za), "r"(ua), "r"(zb), "r"(ub), "r"(zc), "r"(uc), "r"(one), "r"(cneg), "n"(BIT));
+}
+
 // decode the three V1 accumulators into the V0 mask layout (bit w: step a word w,
 // bit 16 + w: step b word w); index i = w (a) or 16 + w (b), acc0: i 0..10,
 // acc1: i 11..21, acc2: i 22..31, weight 2^(i - base)
@@ -122,6 +145,30 @@ __global__ void __launch_bounds__(128, MINB) k_probe(const uint32_t* A, const ui
   const uint32_t one = res ? 1u : 0u;  // runtime 1
   const uint32_t cneg = 0xfffeffffu * one;
   unsigned long long hits = 0, sum = 0;
+  if constexpr (V >= 4) {
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll 1
+      for (int i = 0; i + 3 <= nB; i += 3) {
+        const uint2 ha = Hc[warp][i], hb = Hc[warp][i + 1], hc = Hc[warp][i + 2];
+        uint32_t M = 0;
+        if constexpr (V == 4) {
+          sfor<16>([&](auto wc) { constexpr int w = decltype(wc)::value;
+            t_v4<(1u << w)>(Zp[w], Gp[w], ha.x, ha.y, hb.x, hb.y, hc.x, hc.y, M, one, cneg); });
+        } else {
+          uint32_t Ma = 0, Mb = 0, Mc = 0;
+          sfor<16>([&](auto wc) { constexpr int w = decltype(wc)::value;
+            t_v0<(1u << w)>(Zp[w], Gp[w], ha.x, ha.y, Ma, one, cneg);
+            t_v0<(1u << w)>(Zp[w], Gp[w], hb.x, hb.y, Mb, one, cneg);
+            t_v0<(1u << w)>(Zp[w], Gp[w], hc.x, hc.y, Mc, one, cneg); });
+          M = Ma | Mb | Mc;
+        }
+        if (M) { ++hits; sum += M; }
+      }
+    }
+    atomicAdd(&res[0], hits);
+    atomicAdd(&res[1], sum);
+    return;
+  }
   for (int r = 0; r < reps; ++r) {
 #pragma unroll 1
     for (int i = 0; i + 2 <= nB; i += 2) {
@@ -192,6 +239,8 @@ int main() {
     if (v == 1) k_probe<1><<<grid, 128>>>(dA, dB, nB, reps, dM[1], record, dR);
     if (v == 2) k_probe<2><<<grid, 128>>>(dA, dB, nB, reps, dM[2], record, dR);
     if (v == 3) k_probe<3><<<grid, 128>>>(dA, dB, nB, reps, dM[3], record, dR);
+    if (v == 4) k_probe<4><<<grid, 128>>>(dA, dB, nB, reps, nullptr, 0, dR);
+    if (v == 5) k_probe<5><<<grid, 128>>>(dA, dB, nB, reps, nullptr, 0, dR);
     CK(cudaGetLastError());
   };
   for (int v = 0; v < 4; ++v) launch(v, 1, 1);
@@ -219,6 +268,19 @@ int main() {
     cudaEventRecord(a); launch(v, reps, 0); cudaEventRecord(b); CK(cudaEventSynchronize(b));
     float ms; cudaEventElapsedTime(&ms, a, b);
     const double tests = (double)grid * 128 * reps * (nB / 2) * 32;
+    const double cyc = ms * 1e-3 * clk * 1e3;
+    printf("V%d: %.3f ms, %.2f tests/clk/SM (at %d MHz nominal)\n", v, ms, tests / cyc / nsm, clk / 1000);
+  }
+  // V4 (min3 over three entries) against V5 (the V0 tests in the same layout): same hits and mask sums
+  for (int v = 4; v <= 5; ++v) {
+    launch(v, 1, 0);
+    unsigned long long r2[2]; CK(cudaMemcpy(r2, dR, 16, cudaMemcpyDeviceToHost));
+    printf("V%d: hits %llu, mask sum %llu\n", v, r2[0], r2[1]);
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    launch(v, reps, 0);
+    cudaEventRecord(a); launch(v, reps, 0); cudaEventRecord(b); CK(cudaEventSynchronize(b));
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    const double tests = (double)grid * 128 * reps * (nB / 3) * 3 * 16;
     const double cyc = ms * 1e-3 * clk * 1e3;
     printf("V%d: %.3f ms, %.2f tests/clk/SM (at %d MHz nominal)\n", v, ms, tests / cyc / nsm, clk / 1000);
   }
