@@ -20,10 +20,13 @@
 //     H1 the secondary word for n > 32) and the step within the batch (Hj,
 //     whose parity is the B subset's size parity: batches start at even
 //     steps);
-//   * the filter is the packed test of tp_walk_bucket.cu (1.5 LOP3 per pair:
-//     two pairs per 32-bit word, zero-field test on the FMA pipe); a lane's
-//     passes (mask of words x the two steps, list index) go to its pass list
-//     E and are verified exactly after the loop;
+//   * the filter is the packed test of tp_walk_bucket.cu (two pairs per
+//     32-bit word on 16 columns each) for three entries at a time with one
+//     zero-field test on the halfword-wise minimum of their three result
+//     words (packed_test3: 4/3 ALU ops per pair); a lane's passes (mask of
+//     words, list index of the three entries) go to its pass list E; after
+//     the loop the warp compacts the lists and verifies the passes exactly,
+//     one (record, entry) per lane and round;
 //   * a pass list that overflows, and event-dense matrices, take the exact
 //     evaluation of the whole list; deduplicated (weighted) A sides take the
 //     weighted exact walk, as in k_walk_bucket.
@@ -568,52 +571,39 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
         dense = __any_sync(FULL, bev >= (uint32_t)(K / 2) * nbt);
         continue;
       }
-      // the packed filter over the list, two entries per iteration: bit w
-      // (entry i) / 16 + w (entry i + 1) of M = a pass of word w; pieces of
-      // at most 10 words three entries per iteration: bit W e + w (entry
-      // i + e), the record's list index tagged with W << 16
+      // the packed filter over the list, three entries per iteration: the
+      // three zp words of packed word w meet in one halfword-wise minimum
+      // (packed_test3), so bit w of M = word w passed for one of the entries
+      // i, i + 1, i + 2 (the verify finds which); one or two entries are left
+      // for a last iteration
       uint32_t ne = 0;
-      auto record = [&](uint32_t M, uint32_t tag) {
+      auto record = [&](uint32_t M, uint32_t i) {
         // unconditional store (slot ECAP takes the overflow), no branch
-        E[min(ne, (uint32_t)ECAP)][lane] = make_uint2(M, tag);
+        E[min(ne, (uint32_t)ECAP)][lane] = make_uint2(M, i);
         ne += M != 0u ? 1u : 0u;
       };
       auto filter = [&](auto Wc) {
         constexpr int W = decltype(Wc)::value;
         uint32_t i = 0;
-        if constexpr (W <= 10) {
 #pragma unroll 1
-          for (; i + 3 <= L; i += 3) {
-            const uint2 ha = Hc[i], hb = Hc[i + 1], hc = Hc[i + 2];
-            uint32_t M = 0;
-            static_for<W>([&](auto wc) {
-              constexpr int w = decltype(wc)::value;
-              packed_test<(1u << w)>(Zp[w], Gp[w], ha.x, ha.y, M, one, cneg);
-              packed_test<(1u << (W + w))>(Zp[w], Gp[w], hb.x, hb.y, M, one, cneg);
-              packed_test<(1u << (2 * W + w))>(Zp[w], Gp[w], hc.x, hc.y, M, one, cneg);
-            });
-            record(M, i | ((uint32_t)W << 16));
-          }
-        }
-#pragma unroll 1
-        for (; i + 2 <= L; i += 2) {
-          // (after the three-entry loop i may be odd: two 8-byte loads)
-          uint4 hab;
-          if constexpr (W <= 10) {
-            const uint2 ha = Hc[i], hb = Hc[i + 1];
-            hab = make_uint4(ha.x, ha.y, hb.x, hb.y);
-          } else {
-            hab = *reinterpret_cast<const uint4*>(Hc + i);
-          }
+        for (; i + 3 <= L; i += 3) {
+          const uint2 ha = Hc[i], hb = Hc[i + 1], hc = Hc[i + 2];
           uint32_t M = 0;
           static_for<W>([&](auto wc) {
             constexpr int w = decltype(wc)::value;
-            packed_test<(1u << w)>(Zp[w], Gp[w], hab.x, hab.y, M, one, cneg);
-            packed_test<(1u << (16 + w))>(Zp[w], Gp[w], hab.z, hab.w, M, one, cneg);
+            packed_test3<(1u << w)>(Zp[w], Gp[w], ha.x, ha.y, hb.x, hb.y, hc.x, hc.y, M, one, cneg);
           });
           record(M, i);
         }
-        if (i < L) {  // an odd last entry alone
+        if (i + 2 == L) {
+          const uint2 ha = Hc[i], hb = Hc[i + 1];
+          uint32_t M = 0;
+          static_for<W>([&](auto wc) {
+            constexpr int w = decltype(wc)::value;
+            packed_test2<(1u << w)>(Zp[w], Gp[w], ha.x, ha.y, hb.x, hb.y, M, one, cneg);
+          });
+          record(M, i);
+        } else if (i < L) {
           const uint2 ha = Hc[i];
           uint32_t M = 0;
           static_for<W>([&](auto wc) {
@@ -641,42 +631,62 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
         odd += bodd;
         dense = p.dense_ok != 0 && __any_sync(FULL, bev >= (uint32_t)(K / 2) * nbt);
       } else if (nemax != 0) {
+        // Verify, balanced over the lanes.  The records are compacted row
+        // by row into one flat list in place (row r only lands on flat
+        // positions < 32 (r + 1), all read by then), tagged with their lane;
+        // a work item is (record, entry): lane k takes items k, k + 32, ..
+        // and tests its entry against the record's words of the SOURCE
+        // lane's slots (A2, and the slots' parities SV in the list area,
+        // which the filter has finished with).
+        uint2* Fl = &E[0][0];
+        uint2* SV = Hc;
+        __syncwarp();
+        SV[lane] = make_uint2(spm, vmask);
+        uint32_t nrec = 0;
+        for (uint32_t r = 0; r < nemax; ++r) {
+          const bool has = r < ne;
+          const uint2 rec = E[r][lane];
+          const uint32_t bal = __ballot_sync(FULL, has);
+          __syncwarp();
+          if (has) Fl[nrec + __popc(bal & lanemask_lt)] = make_uint2(rec.x, rec.y | (lane << 16));
+          nrec += __popc(bal);
+        }
+        __syncwarp();
         uint32_t bev = 0, bodd = 0;
-        for (uint32_t e = 0; e < ne; ++e) {
-          const uint2 ent = E[e][lane];
-          uint32_t M = ent.x;
+        for (uint32_t it = lane; it < 3u * nrec; it += 32u) {
+          const uint32_t ri = it / 3u;
+          const uint2 rec = Fl[ri];
+          const uint32_t j = (rec.y & 0xFFFFu) + (it - 3u * ri), src = rec.y >> 16;
+          if (j >= L) continue;  // a last iteration of one or two entries
+          uint2 h, hw;
+          entry_state(j, h.x, h.y, hw.x, hw.y);
+          const uint32_t gh = pair_g2(h.x, h.y);
+          const uint32_t jp = Hj[j] & 1u;
+          const uint2 sv = SV[src];
+          uint32_t M = rec.x;
           while (M) {
-            const uint32_t bit = __ffs(M) - 1;
+            const uint32_t w = __ffs(M) - 1;
             M &= M - 1;
-            // entry and word of the pass: tag W: three entries of W words,
-            // else two of 16
-            const uint32_t tw = ent.y >> 16;
-            const uint32_t eo = tw ? (bit >= 2u * tw ? 2u : bit >= tw ? 1u : 0u) : bit >> 4;
-            const uint32_t j = (ent.y & 0xFFFFu) + eo, w = tw ? bit - eo * tw : bit & 15u;
-            TP_CHECK(j < L);
-            uint2 h, hw;
-            entry_state(j, h.x, h.y, hw.x, hw.y);
-            const uint32_t gh = pair_g2(h.x, h.y);
-            const uint32_t jp = Hj[j] & 1u;
+            TP_CHECK(w < 16u && src < 32u);
+            const uint4 a4 = A2[w][src];
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
               const uint32_t k = w + 16 * hf;
-              const uint4 a4 = A2[w][lane];
               const uint2 a = hf ? make_uint2(a4.z, a4.w) : make_uint2(a4.x, a4.y);
               uint32_t d, zp;
               TP_LOP3(d, a.x, a.y, h.y, 0x06);
               TP_LOP3(zp, d, a.x, h.x, 0x09);
-              if (zp == 0 && ((vmask >> k) & 1u)) {
+              if (zp == 0 && ((sv.y >> k) & 1u)) {
                 uint32_t par = 0;
                 if constexpr (WIDE) {
                   // the primary columns are nonzero: test the secondary ones
                   const uint32_t rr =
-                      bucket_wide_term<FIX, KEYS>(Tm, grp, pbase + 32u * lrow(k) + lane, hw, colmask1);
+                      bucket_wide_term<FIX, KEYS>(Tm, grp, pbase + 32u * lrow(k) + src, hw, colmask1);
                   if (!rr) continue;
                   par = rr >> 1;
                 }
                 bev += 1;
-                bodd += (__popc((d ^ gh) & colmask) + par + jp + ((spm >> k) & 1u)) & 1u;
+                bodd += (__popc((d ^ gh) & colmask) + par + jp + ((sv.x >> k) & 1u)) & 1u;
               }
             }
           }
@@ -684,7 +694,8 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
         ev += bev;
         odd += bodd;
         // event-dense (e.g. all-ones rows): exact mode for the next batches
-        dense = p.dense_ok != 0 && __any_sync(FULL, bev >= (uint32_t)(K / 2) * nbt);
+        // (the verify's events are spread over the lanes: the warp's total)
+        dense = p.dense_ok != 0 && __reduce_add_sync(FULL, bev) >= 4u * (uint32_t)(K / 2) * nbt;
       }
     }
     warp_flush(p.pm + 2 * b, ev - odd, odd, lane);

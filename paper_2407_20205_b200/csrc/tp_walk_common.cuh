@@ -242,6 +242,51 @@ __device__ __forceinline__ void packed_test(uint32_t z1, uint32_t g1, uint32_t z
       : "r"(z1), "r"(g1), "r"(z2), "r"(u2), "r"(one), "r"(cneg), "n"(BIT));
 }
 
+// The same test for three (two) B states against one packed A word with ONE
+// zero-field test: the halfword-wise minimum of the zp words (VIMNMX3.U16x2,
+// ptxas fuses the two min.u16x2) has a zero field iff one of them has.  Sets
+// BIT of m when any of the states passes on either half: per word and state
+// 2 LOP3 + 1/3 (VIMNMX3 + LOP3) on the ALU pipe and 2/3 IMAD on the FMA pipe,
+// against 3 LOP3 + 2 IMAD for packed_test.  The verify finds the state.
+template <uint32_t BIT>
+__device__ __forceinline__ void packed_test3(uint32_t z1, uint32_t g1, uint32_t za, uint32_t ua, uint32_t zb,
+                                             uint32_t ub, uint32_t zc, uint32_t uc, uint32_t& m, uint32_t one,
+                                             uint32_t cneg) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 da, zpa, db, zpb, dc, zpc, mn, t, h;\n\t"
+      "lop3.b32 da, %1, %2, %4, 0x06;\n\t"
+      "lop3.b32 zpa, da, %1, %3, 0x09;\n\t"
+      "lop3.b32 db, %1, %2, %6, 0x06;\n\t"
+      "lop3.b32 zpb, db, %1, %5, 0x09;\n\t"
+      "lop3.b32 dc, %1, %2, %8, 0x06;\n\t"
+      "lop3.b32 zpc, dc, %1, %7, 0x09;\n\t"
+      "min.u16x2 mn, zpa, zpb;\n\t"
+      "min.u16x2 mn, mn, zpc;\n\t"
+      "mad.lo.u32 t, mn, %9, %10;\n\t"
+      "lop3.b32 h, t, 0x80008000, mn, 0x40;\n\t"
+      "setp.ne.u32 p, h, 0;\n\t"
+      "@p mad.lo.u32 %0, %9, %11, %0;\n\t}"
+      : "+r"(m)
+      : "r"(z1), "r"(g1), "r"(za), "r"(ua), "r"(zb), "r"(ub), "r"(zc), "r"(uc), "r"(one), "r"(cneg), "n"(BIT));
+}
+template <uint32_t BIT>
+__device__ __forceinline__ void packed_test2(uint32_t z1, uint32_t g1, uint32_t za, uint32_t ua, uint32_t zb,
+                                             uint32_t ub, uint32_t& m, uint32_t one, uint32_t cneg) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 da, zpa, db, zpb, mn, t, h;\n\t"
+      "lop3.b32 da, %1, %2, %4, 0x06;\n\t"
+      "lop3.b32 zpa, da, %1, %3, 0x09;\n\t"
+      "lop3.b32 db, %1, %2, %6, 0x06;\n\t"
+      "lop3.b32 zpb, db, %1, %5, 0x09;\n\t"
+      "min.u16x2 mn, zpa, zpb;\n\t"
+      "mad.lo.u32 t, mn, %7, %8;\n\t"
+      "lop3.b32 h, t, 0x80008000, mn, 0x40;\n\t"
+      "setp.ne.u32 p, h, 0;\n\t"
+      "@p mad.lo.u32 %0, %7, %9, %0;\n\t}"
+      : "+r"(m)
+      : "r"(z1), "r"(g1), "r"(za), "r"(ua), "r"(zb), "r"(ub), "r"(one), "r"(cneg), "n"(BIT));
+}
+
 __device__ __forceinline__ uint32_t pair_u2(uint32_t z2, uint32_t g2) {
   uint32_t u;
   TP_LOP3(u, z2, g2, 0u, 0xC3);
