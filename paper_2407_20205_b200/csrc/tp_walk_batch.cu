@@ -634,12 +634,13 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
         // Verify, balanced over the lanes.  The records are compacted row
         // by row into one flat list in place (row r only lands on flat
         // positions < 32 (r + 1), all read by then), tagged with their lane;
-        // a work item is (record, entry): lane k takes items k, k + 32, ..
-        // and tests its entry against the record's words of the SOURCE
-        // lane's slots (A2, and the slots' parities SV in the list area,
-        // which the filter has finished with).
+        // lane k takes records k, k + 32, ..: it repeats the packed test of
+        // the record's words for each of the (up to) three entries against
+        // the SOURCE lane's slots (A2; the slots' parities and validity SV
+        // in the pass list's overflow row) to find the entry and half that
+        // passed, and evaluates those on all columns.
         uint2* Fl = &E[0][0];
-        uint2* SV = Hc;
+        uint2* SV = &E[ECAP][0];
         __syncwarp();
         SV[lane] = make_uint2(spm, vmask);
         uint32_t nrec = 0;
@@ -653,25 +654,38 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
         }
         __syncwarp();
         uint32_t bev = 0, bodd = 0;
-        for (uint32_t it = lane; it < 3u * nrec; it += 32u) {
-          const uint32_t ri = it / 3u;
+        for (uint32_t ri = lane; ri < nrec; ri += 32u) {
           const uint2 rec = Fl[ri];
-          const uint32_t j = (rec.y & 0xFFFFu) + (it - 3u * ri), src = rec.y >> 16;
-          if (j >= L) continue;  // a last iteration of one or two entries
-          uint2 h, hw;
-          entry_state(j, h.x, h.y, hw.x, hw.y);
-          const uint32_t gh = pair_g2(h.x, h.y);
-          const uint32_t jp = Hj[j] & 1u;
+          const uint32_t i0 = rec.y & 0xFFFFu, src = rec.y >> 16;
+          const uint32_t i1 = min(i0 + 3u, L);  // a last iteration holds one or two entries
           const uint2 sv = SV[src];
           uint32_t M = rec.x;
+          TP_CHECK(i0 < L && src < 32u && M < 0x10000u);
           while (M) {
             const uint32_t w = __ffs(M) - 1;
             M &= M - 1;
-            TP_CHECK(w < 16u && src < 32u);
             const uint4 a4 = A2[w][src];
+            const uint32_t zk = __byte_perm(a4.x, a4.z, 0x5410), gk = __byte_perm(a4.y, a4.w, 0x5410);
+            // which entries and halves passed: bit 2 e + half, branch-free
+            uint32_t hits = 0;
 #pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-              const uint32_t k = w + 16 * hf;
+            for (uint32_t e = 0; e < 3u; ++e) {
+              const uint2 hq = Hc[min(i0 + e, L - 1u)];
+              uint32_t dq, zq;
+              TP_LOP3(dq, zk, gk, hq.y, 0x06);
+              TP_LOP3(zq, dq, zk, hq.x, 0x09);
+              const uint32_t hit = (zq - 0x00010001u) & ~zq & 0x80008000u;  // bit 15 / 31: half 0 / 1
+              const uint32_t two = ((hit >> 15) & 1u) | (hit >> 30);
+              hits |= (i0 + e < i1 ? two : 0u) << (2u * e);
+            }
+            while (hits) {
+              const uint32_t bq = __ffs(hits) - 1;
+              hits &= hits - 1;
+              const uint32_t j = i0 + (bq >> 1), hf = bq & 1u;
+              TP_CHECK(j < L);
+              uint2 h, hw;
+              entry_state(j, h.x, h.y, hw.x, hw.y);
+              const uint32_t k = w + 16u * hf;
               const uint2 a = hf ? make_uint2(a4.z, a4.w) : make_uint2(a4.x, a4.y);
               uint32_t d, zp;
               TP_LOP3(d, a.x, a.y, h.y, 0x06);
@@ -686,7 +700,7 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
                   par = rr >> 1;
                 }
                 bev += 1;
-                bodd += (__popc((d ^ gh) & colmask) + par + jp + ((sv.x >> k) & 1u)) & 1u;
+                bodd += (__popc((d ^ pair_g2(h.x, h.y)) & colmask) + par + (Hj[j] & 1u) + ((sv.x >> k) & 1u)) & 1u;
               }
             }
           }
