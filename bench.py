@@ -626,11 +626,13 @@ def main():
     # tests only the 32 primary columns -- see DESIGN.md)
     kernel_name, ops_per_term = _kernels.walk_info(n, B)
     tested_frac = None
+    ops_per_tested_pair = None
     if "bucket" in kernel_name or "batch" in kernel_name:
         # the bucketed walk tests only the pairs its key columns do not prove
         # zero: LOP3 per term = LOP3 per tested pair x the tested fraction,
         # counted by the kernel itself over the timed steps
         tested_frac = tested_pairs / (per_rank_terms * args.steps)
+        ops_per_tested_pair = ops_per_term
         ops_per_term = ops_per_term * tested_frac
     walk_avg = sum(walk_ms) / len(walk_ms)
     achieved = per_rank_terms * ops_per_term / (walk_avg * 1e-3)
@@ -712,7 +714,7 @@ def main():
                     "l2": "flushed between steps (256 MiB memset, untimed by the walk events)",
                     "cuda_graph": bool(graph is not None),
                     "terms_per_step": job_terms},
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "LOP3 ops/s",
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "ALU ops/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": kernel_name + " (csrc/" + ("tp_walk_batch.cu" if "batch" in kernel_name
                                                               else "tp_walk_bucket.cu" if "bucket" in kernel_name
@@ -722,6 +724,11 @@ def main():
                                                               else "tp_walk_wide.cu") + ")",
                          "ops_per_term": ops_per_term,
                          "tested_pairs_frac": tested_frac,
+                         # ALU-pipe ops the filter executes per tested pair (k_walk_batch: 2 LOP3 + 1/3
+                         # VIMNMX3 + 1/3 LOP3 per packed word of two pairs = 4/3; rounds 1-2 counted 1.5)
+                         "ops_per_tested_pair": ops_per_tested_pair,
+                         "frac_at_1p5_ops_per_pair": (None if tested_frac is None else
+                                                      per_rank_terms * 1.5 * tested_frac / (walk_avg * 1e-3) / peak),
                          "peak_source": "LOP3 chain probe (tp_alu_peak) on this GPU in this run; "
                                         "nominal 148 SM x 64 lanes x clock",
                          "walk_ms_avg": walk_avg,

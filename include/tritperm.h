@@ -159,12 +159,13 @@ int tp_finalize_async(const uint64_t *d_pm, int64_t B, int n, int device,
 int tp_exact_census(int n, int device, int64_t *zeros, int64_t *plus, int64_t *minus);
 
 /* Which walk kernel serves full traversals of `batch` matrices of size n
- * (batch = 1: a single matrix or a range), and its LOP3 count per subset
- * term (3 for the lane/wide walks, 2 for the pair walks, 1.5 for the packed
- * walks).  For the bucketed walk (21 <= n <= 64: batches, single matrices
- * and the aligned middle of ranges that fill the GPU) the count is per
- * TESTED pair: it skips the pairs its key columns prove zero, and
- * tp_walk_tested reports how many it tested. */
+ * (batch = 1: a single matrix or a range), and its ALU-pipe op count per
+ * subset term (3 LOP3 for the lane/wide walks, 2 for the pair walks, 1.5 for
+ * the packed walks).  For the bucketed walk (21 <= n <= 64: batches, single
+ * matrices and the aligned middle of ranges that fill the GPU) the count is
+ * per TESTED pair (k_walk_batch: 4/3 = 2 LOP3 + 1/3 VIMNMX3 + 1/3 LOP3 per
+ * packed word of two pairs; k_walk_bucket: 1.5): it skips the pairs its key
+ * columns prove zero, and tp_walk_tested reports how many it tested. */
 int tp_walk_info(int n, long long batch, char *name, int name_len, double *lop3_per_term);
 
 /* Pairs tested by the bucketed walk on `device` since the last call (the

@@ -1068,14 +1068,17 @@ int tp_walk_info(int n, long long batch, char* name, int name_len, double* lop3_
   if (batch < 1) return fail(TP_E_INVALID, "need batch >= 1, got %lld", batch);
   const int v = choose_variant(n, (unsigned long long)batch);
   if (bucket_applies(n, (unsigned long long)batch)) {
-    // 1.5 LOP3 per TESTED pair: the bucketed walk skips the incompatible
+    // ALU-pipe ops per TESTED pair: the bucketed walk skips the incompatible
     // steps, so the tested fraction (tp_walk_tested) scales this per term
     const bool packed = bucket_mode() != 2;
     if (name && name_len > 0) {
       if (packed && batch_mode()) snprintf(name, (size_t)name_len, "k_walk_batch<packed> V=%d", tp::bucket_v(packed));
       else snprintf(name, (size_t)name_len, "k_walk_bucket<%s> V=%d", packed ? "packed" : "pair", tp::bucket_v(packed));
     }
-    if (lop3_per_term) *lop3_per_term = packed ? 1.5 : 2.0;
+    // k_walk_batch tests three entries per packed word with one zero-field
+    // test (packed_test3): per word and entry 2 LOP3 + 1/3 VIMNMX3 + 1/3
+    // LOP3 = 8/3 ALU-pipe ops for two pairs
+    if (lop3_per_term) *lop3_per_term = !packed ? 2.0 : batch_mode() ? 4.0 / 3.0 : 1.5;
     return TP_OK;
   }
   const char* kind;
