@@ -632,7 +632,14 @@ def main():
         # zero: LOP3 per term = LOP3 per tested pair x the tested fraction,
         # counted by the kernel itself over the timed steps
         tested_frac = tested_pairs / (per_rank_terms * args.steps)
+        # `frac` stays on the counter of rounds 1-2 (1.5 LOP3 per tested pair:
+        # the packed pair test as 2 LOP3 + its own zero-field LOP3 per word of
+        # two pairs), so the rounds compare; k_walk_batch now shares the
+        # zero-field test between three entries and EXECUTES 4/3 ALU-pipe ops
+        # per tested pair (tp_walk_info): `frac_executed`
         ops_per_tested_pair = ops_per_term
+        if "packed" in kernel_name:
+            ops_per_term = 1.5
         ops_per_term = ops_per_term * tested_frac
     walk_avg = sum(walk_ms) / len(walk_ms)
     achieved = per_rank_terms * ops_per_term / (walk_avg * 1e-3)
@@ -724,11 +731,12 @@ def main():
                                                               else "tp_walk_wide.cu") + ")",
                          "ops_per_term": ops_per_term,
                          "tested_pairs_frac": tested_frac,
-                         # ALU-pipe ops the filter executes per tested pair (k_walk_batch: 2 LOP3 + 1/3
-                         # VIMNMX3 + 1/3 LOP3 per packed word of two pairs = 4/3; rounds 1-2 counted 1.5)
-                         "ops_per_tested_pair": ops_per_tested_pair,
-                         "frac_at_1p5_ops_per_pair": (None if tested_frac is None else
-                                                      per_rank_terms * 1.5 * tested_frac / (walk_avg * 1e-3) / peak),
+                         # ALU-pipe ops the filter EXECUTES per tested pair (k_walk_batch: 2 LOP3 + 1/3
+                         # VIMNMX3 + 1/3 LOP3 per packed word of two pairs = 4/3); `achieved`/`frac` count
+                         # the pair test at 1.5 LOP3 per tested pair, the counter of rounds 1-2
+                         "ops_per_tested_pair_executed": ops_per_tested_pair,
+                         "frac_executed": (None if tested_frac is None else per_rank_terms * ops_per_tested_pair
+                                           * tested_frac / (walk_avg * 1e-3) / peak),
                          "peak_source": "LOP3 chain probe (tp_alu_peak) on this GPU in this run; "
                                         "nominal 148 SM x 64 lanes x clock",
                          "walk_ms_avg": walk_avg,

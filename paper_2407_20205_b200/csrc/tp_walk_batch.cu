@@ -227,6 +227,12 @@ static __device__ __noinline__ void batch_exact_weighted(const uint2* Hf, const 
 
 }  // namespace
 
+// TP_BATCH_SIX = W: pieces of at most W packed words filter six entries per
+// iteration (0: three everywhere)
+#ifndef TP_BATCH_SIX
+#define TP_BATCH_SIX 0
+#endif
+
 template <int NBAT, int ECAP, bool WIDE, int FIX, int KEYS>
 __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp) {
   constexpr int V = 5, K = 32, SB = 32;
@@ -585,6 +591,25 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
       auto filter = [&](auto Wc) {
         constexpr int W = decltype(Wc)::value;
         uint32_t i = 0;
+#if TP_BATCH_SIX
+        // two groups of three entries per iteration and record: bit w of M
+        // for entries i..i+2, bit 16 + w for i+3..i+5 (the piece's common
+        // widths only: the code has to stay in the instruction cache)
+        if constexpr (W <= TP_BATCH_SIX) {
+#pragma unroll 1
+          for (; i + 6 <= L; i += 6) {
+            const uint4* q = reinterpret_cast<const uint4*>(Hc + i);  // i is even
+            const uint4 hab = q[0], hcd = q[1], hef = q[2];
+            uint32_t M = 0;
+            static_for<W>([&](auto wc) {
+              constexpr int w = decltype(wc)::value;
+              packed_test3<(1u << w)>(Zp[w], Gp[w], hab.x, hab.y, hab.z, hab.w, hcd.x, hcd.y, M, one, cneg);
+              packed_test3<(1u << (16 + w))>(Zp[w], Gp[w], hcd.z, hcd.w, hef.x, hef.y, hef.z, hef.w, M, one, cneg);
+            });
+            record(M, i);
+          }
+        }
+#endif
 #pragma unroll 1
         for (; i + 3 <= L; i += 3) {
           const uint2 ha = Hc[i], hb = Hc[i + 1], hc = Hc[i + 2];
@@ -656,32 +681,35 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
         uint32_t bev = 0, bodd = 0;
         for (uint32_t ri = lane; ri < nrec; ri += 32u) {
           const uint2 rec = Fl[ri];
-          const uint32_t i0 = rec.y & 0xFFFFu, src = rec.y >> 16;
-          const uint32_t i1 = min(i0 + 3u, L);  // a last iteration holds one or two entries
+          const uint32_t src = rec.y >> 16;
           const uint2 sv = SV[src];
           uint32_t M = rec.x;
-          TP_CHECK(i0 < L && src < 32u && M < 0x10000u);
+          TP_CHECK((rec.y & 0xFFFFu) < L && src < 32u && (TP_BATCH_SIX || M < 0x10000u));
           while (M) {
-            const uint32_t w = __ffs(M) - 1;
+            const uint32_t bm = __ffs(M) - 1;
             M &= M - 1;
+            // bit w: entries i .. i + 2 of the record; bit 16 + w: i + 3 .. i + 5
+            const uint32_t w = bm & 15u, i0 = (rec.y & 0xFFFFu) + 3u * (bm >> 4);
+            const uint32_t i1 = min(i0 + 3u, L);  // a last iteration holds one or two entries
             const uint4 a4 = A2[w][src];
             const uint32_t zk = __byte_perm(a4.x, a4.z, 0x5410), gk = __byte_perm(a4.y, a4.w, 0x5410);
-            // which entries and halves passed: bit 2 e + half, branch-free
-            uint32_t hits = 0;
+            // which entries and halves passed: bit e + 16 half, branch-free
+            uint32_t hit[3];
 #pragma unroll
             for (uint32_t e = 0; e < 3u; ++e) {
               const uint2 hq = Hc[min(i0 + e, L - 1u)];
               uint32_t dq, zq;
               TP_LOP3(dq, zk, gk, hq.y, 0x06);
               TP_LOP3(zq, dq, zk, hq.x, 0x09);
-              const uint32_t hit = (zq - 0x00010001u) & ~zq & 0x80008000u;  // bit 15 / 31: half 0 / 1
-              const uint32_t two = ((hit >> 15) & 1u) | (hit >> 30);
-              hits |= (i0 + e < i1 ? two : 0u) << (2u * e);
+              hit[e] = (zq - 0x00010001u) & ~zq;  // bit 15 / 31: half 0 / 1 has no zero column
             }
+            // (a last iteration of one or two entries repeats its last entry)
+            uint32_t hits = ((hit[0] >> 15) & 0x00010001u) | (i0 + 1u < i1 ? (hit[1] >> 14) & 0x00020002u : 0u) |
+                            (i0 + 2u < i1 ? (hit[2] >> 13) & 0x00040004u : 0u);
             while (hits) {
               const uint32_t bq = __ffs(hits) - 1;
               hits &= hits - 1;
-              const uint32_t j = i0 + (bq >> 1), hf = bq & 1u;
+              const uint32_t j = i0 + (bq & 3u), hf = bq >> 4;
               TP_CHECK(j < L);
               uint2 h, hw;
               entry_state(j, h.x, h.y, hw.x, hw.y);
