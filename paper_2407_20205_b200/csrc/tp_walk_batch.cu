@@ -228,9 +228,11 @@ static __device__ __noinline__ void batch_exact_weighted(const uint2* Hf, const 
 }  // namespace
 
 // TP_BATCH_SIX = W: pieces of at most W packed words filter six entries per
-// iteration (0: three everywhere)
+// iteration and pass record (0: three everywhere).  Measured on B200: C2
+// -0.9 %, C4 -0.9 %, C5 -0.3 %, but C3 (n <= 32, 17 rows / 5 keys) +3.5 %, so
+// that kernel keeps three.
 #ifndef TP_BATCH_SIX
-#define TP_BATCH_SIX 0
+#define TP_BATCH_SIX 10
 #endif
 
 template <int NBAT, int ECAP, bool WIDE, int FIX, int KEYS>
@@ -595,7 +597,7 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
         // two groups of three entries per iteration and record: bit w of M
         // for entries i..i+2, bit 16 + w for i+3..i+5 (the piece's common
         // widths only: the code has to stay in the instruction cache)
-        if constexpr (W <= TP_BATCH_SIX) {
+        if constexpr (W <= TP_BATCH_SIX && (FIX == 14 || WIDE)) {
 #pragma unroll 1
           for (; i + 6 <= L; i += 6) {
             const uint4* q = reinterpret_cast<const uint4*>(Hc + i);  // i is even
