@@ -275,3 +275,56 @@ def test_walk_options_agree(gpu, oracle, monkeypatch):
         assert _kernels.walk_tested(0) > 0, env  # the bucketed walks ran
         for k in env:
             monkeypatch.delenv(k)
+
+
+def test_filter_list_lengths_and_dense_passes(gpu, oracle):
+    """The batched walk's filter takes its list six, three, two or one entries
+    at a time, and its pass records are compacted and verified across the
+    lanes.  Inputs that push both to their edges, raw partials against the C
+    oracle: B-side rows with no entry on the key columns (every state of a
+    superblock has the same key trits: lists of 0 or all 128 steps), with
+    few entries there (ragged list lengths), filter-heavy rows (the low 16
+    columns all ones: the pass lists fill and overflow into the exact path)
+    and sparse rows (short pieces, many passes per record); n = 24 (14-row A
+    side, six-entry loop), n = 29 (17 rows, three-entry loop) in full, and
+    n = 36 windows (wide kernel)."""
+    from paper_2407_20205_b200 import _kernels
+
+    r = np.random.default_rng(2407)
+
+    def family(n, fix, count):
+        out = []
+        for v in range(count):
+            a = r.integers(0, 3, (n, n)).astype(np.uint8)
+            keys = slice(0, 5)  # the key columns are the leading columns of the (primary) word
+            if v % 4 == 0:
+                a[fix:, keys] = 0
+            elif v % 4 == 1:
+                a[fix:, keys] = 0
+                a[fix + (v // 4) % (n - fix), 0] = 1 + v % 2
+            elif v % 4 == 2:
+                a[:, n - 16:] = 1
+                a[fix:, keys] = (r.random((n - fix, 5)) < 0.3) * r.integers(1, 3, (n - fix, 5))
+            else:
+                a = ((r.random((n, n)) < 0.25) * r.integers(1, 3, (n, n))).astype(np.uint8)
+            out.append(a)
+        return np.stack(out)
+
+    for n, fix, count in ((24, 14, 16), (29, 17, 4)):
+        e = family(n, fix, count)
+        _kernels.walk_tested(0)
+        _, part, _ = gpu.perm_mod3_batch(e)
+        assert _kernels.walk_tested(0) > 0, n
+        assert np.array_equal(part, _oracle_partials(oracle, e)), n
+    # n = 36: 2^28-step windows of each matrix (the bucketed walk takes the aligned middle)
+    n = 36
+    e = family(n, 17, 8)
+    for k, a in enumerate(e):
+        m = gpu.MatrixF3(centred(a))
+        mags, sgns = oracle.planes_from_classes(a)
+        lo = (1 << 33) + (k << 29) + 1000 * k
+        hi = lo + (1 << 28) + 77
+        _kernels.walk_tested(0)
+        got = gpu.perm_chunk(m, lo, hi).partial_sum
+        assert _kernels.walk_tested(0) > 0, k
+        assert got == oracle.chunk_sum_mt(mags, sgns, n, lo, hi, 8), k
