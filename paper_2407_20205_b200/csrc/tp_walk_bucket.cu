@@ -93,6 +93,53 @@ __global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n,
   const uint32_t cm1 = n <= 32 ? 0u : n >= 64 ? 0xffffffffu : (1u << (n - 32)) - 1u;
   uint32_t key[EPT], rank[EPT], wt[EPT];
   uint4 vec[EPT];
+  // Forced rows (packed variants).  A column with a single nonzero entry, in
+  // row r, is zero in every subset sum without row r, so only subsets
+  // containing r give terms: A-side subsets without a forced row of their
+  // half stay out of the table.  A column without any nonzero entry makes
+  // every term zero: the table stays empty (all pieces count 0) and the
+  // matrix's counters stay 0.  Only zero terms are dropped, so the raw
+  // partials are unchanged.  (Permutation-like and very sparse matrices;
+  // uniform inputs have no such columns.)
+  __shared__ uint32_t forcedA;  // forced rows among 0..FIX-1
+  __shared__ int deadm;         // a zero column
+  if (warp == 0) {
+    uint32_t fa = 0;
+    int dd = 0;
+    if (DEDUP) {
+      const RowRec* rr = rows + (size_t)blockIdx.x * 64;
+      uint32_t o0 = 0, m0 = 0, o1 = 0, m1 = 0;  // columns seen in a row / in more than one row
+      uint32_t own0 = 0, own1 = 0;              // this lane's row r = lane
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int r = (int)lane + 32 * k;
+        const uint32_t a0 = r < n ? rr[r].m[0] & cm0 : 0u, a1 = r < n ? rr[r].m[1] & cm1 : 0u;
+        if (k == 0) {
+          own0 = a0;
+          own1 = a1;
+        }
+        m0 |= o0 & a0;
+        o0 |= a0;
+        m1 |= o1 & a1;
+        o1 |= a1;
+      }
+#pragma unroll
+      for (int sft = 16; sft; sft >>= 1) {
+        const uint32_t po0 = __shfl_xor_sync(FULL, o0, sft), pm0 = __shfl_xor_sync(FULL, m0, sft);
+        const uint32_t po1 = __shfl_xor_sync(FULL, o1, sft), pm1 = __shfl_xor_sync(FULL, m1, sft);
+        m0 |= pm0 | (o0 & po0);
+        o0 |= po0;
+        m1 |= pm1 | (o1 & po1);
+        o1 |= po1;
+      }
+      dd = ((~o0 & cm0) | (~o1 & cm1)) != 0u;
+      fa = __ballot_sync(FULL, ((own0 & o0 & ~m0) | (own1 & o1 & ~m1)) != 0u) & ((1u << FIX) - 1u);
+    }
+    if (lane == 0) {
+      forcedA = fa;
+      deadm = dd;
+    }
+  }
   __syncthreads();
   if (tid < 2) dep[tid] = DEDUP && !f3_rows_independent(R, tid ? T::TB : 0, tid ? T::HB : T::TB);
 #pragma unroll
@@ -113,7 +160,8 @@ __global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n,
     uint32_t pat = 0;  // first key column most significant
 #pragma unroll
     for (int i = 0; i < KEYS; ++i) pat = 3u * pat + trit(k1 - i);
-    key[q] = act ? h * NB + pat : 0xFFFFu;
+    const uint32_t fh = h ? forcedA >> T::TB : forcedA & ((1u << T::TB) - 1u);
+    key[q] = act && !deadm && (sub & fh) == fh ? h * NB + pat : 0xFFFFu;
     wt[q] = (__popc(sub) & 1) ? 1u << 16 : 1u;
     // canonical sign bits (zero columns carry sgn 0) so equal vectors compare equal
     g0 &= ~z0;

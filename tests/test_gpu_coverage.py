@@ -285,9 +285,11 @@ def test_filter_list_lengths_and_dense_passes(gpu, oracle):
     superblock has the same key trits: lists of 0 or all 128 steps), with
     few entries there (ragged list lengths), filter-heavy rows (the low 16
     columns all ones: the pass lists fill and overflow into the exact path)
-    and sparse rows (short pieces, many passes per record); n = 24 (14-row A
-    side, six-entry loop), n = 29 (17 rows, three-entry loop) in full, and
-    n = 36 windows (wide kernel)."""
+    and sparse rows (short pieces, many passes per record); and the group
+    kernel's forced rows: columns with a single nonzero entry (subsets
+    without that row stay out of the tables), zero columns (empty tables),
+    permutation-like matrices.  n = 24 (14-row A side, six-entry loop), n = 29
+    (17 rows, three-entry loop) in full, and n = 36 windows (wide kernel)."""
     from paper_2407_20205_b200 import _kernels
 
     r = np.random.default_rng(2407)
@@ -297,7 +299,17 @@ def test_filter_list_lengths_and_dense_passes(gpu, oracle):
         for v in range(count):
             a = r.integers(0, 3, (n, n)).astype(np.uint8)
             keys = slice(0, 5)  # the key columns are the leading columns of the (primary) word
-            if v % 4 == 0:
+            if v % 8 == 4:  # forced rows: columns with a single nonzero entry (A side, B side), or none
+                for c, row in ((7, 2), (9, fix + 1), (12, n - 1)):
+                    a[:, c] = 0
+                    a[row, c] = 1 + (v // 8 + c) % 2
+                if v % 16 == 12:
+                    a[:, 11] = 0
+            elif v % 8 == 5:  # a permutation matrix with a few extra entries
+                a[:] = 0
+                a[np.arange(n), r.permutation(n)] = r.integers(1, 3, n)
+                a[r.integers(0, n, 3), r.integers(0, n, 3)] = 1
+            elif v % 4 == 0:
                 a[fix:, keys] = 0
             elif v % 4 == 1:
                 a[fix:, keys] = 0
@@ -310,7 +322,7 @@ def test_filter_list_lengths_and_dense_passes(gpu, oracle):
             out.append(a)
         return np.stack(out)
 
-    for n, fix, count in ((24, 14, 16), (29, 17, 4)):
+    for n, fix, count in ((24, 14, 16), (29, 17, 6)):
         e = family(n, fix, count)
         _kernels.walk_tested(0)
         _, part, _ = gpu.perm_mod3_batch(e)
@@ -318,7 +330,7 @@ def test_filter_list_lengths_and_dense_passes(gpu, oracle):
         assert np.array_equal(part, _oracle_partials(oracle, e)), n
     # n = 36: 2^28-step windows of each matrix (the bucketed walk takes the aligned middle)
     n = 36
-    e = family(n, 17, 8)
+    e = family(n, 17, 14)
     for k, a in enumerate(e):
         m = gpu.MatrixF3(centred(a))
         mags, sgns = oracle.planes_from_classes(a)
@@ -326,5 +338,6 @@ def test_filter_list_lengths_and_dense_passes(gpu, oracle):
         hi = lo + (1 << 28) + 77
         _kernels.walk_tested(0)
         got = gpu.perm_chunk(m, lo, hi).partial_sum
-        assert _kernels.walk_tested(0) > 0, k
+        # (a zero column or forced rows can leave the tables without a pair to test)
+        assert _kernels.walk_tested(0) > 0 or k % 8 in (4, 5), k
         assert got == oracle.chunk_sum_mt(mags, sgns, n, lo, hi, 8), k
