@@ -341,3 +341,27 @@ def test_filter_list_lengths_and_dense_passes(gpu, oracle):
         # (a zero column or forced rows can leave the tables without a pair to test)
         assert _kernels.walk_tested(0) > 0 or k % 8 in (4, 5), k
         assert got == oracle.chunk_sum_mt(mags, sgns, n, lo, hi, 8), k
+
+
+def test_table4_tool_small_scale(gpu):
+    """tools/table4.py (the paper's Monte Carlo table through montecarlo_zero)
+    at 10^-6 of the paper's trial counts: every n = 6..30 runs, the records
+    carry the paper's tallies, and the n = 6 frequency sits at the calibration
+    value 0.3546 (tests/test_acceptance.py:143-158)."""
+    import json
+    import subprocess
+    import sys
+
+    from conftest import REPO
+
+    out = subprocess.run([sys.executable, os.path.join(REPO, "tools", "table4.py"), "--scale", "1e-6"],
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    recs = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
+    rows = {r["n"]: r for r in recs if "n" in r}
+    assert sorted(rows) == list(range(6, 31))
+    assert rows[6]["trials"] == 100000 and abs(rows[6]["zero_fraction"] - 0.35456) < 0.01
+    assert rows[24]["paper_zero_count"] == 3333518 and rows[30]["trials"] == 1
+    # the same call through the API gives the same tally (seed 0)
+    assert rows[10]["zero_count"] == gpu.montecarlo_zero(10, rows[10]["trials"], seed=0).zero_count
+    assert "summary" in recs[-1]
