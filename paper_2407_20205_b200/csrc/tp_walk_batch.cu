@@ -43,6 +43,10 @@ namespace {
 template <int NBAT, int ECAP, bool WIDE, int FIX>
 struct BatchSmem {
   static constexpr int NR = (WIDE ? 64 : 32) - FIX;  // B-side rows FIX..n-1
+  // the list keeps only what the filter reads; the entries' full states are
+  // recomputed from the superblock's H and the lane's L (n > 32, and
+  // batches of 8 superblocks, whose lists leave no room for them)
+  static constexpr bool RECOMP = WIDE || NBAT > 4;
   static constexpr int NS = NBAT * 32;               // list capacity: steps per batch
   static constexpr int oR = 0;                          // RowRec[NR]: row r at r - FIX
   static constexpr int oA = align16(oR + 32 * NR);      // uint4[16][32]: full A words (slot w | slot w + 16)
@@ -51,8 +55,8 @@ struct BatchSmem {
   // n <= 32: uint2[NS] the entries' full states (z, u); n > 32 recomputes
   // them from Hs and the L tables (entry_state) and keeps the room for a
   // batch of 4 superblocks
-  static constexpr int oHf = oHs + (WIDE ? 16 * NBAT : 0);
-  static constexpr int oHj = oHf + (WIDE ? 0 : 8 * NS);  // uint8[NS]: step within the batch (32 t + lane)
+  static constexpr int oHf = oHs + (RECOMP ? 16 * NBAT : 0);
+  static constexpr int oHj = oHf + (RECOMP ? 0 : 8 * NS);  // uint8[NS]: step within the batch (32 t + lane)
   static constexpr int oE = align16(oHj + NS);          // uint2[ECAP + 1][32]: passes (mask, list index)
   // per lane the low-row part of its B state in row form, for superblocks
   // of even / odd index: uint2 (m, s) [2][32], n > 32 uint4 (m0, s0, m1, s1)
@@ -60,7 +64,7 @@ struct BatchSmem {
   static constexpr int kWarp = align16(oL + 2 * 32 * (WIDE ? 16 : 8));
   // n > 32: the exact paths materialise the entries' full states (Hf, H1)
   // in the pass-list area, which they do not use
-  __host__ __device__ static constexpr bool states_fit() { return !WIDE || 16 * NS <= oL - oE; }
+  __host__ __device__ static constexpr bool states_fit() { return !RECOMP || (WIDE ? 16 : 8) * NS <= oL - oE; }
   // the A decode's run table (run_table) borrows [oHc, kWarp): the lists,
   // the pass list and the L tables are all written after the decode
   template <int KEYS>
@@ -254,7 +258,8 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
   uint4* Hs = reinterpret_cast<uint4*>(ws + S::oHs);
   // the entries' full states: stored (n <= 32) or materialised for the
   // exact paths in the pass-list area (n > 32)
-  uint2* Hf = reinterpret_cast<uint2*>(ws + (WIDE ? S::oE : S::oHf));
+  constexpr bool RECOMP = S::RECOMP;
+  uint2* Hf = reinterpret_cast<uint2*>(ws + (RECOMP ? S::oE : S::oHf));
   uint2* H1 = reinterpret_cast<uint2*>(ws + S::oE + 8 * S::NS);
   uint8_t* Hj = ws + S::oHj;
   uint2 (*E)[32] = reinterpret_cast<uint2 (*)[32]>(ws + S::oE);
@@ -454,7 +459,7 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
       // (L in row form: add = sub of the negated row, sign m ^ s), its
       // compatibility, and the compacted list entry
       auto superblock = [&](uint32_t t, uint32_t gp) {
-        if (WIDE && lane == 0) Hs[t] = make_uint4(zh, uh, zhw, uhw);
+        if (RECOMP && lane == 0) Hs[t] = make_uint4(zh, uh, zhw, uhw);
         uint32_t zj = zh, uj = uh, zjw = zhw, ujw = uhw;
         if constexpr (WIDE) {
           const uint4 l = L4[32 * gp + lane];
@@ -471,7 +476,7 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
           const uint32_t pos = L + __popc(cmask & lanemask_lt);
           TP_CHECK(pos < (uint32_t)S::NS);
           Hc[pos] = make_uint2(__byte_perm(zj, zj, 0x1010), __byte_perm(uj, uj, 0x1010));
-          if (!WIDE) Hf[pos] = make_uint2(zj, uj);
+          if (!RECOMP) Hf[pos] = make_uint2(zj, uj);
           Hj[pos] = (uint8_t)(32u * t + lane);
         }
         L += __popc(cmask);
@@ -522,7 +527,7 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
       // the full state of list entry j (step 32 t + l of the batch): H of
       // superblock t plus L[parity][l], as in the compaction
       auto entry_state = [&](uint32_t j, uint32_t& z, uint32_t& u, uint32_t& zw, uint32_t& uw) {
-        if constexpr (!WIDE) {
+        if constexpr (!RECOMP) {
           const uint2 h = Hf[j];
           z = h.x;
           u = h.y;
@@ -547,7 +552,7 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
       // the exact paths read every entry's state: materialise them (Hf, H1)
       // in the pass-list area
       auto materialise = [&]() {
-        if constexpr (!WIDE) return;
+        if constexpr (!RECOMP) return;
         __syncwarp();
         for (uint32_t e = lane; e < L; e += 32) {
           uint32_t z, u, zw = 0, uw = 0;
@@ -757,23 +762,27 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
 
 // Batch shapes: NBAT superblocks per list, ECAP pass-list entries per lane.
 // Sized so that four 4-warp blocks fit an SM (228 KB of shared memory).
-template <bool WIDE>
+template <bool WIDE, int FIX>
 struct BatchShape {
 #ifndef TP_BATCH_NB_NARROW
 #define TP_BATCH_NB_NARROW 4
 #define TP_BATCH_EC_NARROW 10
 #endif
-  static constexpr int NBAT = WIDE ? 4 : TP_BATCH_NB_NARROW;
-  static constexpr int ECAP = WIDE ? 8 : TP_BATCH_EC_NARROW;
+// the 17-row A side for n <= 32 (28 <= n <= 32; C3)
+#ifndef TP_BATCH_NB17
+#define TP_BATCH_NB17 4
+#define TP_BATCH_EC17 10
+#endif
+  static constexpr int NBAT = WIDE ? 4 : FIX == 17 ? TP_BATCH_NB17 : TP_BATCH_NB_NARROW;
+  static constexpr int ECAP = WIDE ? 8 : FIX == 17 ? TP_BATCH_EC17 : TP_BATCH_EC_NARROW;
   // four blocks per SM: 228 KB of shared memory, 1 KB reserved per block
-  // (the smallest A side in use: 14 rows for n <= 32, 17 for n > 32)
-  static_assert(4 * (4 * BatchSmem<NBAT, ECAP, WIDE, WIDE ? 17 : 14>::kWarp + 1024) <= 228 * 1024,
+  static_assert(4 * (4 * BatchSmem<NBAT, ECAP, WIDE, FIX>::kWarp + 1024) <= 228 * 1024,
                 "k_walk_batch: four blocks must fit an SM");
 };
 
 template <bool WIDE, int FIX, int KEYS>
 static cudaError_t launch_batch_k(int grid, const BucketParamsCfg& bc, cudaStream_t st) {
-  using Sh = BatchShape<WIDE>;
+  using Sh = BatchShape<WIDE, FIX>;
   constexpr int bytes = 4 * BatchSmem<Sh::NBAT, Sh::ECAP, WIDE, FIX>::kWarp;
   auto* k = &k_walk_batch<Sh::NBAT, Sh::ECAP, WIDE, FIX, KEYS>;
   static const cudaError_t attr = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
@@ -794,7 +803,7 @@ cudaError_t launch_walk_batch(int grid, const BucketParams& bp, BucketCfg c, cud
 // blocks of the batched walk resident per SM (the plan sizes its grid with it)
 template <bool WIDE, int FIX, int KEYS>
 static int batch_occupancy() {
-  using Sh = BatchShape<WIDE>;
+  using Sh = BatchShape<WIDE, FIX>;
   constexpr int bytes = 4 * BatchSmem<Sh::NBAT, Sh::ECAP, WIDE, FIX>::kWarp;
   auto* k = &k_walk_batch<Sh::NBAT, Sh::ECAP, WIDE, FIX, KEYS>;
   int nb = 0;
