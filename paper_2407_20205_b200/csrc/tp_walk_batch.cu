@@ -48,8 +48,11 @@ struct BatchSmem {
   // batches of 8 superblocks, whose lists leave no room for them)
   static constexpr bool RECOMP = WIDE || NBAT > 4;
   static constexpr int NS = NBAT * 32;               // list capacity: steps per batch
-  static constexpr int oR = 0;                          // RowRec[NR]: row r at r - FIX
-  static constexpr int oA = align16(oR + 32 * NR);      // uint4[16][32]: full A words (slot w | slot w + 16)
+  // B-side rows, row r at r - FIX: RowRec[NR] (32 bytes), n > 32 uint4 (m0, m1, s0, s1) with a = m ^ s
+  // derived at use, which makes room for longer lists
+  static constexpr int kRow = WIDE ? 16 : 32;
+  static constexpr int oR = 0;
+  static constexpr int oA = align16(oR + kRow * NR);    // uint4[16][32]: full A words (slot w | slot w + 16)
   static constexpr int oHc = oA + 16 * 32 * 16;         // uint2[NS]: doubled low 16 columns (zz, uu)
   static constexpr int oHs = oHc + 8 * NS;              // n > 32: uint4[NBAT] H of each superblock (z, u, zw, uw)
   // n <= 32: uint2[NS] the entries' full states (z, u); n > 32 recomputes
@@ -64,7 +67,7 @@ struct BatchSmem {
   static constexpr int kWarp = align16(oL + 2 * 32 * (WIDE ? 16 : 8));
   // n > 32: the exact paths materialise the entries' full states (Hf, H1)
   // in the pass-list area, which they do not use
-  __host__ __device__ static constexpr bool states_fit() { return !RECOMP || (WIDE ? 16 : 8) * NS <= oL - oE; }
+  __host__ __device__ static constexpr bool states_fit() { return !RECOMP || (WIDE ? 16 : 8) * 64 <= oL - oE; }
   // the A decode's run table (run_table) borrows [oHc, kWarp): the lists,
   // the pass list and the L tables are all written after the decode
   template <int KEYS>
@@ -246,12 +249,24 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
   using T = Tab<FIX, KEYS, WIDE>;
   using S = BatchSmem<NBAT, ECAP, WIDE, FIX>;
   static_assert(S::template run_table_fits<KEYS>(), "k_walk_batch: the run table must fit the list area");
-  static_assert(S::states_fit(), "k_walk_batch: the exact paths' states must fit the pass-list area");
+  static_assert(S::states_fit(), "k_walk_batch: the exact paths need room for 64 entries' states in the pass-list area");
   const FastParams& p = bp.fp;
   extern __shared__ __align__(16) uint8_t batch_smem[];
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   uint8_t* ws = batch_smem + warp * S::kWarp;
-  RowRec* R = reinterpret_cast<RowRec*>(ws + S::oR);  // row r at R[r - FIX]
+  // B-side row r at index r - FIX, as the walk consumes it (a = m ^ s: the add operand)
+  struct BRow {
+    uint32_t m0, s0, a0, m1, s1, a1;
+  };
+  auto brow = [&](int i) -> BRow {
+    if constexpr (WIDE) {
+      const uint4 v = reinterpret_cast<const uint4*>(ws + S::oR)[i];
+      return BRow{v.x, v.z, v.x ^ v.z, v.y, v.w, v.y ^ v.w};
+    } else {
+      const RowRec& r = reinterpret_cast<const RowRec*>(ws + S::oR)[i];
+      return BRow{r.m[0], r.s[0], r.a[0], 0u, 0u, 0u};
+    }
+  };
   uint4 (*A2)[32] = reinterpret_cast<uint4 (*)[32]>(ws + S::oA);
   uint32_t* IX = reinterpret_cast<uint32_t*>(ws + S::oA);  // weighted items: slot r's table indices [r][lane]
   uint2* Hc = reinterpret_cast<uint2*>(ws + S::oHc);
@@ -260,7 +275,9 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
   // exact paths in the pass-list area (n > 32)
   constexpr bool RECOMP = S::RECOMP;
   uint2* Hf = reinterpret_cast<uint2*>(ws + (RECOMP ? S::oE : S::oHf));
-  uint2* H1 = reinterpret_cast<uint2*>(ws + S::oE + 8 * S::NS);
+  // recompute mode: the exact paths materialise the states of kChunk entries at a time (Hf, then H1)
+  constexpr uint32_t kChunk = RECOMP ? (uint32_t)(((S::oL - S::oE) / (WIDE ? 16 : 8)) & ~1) : (uint32_t)S::NS;
+  uint2* H1 = reinterpret_cast<uint2*>(ws + S::oE) + kChunk;
   uint8_t* Hj = ws + S::oHj;
   uint2 (*E)[32] = reinterpret_cast<uint2 (*)[32]>(ws + S::oE);
   uint2* L2 = reinterpret_cast<uint2*>(ws + S::oL);  // [parity][lane] (m, s), n <= 32
@@ -317,9 +334,13 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
     __syncwarp();
     {  // B-side rows FIX..n-1
       const uint4* s = reinterpret_cast<const uint4*>(p.rows + b * 64 + FIX);
-      uint4* d = reinterpret_cast<uint4*>(R);
+      uint4* d = reinterpret_cast<uint4*>(ws + S::oR);
       TP_CHECK(p.n - FIX <= S::NR);
-      for (int x = (int)lane; x < 2 * (p.n - FIX); x += 32) d[x] = s[x];
+      if constexpr (WIDE) {  // (m0, m1, s0, s1): the first half of each RowRec
+        for (int x = (int)lane; x < p.n - FIX; x += 32) d[x] = s[2 * x];
+      } else {
+        for (int x = (int)lane; x < 2 * (p.n - FIX); x += 32) d[x] = s[x];
+      }
     }
 
     // A side: slot k of this lane is position pbase + 32 lrow(k) + lane of
@@ -422,8 +443,9 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
 #pragma unroll
         for (int r = 0; r < V; ++r)
           if ((gl >> r) & 1u) {
-            sub_word(zl, gll, R[r].m[0], R[r].a[0]);
-            if (WIDE) sub_word(zlw, glw, R[r].m[1], R[r].a[1]);
+            const BRow rw = brow(r);
+            sub_word(zl, gll, rw.m0, rw.a0);
+            if (WIDE) sub_word(zlw, glw, rw.m1, rw.a1);
           }
         // row form on the real columns (padding columns stay H's +1)
         const uint32_t m0 = ~zl & colmask, m1 = ~zlw & colmask1;
@@ -440,8 +462,9 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
       const unsigned long long hs = sb0 ^ (sb0 >> 1);
       for (int r = FIX + V; r < p.n; ++r)
         if ((hs >> (r - FIX - V)) & 1ull) {
-          sub_word(z, g, R[r - FIX].m[0], R[r - FIX].a[0]);
-          if (WIDE) sub_word(zw, gw, R[r - FIX].m[1], R[r - FIX].a[1]);
+          const BRow rw = brow(r - FIX);
+          sub_word(z, g, rw.m0, rw.a0);
+          if (WIDE) sub_word(zw, gw, rw.m1, rw.a1);
         }
       zh = z;
       uh = pair_u2(z, g);
@@ -483,9 +506,9 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
       };
       // H of global superblock G flips row FIX + V + tz(G); it leaves iff
       // bit tz(G) + 1 of G is set
-      auto h_flip = [&](const RowRec& row, bool lv) {
-        sub_word_u(zh, uh, row.m[0], lv ? row.s[0] : row.a[0], lv ? row.a[0] : row.s[0]);
-        if (WIDE) sub_word_u(zhw, uhw, row.m[1], lv ? row.s[1] : row.a[1], lv ? row.a[1] : row.s[1]);
+      auto h_flip = [&](const BRow& row, bool lv) {
+        sub_word_u(zh, uh, row.m0, lv ? row.s0 : row.a0, lv ? row.a0 : row.s0);
+        if (WIDE) sub_word_u(zhw, uhw, row.m1, lv ? row.s1 : row.a1, lv ? row.a1 : row.s1);
       };
       const unsigned long long G0 = sb0 + kb0;
       if (nbt == (uint32_t)NBAT && (G0 & (unsigned long long)(NBAT - 1)) == 0) {
@@ -501,13 +524,13 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
             constexpr int tzt = __builtin_ctz(t + 1);
             // bit tz + 1 of G0 + t + 1: inside the batch offset unless it is bit LNB (of G0)
             const bool lv = tzt + 1 < LNB ? (((t + 1) >> (tzt + 1)) & 1u) != 0 : ((G0 >> LNB) & 1ull) != 0;
-            h_flip(R[V + tzt], lv);
+            h_flip(brow(V + tzt), lv);
           }
         });
         if (kb0 + NBAT < nsb) {
           const unsigned long long G = G0 + NBAT;
           const int tzg = tz64(G);
-          h_flip(R[V + tzg], ((G >> (tzg + 1)) & 1ull) != 0);
+          h_flip(brow(V + tzg), ((G >> (tzg + 1)) & 1ull) != 0);
         }
       } else {
 #pragma unroll 1
@@ -517,7 +540,7 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
           if (kb + 1 < nsb) {
             const unsigned long long G = sb0 + kb + 1;
             const int tzg = tz64(G);
-            h_flip(R[V + tzg], ((G >> (tzg + 1)) & 1ull) != 0);
+            h_flip(brow(V + tzg), ((G >> (tzg + 1)) & 1ull) != 0);
           }
         }
       }
@@ -549,41 +572,68 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
           sub_word_u(z, u, l.x, l.x ^ l.y, l.y);
         }
       };
-      // the exact paths read every entry's state: materialise them (Hf, H1)
-      // in the pass-list area
-      auto materialise = [&]() {
-        if constexpr (!RECOMP) return;
+      // the exact paths read their entries' states: stored (Hf), or
+      // materialised kChunk entries at a time in the pass-list area
+      auto materialise = [&](uint32_t e0, uint32_t cn) {
         __syncwarp();
-        for (uint32_t e = lane; e < L; e += 32) {
+        for (uint32_t e = lane; e < cn; e += 32) {
           uint32_t z, u, zw = 0, uw = 0;
-          entry_state(e, z, u, zw, uw);
+          entry_state(e0 + e, z, u, zw, uw);
           Hf[e] = make_uint2(z, u);
           if (WIDE) H1[e] = make_uint2(zw, uw);
         }
         __syncwarp();
       };
       if (weighted) {  // deduplicated A side: every listed step exactly, with weights
-        materialise();
-        batch_exact_weighted<FIX, KEYS, WIDE>(Hf, H1, Hj, L, Tm, IX, cnt, lane, colmask, colmask1,
-                                              p.pm + 2 * b);
+        if constexpr (!RECOMP) {
+          batch_exact_weighted<FIX, KEYS, WIDE>(Hf, H1, Hj, L, Tm, IX, cnt, lane, colmask, colmask1, p.pm + 2 * b);
+        } else {
+          for (uint32_t c0 = 0; c0 < L; c0 += kChunk) {
+            const uint32_t cc = min(kChunk, L - c0);
+            materialise(c0, cc);
+            batch_exact_weighted<FIX, KEYS, WIDE>(Hf, H1, Hj + c0, cc, Tm, IX, cnt, lane, colmask, colmask1,
+                                                  p.pm + 2 * b);
+          }
+        }
         continue;
       }
-      auto exact_list = [&](uint32_t& bev, uint32_t& bodd) {
-        materialise();
-        unsigned long long r;
-        if constexpr (WIDE) r = batch_exact_wide<FIX, KEYS>(A2, Hf, H1, Hj, L, Tm, grp, pbase, cnt, lane, spm, colmask1);
-        else r = batch_exact_packed(A2, Hf, Hj, L, lane, spm, vmask, colmask, p.n, one);
-        bev = (uint32_t)r;
-        bodd = (uint32_t)(r >> 32);
+      // list entries [ib, ib + cn) exactly
+      auto exact_range = [&](uint32_t ib, uint32_t cn, uint32_t& bev, uint32_t& bodd) {
+        if constexpr (!RECOMP) {  // stored states: one call
+          const unsigned long long r = batch_exact_packed(A2, Hf + ib, Hj + ib, cn, lane, spm, vmask, colmask, p.n, one);
+          bev = (uint32_t)r;
+          bodd = (uint32_t)(r >> 32);
+          return;
+        }
+        bev = bodd = 0;
+        for (uint32_t c0 = ib; c0 < ib + cn; c0 += kChunk) {
+          const uint32_t cc = min(kChunk, ib + cn - c0);
+          materialise(c0, cc);
+          unsigned long long r;
+          if constexpr (WIDE)
+            r = batch_exact_wide<FIX, KEYS>(A2, Hf, H1, Hj + c0, cc, Tm, grp, pbase, cnt, lane, spm, colmask1);
+          else
+            r = batch_exact_packed(A2, Hf, Hj + c0, cc, lane, spm, vmask, colmask, p.n, one);
+          bev += (uint32_t)r;
+          bodd += (uint32_t)(r >> 32);
+        }
       };
       if (dense) {
         uint32_t bev, bodd;
-        exact_list(bev, bodd);
+        exact_range(0, L, bev, bodd);
         ev += bev;
         odd += bodd;
         dense = __any_sync(FULL, bev >= (uint32_t)(K / 2) * nbt);
         continue;
       }
+      // Long lists (batches of 8 superblocks; pieces that most B states are
+      // compatible with) are filtered and verified in segments, so that a
+      // lane's pass list sees at most kSeg entries between two verifies.
+      // (Batches of up to 4 superblocks: one segment; the loop compiles away.)
+      constexpr uint32_t kSeg = 96u;
+      uint32_t ib = 0;
+      do {
+      const uint32_t ie = NBAT > 4 ? min(L, ib + kSeg) : L;
       // the packed filter over the list, three entries per iteration: the
       // three zp words of packed word w meet in one halfword-wise minimum
       // (packed_test3), so bit w of M = word w passed for one of the entries
@@ -597,14 +647,14 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
       };
       auto filter = [&](auto Wc) {
         constexpr int W = decltype(Wc)::value;
-        uint32_t i = 0;
+        uint32_t i = ib;
 #if TP_BATCH_SIX
         // two groups of three entries per iteration and record: bit w of M
         // for entries i..i+2, bit 16 + w for i+3..i+5 (the piece's common
         // widths only: the code has to stay in the instruction cache)
         if constexpr (W <= TP_BATCH_SIX && (FIX == 14 || WIDE)) {
 #pragma unroll 1
-          for (; i + 6 <= L; i += 6) {
+          for (; i + 6 <= ie; i += 6) {
             const uint4* q = reinterpret_cast<const uint4*>(Hc + i);  // i is even
             const uint4 hab = q[0], hcd = q[1], hef = q[2];
             uint32_t M = 0;
@@ -618,7 +668,7 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
         }
 #endif
 #pragma unroll 1
-        for (; i + 3 <= L; i += 3) {
+        for (; i + 3 <= ie; i += 3) {
           const uint2 ha = Hc[i], hb = Hc[i + 1], hc = Hc[i + 2];
           uint32_t M = 0;
           static_for<W>([&](auto wc) {
@@ -627,7 +677,7 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
           });
           record(M, i);
         }
-        if (i + 2 == L) {
+        if (i + 2 == ie) {
           const uint2 ha = Hc[i], hb = Hc[i + 1];
           uint32_t M = 0;
           static_for<W>([&](auto wc) {
@@ -635,7 +685,7 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
             packed_test2<(1u << w)>(Zp[w], Gp[w], ha.x, ha.y, hb.x, hb.y, M, one, cneg);
           });
           record(M, i);
-        } else if (i < L) {
+        } else if (i < ie) {
           const uint2 ha = Hc[i];
           uint32_t M = 0;
           static_for<W>([&](auto wc) {
@@ -655,13 +705,13 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
       }
       const uint32_t nemax = __reduce_max_sync(FULL, ne);
       if (nemax > (uint32_t)ECAP) {
-        // a lane's pass list overflowed (event-dense matrix): the whole list exactly
+        // a lane's pass list overflowed (event-dense matrix): the segment exactly
         __syncwarp();
         uint32_t bev, bodd;
-        exact_list(bev, bodd);
+        exact_range(ib, ie - ib, bev, bodd);
         ev += bev;
         odd += bodd;
-        dense = p.dense_ok != 0 && __any_sync(FULL, bev >= (uint32_t)(K / 2) * nbt);
+        dense = dense || (p.dense_ok != 0 && __any_sync(FULL, bev >= (uint32_t)(K / 2) * nbt));
       } else if (nemax != 0) {
         // Verify, balanced over the lanes.  The records are compacted row
         // by row into one flat list in place (row r only lands on flat
@@ -697,14 +747,14 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
             M &= M - 1;
             // bit w: entries i .. i + 2 of the record; bit 16 + w: i + 3 .. i + 5
             const uint32_t w = bm & 15u, i0 = (rec.y & 0xFFFFu) + 3u * (bm >> 4);
-            const uint32_t i1 = min(i0 + 3u, L);  // a last iteration holds one or two entries
+            const uint32_t i1 = min(i0 + 3u, ie);  // a last iteration holds one or two entries
             const uint4 a4 = A2[w][src];
             const uint32_t zk = __byte_perm(a4.x, a4.z, 0x5410), gk = __byte_perm(a4.y, a4.w, 0x5410);
             // which entries and halves passed: bit e + 16 half, branch-free
             uint32_t hit[3];
 #pragma unroll
             for (uint32_t e = 0; e < 3u; ++e) {
-              const uint2 hq = Hc[min(i0 + e, L - 1u)];
+              const uint2 hq = Hc[min(i0 + e, ie - 1u)];
               uint32_t dq, zq;
               TP_LOP3(dq, zk, gk, hq.y, 0x06);
               TP_LOP3(zq, dq, zk, hq.x, 0x09);
@@ -744,8 +794,12 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
         odd += bodd;
         // event-dense (e.g. all-ones rows): exact mode for the next batches
         // (the verify's events are spread over the lanes: the warp's total)
-        dense = p.dense_ok != 0 && __reduce_add_sync(FULL, bev) >= 4u * (uint32_t)(K / 2) * nbt;
+        dense = dense || (p.dense_ok != 0 && __reduce_add_sync(FULL, bev) >= 4u * (uint32_t)(K / 2) * nbt);
       }
+      if constexpr (NBAT <= 4) break;
+      __syncwarp();  // the segment's records are consumed
+      ib += kSeg;
+      } while (ib < L);  // segments
     }
     warp_flush(p.pm + 2 * b, ev - odd, odd, lane);
     if (bp.tested && lane == 0) {
@@ -768,13 +822,22 @@ struct BatchShape {
 #define TP_BATCH_NB_NARROW 4
 #define TP_BATCH_EC_NARROW 10
 #endif
-// the 17-row A side for n <= 32 (28 <= n <= 32; C3)
+// the 17-row A side for n <= 32 (28 <= n <= 32; C3): batches of 8 (states
+// recomputed) gain 6 % on uniform inputs but lose on C3's sparse family
+// (long lists: more segments, more pass-list overflows): 4
 #ifndef TP_BATCH_NB17
 #define TP_BATCH_NB17 4
 #define TP_BATCH_EC17 10
 #endif
-  static constexpr int NBAT = WIDE ? 4 : FIX == 17 ? TP_BATCH_NB17 : TP_BATCH_NB_NARROW;
-  static constexpr int ECAP = WIDE ? 8 : FIX == 17 ? TP_BATCH_EC17 : TP_BATCH_EC_NARROW;
+// n > 32: batches of 8 superblocks (the 16-byte rows make the room; lists of
+// ~34 steps on uniform inputs instead of ~17 halve the per-batch costs of
+// the verify: C4 1.66 -> 1.53 ms, C5 window 362 -> 327 ms)
+#ifndef TP_BATCH_NBW
+#define TP_BATCH_NBW 8
+#define TP_BATCH_ECW 6
+#endif
+  static constexpr int NBAT = WIDE ? TP_BATCH_NBW : FIX == 17 ? TP_BATCH_NB17 : TP_BATCH_NB_NARROW;
+  static constexpr int ECAP = WIDE ? TP_BATCH_ECW : FIX == 17 ? TP_BATCH_EC17 : TP_BATCH_EC_NARROW;
   // four blocks per SM: 228 KB of shared memory, 1 KB reserved per block
   static_assert(4 * (4 * BatchSmem<NBAT, ECAP, WIDE, FIX>::kWarp + 1024) <= 228 * 1024,
                 "k_walk_batch: four blocks must fit an SM");
