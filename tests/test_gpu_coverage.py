@@ -365,3 +365,30 @@ def test_table4_tool_small_scale(gpu):
     # the same call through the API gives the same tally (seed 0)
     assert rows[10]["zero_count"] == gpu.montecarlo_zero(10, rows[10]["trials"], seed=0).zero_count
     assert "summary" in recs[-1]
+
+
+def test_wide_batch_above_4096_matrices_uses_four_keys(gpu, oracle):
+    """n > 32 batches of more than 4,096 matrices take the 4-key tables (26.6 KB
+    of run starts per matrix instead of 237 KB) and so another instantiation
+    of the batched walk than single matrices and small batches (5 keys).  A
+    batch of 4,100 33x33 matrices (mostly sparse, so the traversals are
+    short on events but every piece and batch is walked): the first 48 raw
+    partials against the same matrices as a small batch (the 5-key kernel),
+    three of them against the C oracle's full 2^33 traversal."""
+    from paper_2407_20205_b200 import _kernels
+
+    n, B = 33, 4100
+    r = np.random.default_rng(3317)
+    e = ((r.random((B, n, n)) < 0.3) * r.integers(1, 3, (B, n, n))).astype(np.uint8)
+    e[:16] = r.integers(0, 3, (16, n, n))  # uniform
+    e[16] = 1                              # all-ones: weighted
+    e[17, :, 20:] = 1                      # filter-heavy
+    _kernels.walk_tested(0)
+    _, part, hist = gpu.perm_mod3_batch(e)
+    assert _kernels.walk_tested(0) > 0
+    assert hist.sum() == B
+    _, small, _ = gpu.perm_mod3_batch(e[:48])
+    assert np.array_equal(part[:48], small)
+    for k in (0, 17, 40):
+        mags, sgns = oracle.planes_from_classes(e[k])
+        assert part[k] == oracle.chunk_sum_mt(mags, sgns, n, 1, 1 << n, os.cpu_count() or 8), k
