@@ -13,23 +13,24 @@
 // pass-list votes, the verify dispatch) is paid for every 7 or 3 filter
 // iterations.  Here each superblock's compatible states are compacted into a
 // per-warp list in shared memory (ballot + prefix popcount), NBAT superblocks
-// fill one list, and the filter then runs one long counted loop over it:
+// (4; 8 for n > 32) fill one list, and the filter then runs one long counted
+// loop over it (lists of 8 superblocks in segments of 96 entries):
 //
 //   * list entry e: the doubled low 16 columns (Hc, what the filter reads,
 //     two entries = one 16-byte load), the full state (Hf, z and u words;
-//     H1 the secondary word for n > 32) and the step within the batch (Hj,
-//     whose parity is the B subset's size parity: batches start at even
-//     steps);
+//     n > 32: recomputed from the superblock's H and the lane's L when a
+//     pass needs it) and the step within the batch (Hj, whose parity is the
+//     B subset's size parity: batches start at even steps);
 //   * the filter is the packed test of tp_walk_bucket.cu (two pairs per
 //     32-bit word on 16 columns each) for three entries at a time with one
 //     zero-field test on the halfword-wise minimum of their three result
 //     words (packed_test3: 4/3 ALU ops per pair); a lane's passes (mask of
 //     words, list index of the three entries) go to its pass list E; after
 //     the loop the warp compacts the lists and verifies the passes exactly,
-//     one (record, entry) per lane and round;
+//     one record per lane and round;
 //   * a pass list that overflows, and event-dense matrices, take the exact
-//     evaluation of the whole list; deduplicated (weighted) A sides take the
-//     weighted exact walk, as in k_walk_bucket.
+//     evaluation of the segment or list; deduplicated (weighted) A sides
+//     take the weighted exact walk, as in k_walk_bucket.
 //
 // Only zero terms are skipped, so the raw partials equal chunk_sum
 // (src/_kernels.py:90-128) bit for bit.
@@ -54,10 +55,10 @@ struct BatchSmem {
   static constexpr int oR = 0;
   static constexpr int oA = align16(oR + kRow * NR);    // uint4[16][32]: full A words (slot w | slot w + 16)
   static constexpr int oHc = oA + 16 * 32 * 16;         // uint2[NS]: doubled low 16 columns (zz, uu)
-  static constexpr int oHs = oHc + 8 * NS;              // n > 32: uint4[NBAT] H of each superblock (z, u, zw, uw)
-  // n <= 32: uint2[NS] the entries' full states (z, u); n > 32 recomputes
-  // them from Hs and the L tables (entry_state) and keeps the room for a
-  // batch of 4 superblocks
+  static constexpr int oHs = oHc + 8 * NS;              // RECOMP: uint4[NBAT] H of each superblock (z, u, zw, uw)
+  // stored states: uint2[NS] the entries' full states (z, u); RECOMP
+  // recomputes them from Hs and the L tables (entry_state) and keeps the
+  // room for a longer list
   static constexpr int oHf = oHs + (RECOMP ? 16 * NBAT : 0);
   static constexpr int oHj = oHf + (RECOMP ? 0 : 8 * NS);  // uint8[NS]: step within the batch (32 t + lane)
   static constexpr int oE = align16(oHj + NS);          // uint2[ECAP + 1][32]: passes (mask, list index)
@@ -65,8 +66,9 @@ struct BatchSmem {
   // of even / odd index: uint2 (m, s) [2][32], n > 32 uint4 (m0, s0, m1, s1)
   static constexpr int oL = oE + 8 * 32 * (ECAP + 1);
   static constexpr int kWarp = align16(oL + 2 * 32 * (WIDE ? 16 : 8));
-  // n > 32: the exact paths materialise the entries' full states (Hf, H1)
-  // in the pass-list area, which they do not use
+  // RECOMP: the exact paths materialise the entries' full states (Hf, H1)
+  // in the pass-list area, which they do not use, a chunk of at least 64
+  // entries at a time
   __host__ __device__ static constexpr bool states_fit() { return !RECOMP || (WIDE ? 16 : 8) * 64 <= oL - oE; }
   // the A decode's run table (run_table) borrows [oHc, kWarp): the lists,
   // the pass list and the L tables are all written after the decode
