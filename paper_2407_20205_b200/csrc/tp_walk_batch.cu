@@ -83,6 +83,10 @@ struct BatchSmem {
 
 // Exact evaluation of list entries [0, L) against this lane's 32 slots, n <= 32
 // (dense mode and pass-list overflow).  Returns ev | odd << 32.
+// (One copy per A-side height: ptxas allocates a shared out-of-line callee
+// against all its callers, which ties the kernels' register allocation
+// together; a change in one kernel then moves the others' code.)
+template <int FIX>
 static __device__ __noinline__ unsigned long long batch_exact_packed(const uint4 (*A2)[32], const uint2* Hf,
                                                                      const uint8_t* Hj, uint32_t L, uint32_t lane,
                                                                      uint32_t spm, uint32_t vmask, uint32_t colmask,
@@ -602,7 +606,7 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
       // list entries [ib, ib + cn) exactly
       auto exact_range = [&](uint32_t ib, uint32_t cn, uint32_t& bev, uint32_t& bodd) {
         if constexpr (!RECOMP) {  // stored states: one call
-          const unsigned long long r = batch_exact_packed(A2, Hf + ib, Hj + ib, cn, lane, spm, vmask, colmask, p.n, one);
+          const unsigned long long r = batch_exact_packed<FIX>(A2, Hf + ib, Hj + ib, cn, lane, spm, vmask, colmask, p.n, one);
           bev = (uint32_t)r;
           bodd = (uint32_t)(r >> 32);
           return;
@@ -615,7 +619,7 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
           if constexpr (WIDE)
             r = batch_exact_wide<FIX, KEYS>(A2, Hf, H1, Hj + c0, cc, Tm, grp, pbase, cnt, lane, spm, colmask1);
           else
-            r = batch_exact_packed(A2, Hf, Hj + c0, cc, lane, spm, vmask, colmask, p.n, one);
+            r = batch_exact_packed<FIX>(A2, Hf, Hj + c0, cc, lane, spm, vmask, colmask, p.n, one);
           bev += (uint32_t)r;
           bodd += (uint32_t)(r >> 32);
         }
@@ -630,12 +634,22 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
       }
       // Long lists (batches of 8 superblocks; pieces that most B states are
       // compatible with) are filtered and verified in segments, so that a
-      // lane's pass list sees at most kSeg entries between two verifies.
-      // (Batches of up to 4 superblocks: one segment; the loop compiles away.)
-      constexpr uint32_t kSeg = 96u;
+      // lane's pass list sees at most kSeg entries between two verifies and
+      // rarely overflows into the exact path.
+      // The 17-row kernels (5 key columns: ~17 steps per 4 superblocks on
+      // uniform inputs, but all 128 for a piece without a zero key trit on
+      // sparse B states) run in segments; the 14-row kernel (C2) does not.
+      // TP_BATCH_SEG: entries per segment, a multiple of 6 (C3: 176.7 ms
+      // without segments, 172.4 at 66, 170.1 at 48, 169.8 at 36, 171.4 at 24).
+#ifndef TP_BATCH_SEG
+#define TP_BATCH_SEG 48
+#endif
+      static_assert(TP_BATCH_SEG % 6 == 0, "segments hold whole filter iterations");
+      constexpr bool kSegments = NBAT > 4 || FIX == 17;
+      constexpr uint32_t kSeg = (uint32_t)TP_BATCH_SEG;
       uint32_t ib = 0;
       do {
-      const uint32_t ie = NBAT > 4 ? min(L, ib + kSeg) : L;
+      const uint32_t ie = kSegments ? min(L, ib + kSeg) : L;
       // the packed filter over the list, three entries per iteration: the
       // three zp words of packed word w meet in one halfword-wise minimum
       // (packed_test3), so bit w of M = word w passed for one of the entries
@@ -798,7 +812,7 @@ __global__ void __launch_bounds__(128, 4) k_walk_batch(const BucketParamsCfg bp)
         // (the verify's events are spread over the lanes: the warp's total)
         dense = dense || (p.dense_ok != 0 && __reduce_add_sync(FULL, bev) >= 4u * (uint32_t)(K / 2) * nbt);
       }
-      if constexpr (NBAT <= 4) break;
+      if constexpr (!kSegments) break;
       __syncwarp();  // the segment's records are consumed
       ib += kSeg;
       } while (ib < L);  // segments
