@@ -39,6 +39,56 @@ __device__ __forceinline__ unsigned long long mix64s(unsigned long long z) {
   return z;
 }
 
+// TP_SMALL_SAMPLER 1: a sampled 64-bit word is handled as a whole -- its 32
+// two-bit slices are split into a low-bit and a high-bit mask, the slices
+// of value 3 are rejected by a branch-free compress of both masks (the
+// parallel-suffix method: the moves depend only on the mask and serve both),
+// and the accepted trits are appended to two bit streams (nonzero, minus)
+// from which a row takes n bits at a time (earlier trit = higher column bit:
+// one BREV).  The same trits in the same order as the reference's slice
+// loop (src/_kernels.py:212-242; rng.py:49-65), at ~6 instead of ~25
+// instructions per trit.  0: the slice loop.
+#ifndef TP_SMALL_SAMPLER
+#define TP_SMALL_SAMPLER 1
+#endif
+
+// bits 0, 2, 4, .. of x gathered into the low 16 bits
+__device__ __forceinline__ uint32_t even_bits16(uint32_t x) {
+  x &= 0x55555555u;
+  x = (x | (x >> 1)) & 0x33333333u;
+  x = (x | (x >> 2)) & 0x0F0F0F0Fu;
+  x = (x | (x >> 4)) & 0x00FF00FFu;
+  x = (x | (x >> 8)) & 0x0000FFFFu;
+  return x;
+}
+
+// a and b compressed by mask m (the bits of a, b under the 1-bits of m moved
+// to the low end, order kept): Hacker's Delight 7-4, the move masks shared
+__device__ __forceinline__ void compress2(uint32_t m, uint32_t& a, uint32_t& b) {
+  a &= m;
+  b &= m;
+  uint32_t mk = ~m << 1;
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    uint32_t mp = mk ^ (mk << 1);
+    mp ^= mp << 2;
+    mp ^= mp << 4;
+    mp ^= mp << 8;
+    mp ^= mp << 16;
+    const uint32_t mv = mp & m;
+    m = (m ^ mv) | (mv >> (1 << i));
+    uint32_t t = a & mv;
+    a = (a ^ t) | (t >> (1 << i));
+    t = b & mv;
+    b = (b ^ t) | (t >> (1 << i));
+    mk &= ~mp;
+  }
+}
+
+// (Events are rare from n = 12, (2/3)^n < 1 % of the steps, but putting their
+// accounting behind a warp vote instead of predicating it into every step
+// measured 22 % slower at n = 12..15: the vote and branch per step cost
+// more than the ~4 predicated instructions and break the unrolled schedule.)
 __global__ void __launch_bounds__(kSmallThreads) k_small(SmallParams p) {
   __shared__ uint32_t Sm[kSmallMaxN][kSmallThreads], Ss[kSmallMaxN][kSmallThreads], Sa[kSmallMaxN][kSmallThreads];
   const int tid = threadIdx.x;
@@ -65,6 +115,36 @@ __global__ void __launch_bounds__(kSmallThreads) k_small(SmallParams p) {
     } else {
       const unsigned long long golden = 0x9E3779B97F4A7C15ull;
       unsigned long long state = mix64s(mix64s(p.seed) ^ ((unsigned long long)(p.t0 + b + 1) * golden));
+#if TP_SMALL_SAMPLER
+      // bit streams of the accepted trits, earliest at bit 0: nonzero, minus
+      unsigned long long sm = 0, ss = 0;
+      int have = 0;
+      const uint32_t rowmask = (1u << n) - 1u;  // n <= kSmallMaxN < 32
+      for (int t = 0; t < n; ++t) {
+        while (have < n) {  // < 15 + 32 bits in the streams
+          state += golden;
+          const unsigned long long word = mix64s(state);
+          const uint32_t wl = (uint32_t)word, wh = (uint32_t)(word >> 32);
+          uint32_t lo = even_bits16(wl) | (even_bits16(wh) << 16);            // bit j: low bit of slice j
+          uint32_t hi = even_bits16(wl >> 1) | (even_bits16(wh >> 1) << 16);  // high bit of slice j
+          const uint32_t acc = ~(lo & hi);                                    // slices of value 0, 1, 2
+          uint32_t mg = lo | hi, sg = hi;                                     // nonzero; value 2 = -1
+          compress2(acc, mg, sg);
+          sm |= (unsigned long long)mg << have;
+          ss |= (unsigned long long)sg << have;
+          have += __popc(acc);
+        }
+        // the row's n trits: trit k -> column k -> bit n-1-k
+        const uint32_t m = __brev((uint32_t)sm & rowmask) >> (32 - n);
+        const uint32_t s = __brev((uint32_t)ss & rowmask) >> (32 - n);
+        sm >>= n;
+        ss >>= n;
+        have -= n;
+        Sm[t][tid] = m;
+        Ss[t][tid] = s;
+        Sa[t][tid] = m ^ s;
+      }
+#else
       unsigned long long word = 0;
       int pairs = 0;
       for (int t = 0; t < n; ++t) {
@@ -90,6 +170,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small(SmallParams p) {
         Ss[t][tid] = s;
         Sa[t][tid] = m ^ s;
       }
+#endif
     }
   } else {
     for (int t = 0; t < n; ++t) Sm[t][tid] = Ss[t][tid] = Sa[t][tid] = 0;
