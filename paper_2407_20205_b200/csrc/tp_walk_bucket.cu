@@ -240,17 +240,17 @@ __global__ void __launch_bounds__(256) k_bucket_group(const RowRec* rows, int n,
     reinterpret_cast<uint16_t*>(Tm)[k] = (uint16_t)offs[k / (NB + 1)][k % (NB + 1)];
   for (uint32_t g = tid; g < (uint32_t)NB; g += NT) {
     uint32_t c = 0;
-    for (uint32_t a = 0; a < (uint32_t)NB; ++a) c += kcnt[a] * kcnt[NB + pat_sub<KEYS>(g, a)];
-    bsize[g] = c;
-    if (WIDE) {  // run starts of bucket g (the same sum, kept per run)
+    if (WIDE) {  // run starts of bucket g (the partial sums, kept per run)
       uint32_t* rs = reinterpret_cast<uint32_t*>(Tm + T::kRun) + g * (NB + 1);
-      uint32_t o = 0;
       for (uint32_t a = 0; a < (uint32_t)NB; ++a) {
-        rs[a] = o;
-        o += kcnt[a] * kcnt[NB + pat_sub<KEYS>(g, a)];
+        rs[a] = c;
+        c += kcnt[a] * kcnt[NB + pat_sub<KEYS>(g, a)];
       }
-      rs[NB] = o;
+      rs[NB] = c;
+    } else {
+      for (uint32_t a = 0; a < (uint32_t)NB; ++a) c += kcnt[a] * kcnt[NB + pat_sub<KEYS>(g, a)];
     }
+    bsize[g] = c;
   }
   uint32_t* wout = reinterpret_cast<uint32_t*>(Tm + T::kWt);
 #pragma unroll
